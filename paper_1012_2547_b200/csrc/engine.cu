@@ -1,0 +1,837 @@
+// engine.cu -- sm_100a kernels and the C ABI of the B200 exact matcher.
+//
+// See scan.h for the kernel pipeline and DESIGN.md for the data layout,
+// roofline and per-family byte budgets.  Reference semantics:
+// pkg/src/matchbench/core.py:139-161 (all start positions, overlapping,
+// ascending; m > n -> none).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+#include "scan.h"
+
+namespace mb {
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+// TMA 1D bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// look-back flag word: [epoch:24][status:2][value:38]
+constexpr uint64_t ST_AGG = 1, ST_INCL = 2;
+__device__ __forceinline__ uint64_t pack_state(uint32_t epoch, uint64_t st, uint64_t val) {
+  return ((uint64_t)epoch << 40) | (st << 38) | (val & ((1ULL << 38) - 1));
+}
+
+// ----------------------------------------------------------- SWAR primitives
+// exact per-byte zero flags (0x80 in each zero byte) -> 4-bit mask
+__device__ __forceinline__ uint32_t zero_bytes4(uint32_t x) {
+  uint32_t y = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);
+  return ((y >> 7) * 0x01020408u) >> 24 & 0xFu;
+}
+__device__ __forceinline__ uint32_t shr8(uint32_t lo, uint32_t hi, int k) {
+  return __funnelshift_r(lo, hi, 8 * k);
+}
+
+// -------------------------------------------------------------- filters
+// Each filter looks at the 16 staged bytes of one lane (w[0..3]) plus the
+// next word (w[4]) and returns the candidate mask over the lane's 16 bitmap
+// positions.  `any` is the cheap existence test; `mask` the exact bit set.
+
+// K1 / m <= 3: byte d of x_k is zero iff t[v..v+m) == p (v = 4k+d).
+struct FiltSWAR {
+  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
+    uint32_t x[4], acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      uint32_t v = w[k] ^ P.G[0];
+      if (P.m >= 2) v |= shr8(w[k], w[k + 1], 1) ^ P.G[1];
+      if (P.m >= 3) v |= shr8(w[k], w[k + 1], 2) ^ P.G[2];
+      x[k] = v;
+      acc |= (v - 0x01010101u) & ~v;
+    }
+    if (!(acc & 0x80808080u)) return 0;
+    uint32_t mk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) mk |= zero_bytes4(x[k]) << (4 * k);
+    return mk;
+  }
+};
+
+// K1 / 4 <= m <= 6: 32-bit window at every byte offset vs the anchor word.
+struct FiltWIN4 {
+  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
+    const uint32_t g = P.G[0];
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      hit |= (w[k] == g) | (shr8(w[k], w[k + 1], 1) == g) | (shr8(w[k], w[k + 1], 2) == g) |
+             (shr8(w[k], w[k + 1], 3) == g);
+    }
+    if (!hit) return 0;
+    uint32_t mk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+      for (int d = 0; d < 4; d++)
+        if (shr8(w[k], w[k + 1], d) == g) mk |= 1u << (4 * k + d);
+    return mk;
+  }
+};
+
+// K1/K3 / m >= 7: every occurrence contains one 4-aligned text word inside its
+// 7-byte anchor window [a, a+7); that word equals p[a+j .. a+j+4) for exactly
+// one j in 0..3.  Word k matching G_j marks bitmap position 4k + 3 - j.
+struct FiltALIGNED {
+  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
+    if (!hit) return 0;
+    uint32_t mk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (w[k] == P.G[j]) mk |= 1u << (4 * k + 3 - j);
+    return mk;
+  }
+};
+
+// ------------------------------------------------------------ verification
+// Direct window compare in shared memory (core.py:131-136 match_at).
+__device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* pat, int m) {
+  for (int k = 0; k < m; k++)
+    if (s[k] != pat[k]) return false;
+  return true;
+}
+
+// Break bitmap of the tile: bit y set iff t[y] != t[y + per] (y relative to
+// the tile's first start position).  nbw[k] = first break at or after word k.
+__device__ void build_breaks(const uint8_t* Y0, int per, int nwords, uint32_t* brk, int32_t* nbw) {
+  for (int k = threadIdx.x; k < nwords; k += NT) {
+    const uint8_t* q = Y0 + 32 * k;
+    uint32_t bits = 0;
+#pragma unroll 8
+    for (int i = 0; i < 32; i++) bits |= (uint32_t)(q[i] != q[i + per]) << i;
+    brk[k] = bits;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int seg = (nwords + 31) / 32;
+    const int lo = lane * seg, hi = min(nwords, lo + seg);
+    int first = 0x7fffffff;
+    for (int k = hi - 1; k >= lo; k--)
+      if (brk[k]) first = 32 * k + __ffs(brk[k]) - 1;
+    // exclusive suffix-min over lanes
+    int suf = first;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int o = __shfl_down_sync(0xffffffffu, suf, d);
+      if (lane + d < 32) suf = min(suf, o);
+    }
+    int excl = __shfl_down_sync(0xffffffffu, suf, 1);
+    if (lane == 31) excl = 0x7fffffff;
+    int cur = excl;
+    for (int k = hi - 1; k >= lo; k--) {
+      if (brk[k]) cur = 32 * k + __ffs(brk[k]) - 1;
+      nbw[k] = cur;
+    }
+    if (lane == 0) nbw[nwords] = 0x7fffffff;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- kernel
+template <class Filt>
+__global__ void __launch_bounds__(NT) scan_kernel(const ScanParams P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* stages = smem;
+  uint8_t* tail = smem + STAGES * P.stage_bytes;
+  uint64_t* bars = (uint64_t*)(tail + SM_BARS);
+  int64_t* stage_tk = (int64_t*)(tail + SM_TK);
+  uint32_t* bm = (uint32_t*)(tail + SM_BM);
+  uint32_t* brk = (uint32_t*)(tail + SM_BRK);
+  int32_t* nbw = (int32_t*)(tail + SM_BRK + 4 * P.brk_words);
+  int64_t* red = (int64_t*)(tail + SM_BRK + 8 * P.brk_words + 16);  // per-warp slots + [32] broadcast
+  uint8_t* spat = (uint8_t*)(red + 40);                               // pattern copy
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  auto issue = [&](int s) {  // thread 0 only
+    unsigned long long tk = atomicAdd(P.ticket, 1ULL);
+    if ((int64_t)tk >= P.total_tickets) {
+      stage_tk[s] = -1;
+      return;
+    }
+    stage_tk[s] = (int64_t)tk;
+    int64_t tau = (int64_t)tk % P.ntiles;
+    int64_t start = tau * TILE - P.pre;
+    int64_t end = tau * TILE + TILE + P.post;
+    int64_t cs = start < 0 ? 0 : start;
+    int64_t ce = end > P.nv16 ? P.nv16 : end;
+    uint32_t bytes = ce > cs ? (uint32_t)(ce - cs) : 0u;
+    uint8_t* dst = stages + s * P.stage_bytes + (cs - start);
+    mbar_expect_tx(&bars[s], bytes);
+    if (bytes) bulk_g2s(dst, P.text + cs, bytes, &bars[s]);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; s++) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < STAGES; s++) issue(s);
+  }
+  __syncthreads();
+
+  const int64_t obase = P.out_base ? *P.out_base : 0;
+  int cur_k = -1;
+  for (int it = 0;; it++) {
+    const int s = it % STAGES;
+    const int64_t tk = stage_tk[s];
+    if (tk < 0) break;
+    const int k = (int)(tk / P.ntiles);
+    const int64_t tau = tk % P.ntiles;
+    const int64_t B0 = tau * TILE;
+    const PatDev pd = P.pats[k];
+    if (k != cur_k) {  // stage this pattern's bytes (used after the next barrier)
+      for (int i = tid; i < pd.m; i += NT) spat[i] = pd.bytes[i];
+      cur_k = k;
+    }
+    // valid bitmap range for this pattern: b - delta - off in [0, n - m]
+    const int64_t blo = P.off + pd.delta;
+    const int64_t bhi = P.off + pd.delta + P.n - pd.m;  // inclusive (may be < blo)
+    mbar_wait(&bars[s], (uint32_t)(it / STAGES) & 1u);
+    const uint8_t* S = stages + s * P.stage_bytes + P.pre;  // S[c] = virtual byte B0 + c
+
+    // ---- filter phase
+    bool anyc = false;
+#pragma unroll
+    for (int r = 0; r < ROUNDS; r++) {
+      const int c = warp * (ROUNDS * 512) + r * 512 + lane * 16;
+      uint4 X = *reinterpret_cast<const uint4*>(S + c);
+      uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
+      uint32_t mk = Filt::run(w, pd);
+      const int64_t b = B0 + c;
+      if (b < blo || b + 15 > bhi) {  // boundary chunk: keep only valid positions
+        uint32_t vm = 0;
+        for (int i = 0; i < 16; i++)
+          if (b + i >= blo && b + i <= bhi) vm |= 1u << i;
+        mk &= vm;
+      }
+      anyc |= (mk != 0);
+      uint32_t other = __shfl_down_sync(0xffffffffu, mk, 1);
+      if (!(lane & 1)) bm[c >> 5] = mk | (other << 16);
+    }
+    const int any_tile = __syncthreads_or(anyc);
+
+    // ---- verify phase
+    if (any_tile && !pd.exact) {
+      const int m = (int)pd.m;
+      const uint8_t* Y0 = S - pd.delta;  // Y0[b_local] = text byte at start position of bit b_local
+      if (pd.periodic) {
+        const int nwords = (TILE + pd.L + 31) / 32;
+        build_breaks(Y0, pd.per, nwords, brk, nbw);
+      }
+      for (int wi = 2 * tid; wi < 2 * tid + 2; wi++) {
+        uint32_t cw = bm[wi], mw = 0;
+        while (cw) {
+          const int i = __ffs(cw) - 1;
+          cw &= cw - 1;
+          const int rel = 32 * wi + i;
+          bool ok;
+          if (pd.periodic) {
+            ok = verify_direct(Y0 + rel, spat, pd.per);
+            if (ok) {
+              const uint32_t x = brk[rel >> 5] >> (rel & 31);
+              const int nb = x ? rel + __ffs(x) - 1 : nbw[(rel >> 5) + 1];
+              ok = nb >= rel + pd.L;
+            }
+          } else {
+            ok = verify_direct(Y0 + rel, spat, m);
+          }
+          if (ok) mw |= 1u << i;
+        }
+        bm[wi] = mw;
+      }
+      __syncthreads();
+    }
+
+    // ---- count
+    int64_t tile_cnt = 0;
+    if (any_tile) {
+      uint32_t c2 = __popc(bm[2 * tid]) + __popc(bm[2 * tid + 1]);
+      uint32_t ws = __reduce_add_sync(0xffffffffu, c2);
+      if (lane == 0) red[warp] = ws;
+      __syncthreads();
+      for (int q = 0; q < NWARP; q++) tile_cnt += red[q];
+    }
+
+    // ---- decoupled look-back (warp 0): exclusive prefix over all tickets < tk
+    if (warp == 0) {
+      int64_t excl = 0;
+      if (tk == 0) {
+        if (lane == 0) st_relaxed(&P.state[0], pack_state(P.epoch, ST_INCL, (uint64_t)tile_cnt));
+      } else {
+        if (lane == 0) st_relaxed(&P.state[tk], pack_state(P.epoch, ST_AGG, (uint64_t)tile_cnt));
+        int64_t j = tk - 1;
+        while (true) {
+          const int64_t idx = j - lane;
+          uint64_t v;
+          if (idx < 0) {
+            v = pack_state(P.epoch, ST_INCL, 0);
+          } else {
+            int spins = 0;
+            while (true) {
+              v = ld_relaxed(&P.state[idx]);
+              if ((uint32_t)(v >> 40) == P.epoch && ((v >> 38) & 3)) break;
+              if (++spins > 8) __nanosleep(32);
+            }
+          }
+          const uint64_t st = (v >> 38) & 3;
+          const int64_t val = (int64_t)(v & ((1ULL << 38) - 1));
+          const uint32_t incl = __ballot_sync(0xffffffffu, st == ST_INCL);
+          if (incl) {
+            const int first = __ffs(incl) - 1;
+            int64_t contrib = lane <= first ? val : 0;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
+            excl += contrib;
+            break;
+          }
+          int64_t contrib = val;
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
+          excl += contrib;
+          j -= 32;
+        }
+        if (lane == 0) st_relaxed(&P.state[tk], pack_state(P.epoch, ST_INCL, (uint64_t)(excl + tile_cnt)));
+      }
+      if (lane == 0) {
+        red[32] = excl;
+        if (tau == P.ntiles - 1) P.offsets_plus1[k] = obase + excl + tile_cnt;
+      }
+    }
+    __syncthreads();
+
+    // ---- expansion: ascending positions at out[excl + ...]
+    if (tile_cnt > 0 && P.out) {
+      const int64_t excl = obase + red[32];
+      const uint32_t w0 = bm[2 * tid], w1 = bm[2 * tid + 1];
+      const uint32_t c2 = __popc(w0) + __popc(w1);
+      uint32_t inc = c2;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+      if (lane == 31) red[warp] = inc;  // safe: red[0..7] no longer read
+      __syncthreads();
+      int64_t base = excl;
+      for (int q = 0; q < warp; q++) base += red[q];
+      base += inc - c2;
+      const int64_t pos0 = B0 + 64 * tid - pd.delta - P.off;
+      uint64_t bits = ((uint64_t)w1 << 32) | w0;
+      while (bits) {
+        const int i = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        if (base < P.cap) P.out[base] = pos0 + i;
+        base++;
+      }
+    }
+    __syncthreads();  // stage s, bm, red free
+    if (tid == 0) issue(s);
+  }
+}
+
+// K0: byte histogram (Text.alphabet_size, core.py:42-44)
+__global__ void hist_kernel(const uint8_t* t, int64_t n, unsigned long long* hist) {
+  __shared__ unsigned int h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(&h[t[i]], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+
+}  // namespace mb
+
+// ===================================================================== C ABI
+using namespace mb;
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  return fail(MB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_TRY(x)                               \
+  do {                                            \
+    cudaError_t e_ = (x);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
+  } while (0)
+
+struct mb_plan {
+  PlanHost h;
+  // device copy, uploaded on first use (plans are creatable without a GPU so
+  // the host tables can be inspected anywhere); guarded for shared use
+  mutable std::mutex mu;
+  mutable uint8_t* d_bytes = nullptr;
+  mutable PatDev* d_dev = nullptr;
+  mutable int device = -1;
+};
+
+// Upload the plan to the current device once; returns the device PatDev.
+static int plan_device(const mb_plan* p, const PatDev** out) {
+  std::lock_guard<std::mutex> g(p->mu);
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (p->d_dev && p->device == dev) {
+    *out = p->d_dev;
+    return MB_OK;
+  }
+  if (p->d_dev) {  // used from another device: re-upload there
+    cudaFree(p->d_bytes);
+    cudaFree(p->d_dev);
+    p->d_bytes = nullptr;
+    p->d_dev = nullptr;
+  }
+  if (cudaMalloc(&p->d_bytes, p->h.m + 16) != cudaSuccess) return fail(MB_ENOMEM, "plan bytes alloc");
+  if (cudaMalloc(&p->d_dev, sizeof(PatDev)) != cudaSuccess) {
+    cudaFree(p->d_bytes);
+    p->d_bytes = nullptr;
+    return fail(MB_ENOMEM, "plan params alloc");
+  }
+  CUDA_TRY(cudaMemcpy(p->d_bytes, p->h.pat.data(), p->h.m, cudaMemcpyHostToDevice));
+  PatDev d = p->h.dev;
+  d.bytes = p->d_bytes;
+  CUDA_TRY(cudaMemcpy(p->d_dev, &d, sizeof(PatDev), cudaMemcpyHostToDevice));
+  p->device = dev;
+  *out = p->d_dev;
+  return MB_OK;
+}
+
+struct mb_ctx {
+  int device = 0;
+  int nsm = 0;
+  uint64_t* state = nullptr;
+  int64_t state_cap = 0;
+  uint32_t epoch = 0;
+  unsigned long long* ticket = nullptr;
+  PatDev* d_pats = nullptr;
+  int64_t pats_cap = 0;
+  std::vector<PatDev> h_pats;
+  // host-entry buffers
+  uint8_t* d_text = nullptr;
+  int64_t text_cap = 0;
+  int64_t* d_out = nullptr;
+  int64_t out_cap = 0;
+  int64_t* d_offs = nullptr;
+  int64_t offs_cap = 0;
+  std::vector<mb_plan*> tmp_plans;
+  cudaStream_t stream = nullptr;
+};
+
+extern "C" {
+
+const char* mb_last_error(void) { return g_err.c_str(); }
+const char* mb_version(void) { return "matchb200 0.1.0 (sm_100a)"; }
+int64_t mb_launch_count(void) { return g_launches.load(); }
+
+int mb_plan_create(const uint8_t* h_pattern, int64_t m, const mb_plan_opts* opts, mb_plan** out) {
+  if (!out) return fail(MB_EINVAL, "null out");
+  *out = nullptr;
+  if (m < 1) return fail(MB_EINVAL, "pattern must have length >= 1");
+  if (!h_pattern) return fail(MB_EINVAL, "null pattern");
+  mb_plan* p = new mb_plan();
+  std::string err;
+  int rc = build_plan(h_pattern, m, opts, &p->h, &err);
+  if (rc) {
+    delete p;
+    return fail(rc, err);
+  }
+  if (p->h.family == MB_FAM_SHIFTOR) {
+    delete p;
+    return fail(MB_EINVAL, "shift-or family not built in this version");
+  }
+  *out = p;
+  return MB_OK;
+}
+
+void mb_plan_destroy(mb_plan* p) {
+  if (!p) return;
+  cudaFree(p->d_bytes);
+  cudaFree(p->d_dev);
+  delete p;
+}
+
+int mb_plan_info(const mb_plan* p, mb_plan_info_t* info) {
+  if (!p || !info) return fail(MB_EINVAL, "null argument");
+  info->m = p->h.m;
+  info->family = p->h.family;
+  info->anchor = p->h.anchor;
+  info->delta = p->h.dev.delta;
+  info->period = p->h.period;
+  info->periodic = p->h.dev.periodic;
+  return MB_OK;
+}
+
+int mb_plan_horspool(const mb_plan* p, int64_t* o) {
+  if (!p || !o) return fail(MB_EINVAL, "null argument");
+  memcpy(o, p->h.hor, sizeof(p->h.hor));
+  return MB_OK;
+}
+int mb_plan_sunday(const mb_plan* p, int64_t* o) {
+  if (!p || !o) return fail(MB_EINVAL, "null argument");
+  memcpy(o, p->h.sun, sizeof(p->h.sun));
+  return MB_OK;
+}
+int mb_plan_fwd_masks(const mb_plan* p, uint64_t* o, int64_t words) {
+  if (!p || !o || words < 1) return fail(MB_EINVAL, "bad argument");
+  forward_masks(p->h.pat.data(), p->h.m, o, words);
+  return MB_OK;
+}
+int mb_plan_kmp(const mb_plan* p, int64_t* o) {
+  if (!p || !o) return fail(MB_EINVAL, "null argument");
+  memcpy(o, p->h.kmp.data(), sizeof(int64_t) * (p->h.m + 1));
+  return MB_OK;
+}
+int mb_plan_gram_hash(const mb_plan* p, int q, uint32_t* o) {
+  if (!p || !o) return fail(MB_EINVAL, "null argument");
+  if (q != 3 && q != 5 && q != 8) return fail(MB_EINVAL, "q must be one of (3, 5, 8)");
+  if (p->h.m < q) return fail(MB_EINVAL, "m < q");
+  for (int64_t i = 0; i + q <= p->h.m; i++) o[i] = gram_hash(p->h.pat.data(), i, q);
+  return MB_OK;
+}
+
+int mb_ctx_create(int device, mb_ctx** out) {
+  if (!out) return fail(MB_EINVAL, "null out");
+  *out = nullptr;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(MB_EINVAL, "bad device index");
+  CUDA_TRY(cudaSetDevice(device));
+  mb_ctx* c = new mb_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMalloc(&c->ticket, sizeof(unsigned long long)) != cudaSuccess) {
+    delete c;
+    return fail(MB_ENOMEM, "ticket alloc");
+  }
+  *out = c;
+  return MB_OK;
+}
+
+void mb_ctx_destroy(mb_ctx* c) {
+  if (!c) return;
+  cudaFree(c->state);
+  cudaFree(c->ticket);
+  cudaFree(c->d_pats);
+  cudaFree(c->d_text);
+  cudaFree(c->d_out);
+  cudaFree(c->d_offs);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // extern "C"
+
+template <class F>
+static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
+                       int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, const int64_t* out_base,
+                       cudaStream_t st) {
+  ScanParams P;
+  memset(&P, 0, sizeof(P));
+  uintptr_t addr = (uintptr_t)d_text;
+  P.text = (const uint8_t*)(addr & ~(uintptr_t)15);
+  P.off = (int64_t)(addr & 15);
+  P.n = n;
+  P.nv16 = (P.off + n + 15) & ~(int64_t)15;
+  int64_t nbits = 0;
+  int pre = 0, post = 0, maxL = 0;
+  int64_t maxm = 1;
+  for (int k = 0; k < K; k++) {
+    const PatDev& d = h_pats[k];
+    maxm = std::max<int64_t>(maxm, d.m);
+    if (d.periodic) maxL = std::max(maxL, d.L);
+    if (d.m <= n) nbits = std::max<int64_t>(nbits, P.off + d.delta + n - d.m + 1);
+    pre = std::max(pre, d.pre);
+    post = std::max(post, d.post);
+  }
+  if (nbits == 0) {  // every pattern longer than the text: offsets stay at the base
+    if (out_base) {
+      for (int k = 0; k < K; k++)
+        CUDA_TRY(cudaMemcpyAsync(offsets_plus1 + k, out_base, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    } else {
+      CUDA_TRY(cudaMemsetAsync(offsets_plus1, 0, sizeof(int64_t) * K, st));
+    }
+    return MB_OK;
+  }
+  P.ntiles = (nbits + TILE - 1) / TILE;
+  P.total_tickets = P.ntiles * K;
+  P.pats = d_pats;
+  P.K = K;
+  P.pre = pre;
+  P.post = post;
+  P.stage_bytes = (pre + TILE + post + 127) & ~127;
+  P.brk_words = (((TILE + maxL + 63) / 32) + 3) & ~3;
+  P.pat_cap = (int)((maxm + 15) & ~15) + 16;
+  if (P.total_tickets > c->state_cap || c->epoch >= (1u << 24) - 1) {
+    if (P.total_tickets > c->state_cap) {
+      cudaFree(c->state);
+      c->state = nullptr;
+      int64_t ncap = std::max<int64_t>(P.total_tickets, 1 << 16);
+      if (cudaMalloc(&c->state, sizeof(uint64_t) * ncap) != cudaSuccess) {
+        c->state_cap = 0;
+        return fail(MB_ENOMEM, "look-back state alloc");
+      }
+      c->state_cap = ncap;
+    }
+    CUDA_TRY(cudaMemsetAsync(c->state, 0, sizeof(uint64_t) * c->state_cap, st));
+    c->epoch = 0;
+  }
+  P.state = c->state;
+  P.epoch = ++c->epoch;
+  P.ticket = c->ticket;
+  P.out = d_out;
+  P.cap = d_out ? cap : 0;
+  P.offsets_plus1 = offsets_plus1;
+  P.out_base = out_base;
+  CUDA_TRY(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned long long), st));
+
+  size_t smem = (size_t)STAGES * P.stage_bytes + SM_BRK + 8 * P.brk_words + 16 + 8 * 40 + P.pat_cap;
+  static std::mutex mu;
+  static bool attr_done = false;
+  static int per_sm_cache[4] = {0, 0, 0, 0};  // keyed by stage-size class
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!attr_done) {
+      CUDA_TRY(cudaFuncSetAttribute(scan_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr_done = true;
+    }
+    int cls = smem <= 70000 ? 0 : smem <= 76000 ? 1 : smem <= 82000 ? 2 : 3;
+    if (!per_sm_cache[cls] || cls == 3) {
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_kernel<F>, NT, smem));
+      per_sm_cache[cls] = per_sm;
+    }
+    per_sm = per_sm_cache[cls];
+  }
+  if (per_sm < 1) return fail(MB_ECUDA, "scan kernel does not fit on an SM");
+  int64_t grid = std::min<int64_t>(P.total_tickets, (int64_t)c->nsm * per_sm);
+  scan_kernel<F><<<(int)grid, NT, smem, st>>>(P);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+static int dispatch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
+                    int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, const int64_t* out_base,
+                    cudaStream_t st) {
+  switch (h_pats[0].family) {
+    case MB_FAM_SWAR: return launch_scan<FiltSWAR>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
+    case MB_FAM_WIN4: return launch_scan<FiltWIN4>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
+    case MB_FAM_ALIGNED:
+      return launch_scan<FiltALIGNED>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
+  }
+  return fail(MB_EINVAL, "unknown kernel family");
+}
+
+extern "C" {
+
+int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64_t* d_out, int64_t cap,
+            int64_t* d_count, void* stream) {
+  if (!c || !p || !d_count) return fail(MB_EINVAL, "null argument");
+  if (n < 0 || cap < 0) return fail(MB_EINVAL, "negative size");
+  if (n > 0 && !d_text) return fail(MB_EINVAL, "null text");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->h.m > n) {
+    CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(int64_t), st));
+    return MB_OK;
+  }
+  const PatDev* dd = nullptr;
+  int rc = plan_device(p, &dd);
+  if (rc) return rc;
+  return dispatch(c, dd, &p->h.dev, 1, d_text, n, d_out, cap, d_count, nullptr, st);
+}
+
+int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* d_text, int64_t n,
+                  int64_t* d_out, int64_t cap, int64_t* d_offsets, void* stream) {
+  if (!c || !plans || K < 1 || !d_offsets) return fail(MB_EINVAL, "bad argument");
+  if (n < 0 || cap < 0) return fail(MB_EINVAL, "negative size");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
+  // group consecutive runs of the same family into one launch each; the
+  // look-back ticket order makes each group's output CSR-contiguous, so the
+  // groups chain through d_offsets.
+  c->h_pats.resize(K);
+  for (int k = 0; k < K; k++) {
+    if (!plans[k]) return fail(MB_EINVAL, "null plan in batch");
+    const PatDev* dd = nullptr;
+    int rc = plan_device(plans[k], &dd);
+    if (rc) return rc;
+    c->h_pats[k] = plans[k]->h.dev;
+    c->h_pats[k].bytes = plans[k]->d_bytes;
+  }
+  if (K > c->pats_cap) {
+    cudaFree(c->d_pats);
+    c->d_pats = nullptr;
+    if (cudaMalloc(&c->d_pats, sizeof(PatDev) * K) != cudaSuccess) {
+      c->pats_cap = 0;
+      return fail(MB_ENOMEM, "batch params alloc");
+    }
+    c->pats_cap = K;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice, st));
+  int k0 = 0;
+  while (k0 < K) {
+    int k1 = k0 + 1;
+    while (k1 < K && c->h_pats[k1].family == c->h_pats[k0].family) k1++;
+    // group g starts where group g-1 ended: d_offsets[k0] is its output base
+    int rc = dispatch(c, c->d_pats + k0, c->h_pats.data() + k0, k1 - k0, d_text, n, d_out, cap,
+                      d_offsets + 1 + k0, d_offsets + k0, st);
+    if (rc) return rc;
+    k0 = k1;
+  }
+  return MB_OK;
+}
+
+int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, void* stream) {
+  if (!c || !d_hist) return fail(MB_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(d_hist, 0, 256 * sizeof(int64_t), st));
+  if (n <= 0) return MB_OK;
+  int64_t blocks = std::min<int64_t>((n + 4095) / 4096, (int64_t)c->nsm * 8);
+  hist_kernel<<<(int)blocks, 256, 0, st>>>(d_text, n, (unsigned long long*)d_hist);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+static int ensure_host_bufs(mb_ctx* c, int64_t n, int64_t outcap, int64_t nofs) {
+  if (!c->stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  if (n > c->text_cap) {
+    cudaFree(c->d_text);
+    c->d_text = nullptr;
+    if (cudaMalloc(&c->d_text, n + 16) != cudaSuccess) {
+      c->text_cap = 0;
+      return fail(MB_ENOMEM, "text buffer alloc");
+    }
+    c->text_cap = n;
+  }
+  if (outcap > c->out_cap) {
+    cudaFree(c->d_out);
+    c->d_out = nullptr;
+    if (cudaMalloc(&c->d_out, sizeof(int64_t) * outcap) != cudaSuccess) {
+      c->out_cap = 0;
+      return fail(MB_ENOMEM, "output buffer alloc");
+    }
+    c->out_cap = outcap;
+  }
+  if (nofs > c->offs_cap) {
+    cudaFree(c->d_offs);
+    c->d_offs = nullptr;
+    if (cudaMalloc(&c->d_offs, sizeof(int64_t) * nofs) != cudaSuccess) {
+      c->offs_cap = 0;
+      return fail(MB_ENOMEM, "offsets alloc");
+    }
+    c->offs_cap = nofs;
+  }
+  return MB_OK;
+}
+
+int mb_search_batch_host(mb_ctx* c, const uint8_t* const* h_patterns, const int64_t* ms, int K,
+                         const uint8_t* h_text, int64_t n, int64_t* h_out, int64_t cap, int64_t* h_offsets) {
+  if (!c || !h_patterns || !ms || K < 1 || !h_offsets) return fail(MB_EINVAL, "bad argument");
+  if (n < 0 || cap < 0 || (n > 0 && !h_text)) return fail(MB_EINVAL, "bad text");
+  std::vector<mb_plan*> plans(K, nullptr);
+  auto cleanup = [&]() {
+    for (auto* p : plans) mb_plan_destroy(p);
+  };
+  for (int k = 0; k < K; k++) {
+    int rc = mb_plan_create(h_patterns[k], ms[k], nullptr, &plans[k]);
+    if (rc) {
+      cleanup();
+      return rc;
+    }
+  }
+  int rc = ensure_host_bufs(c, n, std::max<int64_t>(cap, 1), K + 1);
+  if (rc) {
+    cleanup();
+    return rc;
+  }
+  cudaStream_t st = c->stream;
+  if (n > 0) cudaMemcpyAsync(c->d_text, h_text, n, cudaMemcpyHostToDevice, st);
+  rc = mb_find_batch(c, plans.data(), K, c->d_text, n, c->d_out, cap, c->d_offs, st);
+  if (!rc) {
+    cudaMemcpyAsync(h_offsets, c->d_offs, sizeof(int64_t) * (K + 1), cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "batch search");
+  }
+  if (!rc) {
+    int64_t total = h_offsets[K];
+    int64_t ncopy = std::min(total, cap);
+    if (ncopy > 0) {
+      cudaError_t e = cudaMemcpy(h_out, c->d_out, sizeof(int64_t) * ncopy, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) rc = cuda_fail(e, "position copy");
+    }
+    if (!rc && total > cap) rc = fail(MB_EOVERFLOW, "output capacity too small");
+  }
+  cleanup();
+  return rc;
+}
+
+int mb_search_host(mb_ctx* c, const uint8_t* h_pattern, int64_t m, const uint8_t* h_text, int64_t n,
+                   int64_t* h_out, int64_t cap, int64_t* h_count) {
+  if (!h_count) return fail(MB_EINVAL, "null count");
+  int64_t offs[2] = {0, 0};
+  int rc = mb_search_batch_host(c, &h_pattern, &m, 1, h_text, n, h_out, cap, offs);
+  *h_count = offs[1];
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+// plan.h -- shared plan structures (host preprocessing <-> device scan).
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/matchb200.h"
+
+namespace mb {
+
+// Per-pattern scan parameters as the kernel reads them (one entry per pattern
+// of a batch; a single search is a batch of one).
+struct PatDev {
+  const uint8_t* bytes;  // device copy of the pattern
+  int64_t m;
+  int32_t family;
+  int32_t anchor;   // pattern offset of the anchor window
+  int32_t delta;    // bitmap index b <-> start position s = b - delta - text_misalignment
+  int32_t per;      // smallest period
+  int32_t L;        // m - per when periodic (break-run length), else 0
+  int32_t periodic; // verification by first period block + no break in [s, s+L)
+  int32_t exact;    // filter alone decides (no verification)
+  int32_t pre;      // staged bytes before the tile's first bit (multiple of 16)
+  int32_t post;     // staged bytes after the tile's last bit (multiple of 16)
+  uint32_t G[4];    // filter words (family specific)
+};
+
+struct PlanHost {
+  int64_t m = 0;
+  std::vector<uint8_t> pat;
+  int64_t hor[256];
+  int64_t sun[256];
+  std::vector<int64_t> kmp;
+  int period = 0;
+  int family = 0;
+  int anchor = 0;
+  PatDev dev;
+};
+
+void horspool_table(const uint8_t* p, int64_t m, int64_t* tbl);
+void sunday_table(const uint8_t* p, int64_t m, int64_t* tbl);
+void kmp_failure(const uint8_t* p, int64_t m, int64_t* fail);
+void forward_masks(const uint8_t* p, int64_t m, uint64_t* out, int64_t words);
+uint32_t gram_hash(const uint8_t* s, int64_t start, int q);
+int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost* ph, std::string* err);
+
+}  // namespace mb

@@ -1,0 +1,166 @@
+"""GPU parity: the sm_100a engine (through the C ABI) vs the CPU oracle.
+
+Bit-exact on every position (integer work: no tolerance).  Cases follow the
+reference suite's generators (tests/cases.py) plus GPU-specific edges: tile
+and halo boundaries, misaligned text pointers, dense/periodic matches,
+capacity overflow and batched CSR output.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1012_2547_b200 as mb
+from cases import KNOWN, fuzz_cases, rand_bytes
+from paper_1012_2547_b200 import engine
+
+pytestmark = pytest.mark.gpu
+TILE = 16384
+
+
+def gpu_positions(p: bytes, t, family="auto") -> np.ndarray:
+    plan = engine.Plan(p, family)
+    return engine.find(plan, t).cpu().numpy()
+
+
+def check(p: bytes, t: bytes, family="auto"):
+    want = oracle.search(p, t)
+    got = gpu_positions(p, t, family) if len(p) <= len(t) else np.empty(0, np.int64)
+    assert np.array_equal(got, want), (
+        f"m={len(p)} n={len(t)} fam={family}: got {got[:8]} (#{got.size}) want {want[:8]} (#{want.size})")
+
+
+def test_known_answers(cuda):
+    for p, t, exp in KNOWN:
+        assert mb.brute_force_search(p, t) == exp
+        assert mb.search_hor(p, t) == exp
+
+
+def test_entry_points_agree(cuda):
+    t = b"abracadabra" * 50
+    p = b"abra"
+    exp = oracle.search(p, t).tolist()
+    for fn in (mb.search_hor, mb.search_qs, mb.search_br, mb.search_tvsbs, mb.search_fjs, mb.search_bom,
+               mb.search_ebom, mb.search_so, mb.search_sa, mb.search_bndm, mb.search_sbndm, mb.search_lbndm,
+               mb.search_sbndm_bmh, mb.search_bmh_sbndm, mb.search_fsbndm):
+        assert fn(p, t) == exp, fn.__name__
+    assert mb.search_hashq(3, p, t) == exp
+    assert mb.search_sbndmq(4, p, t) == exp
+    assert mb.get_algorithm("B200").search(p, t) == exp
+
+
+@pytest.mark.parametrize("lo,hi,n_max,count", [
+    (1, 3, 600, 300), (4, 6, 600, 300), (7, 16, 1200, 300), (17, 64, 2048, 300),
+    (65, 300, 4096, 200), (301, 1024, 8192, 120), (1025, 4096, 12000, 40),
+])
+def test_fuzz_vs_oracle(cuda, lo, hi, n_max, count):
+    for p, t in fuzz_cases(1000 + lo, count, lo, hi, n_max=n_max):
+        check(p, t)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8, 15, 16, 17, 31, 32, 33, 63, 64, 100, 128, 500, 1024])
+def test_tile_boundaries(cuda, m):
+    rng = np.random.default_rng(m)
+    n = 3 * TILE + 1000
+    t = bytearray(rand_bytes(rng, 256, n))
+    p = rand_bytes(rng, 256, m)
+    plants = []
+    for b in (TILE, 2 * TILE, 3 * TILE):
+        for d in (-m - 3, -m, -m + 1, -5, -1, 0, 1, 3, 7):
+            s = b + d
+            if 0 <= s <= n - m:
+                plants.append(s)
+    plants += [0, n - m]
+    for s in sorted(set(plants)):
+        t[s : s + m] = p
+    check(p, bytes(t))
+
+
+@pytest.mark.parametrize("off", list(range(16)))
+def test_misaligned_text(cuda, off):
+    rng = np.random.default_rng(100 + off)
+    base = torch.from_numpy(np.frombuffer(rand_bytes(rng, 4, 70000 + 64), dtype=np.uint8).copy()).cuda()
+    n = 70000 - off
+    view = base[off : off + n]
+    host = view.cpu().numpy().tobytes()
+    for m in (1, 2, 3, 5, 8, 13, 40):
+        i = int(rng.integers(0, n - m + 1))
+        p = host[i : i + m]
+        got = gpu_positions(p, view)
+        assert np.array_equal(got, oracle.search(p, host)), (off, m)
+
+
+@pytest.mark.parametrize("m", [2, 3, 5, 16, 17, 64, 128, 1024, 2000])
+def test_dense_periodic(cuda, m):
+    rng = np.random.default_rng(m)
+    n = 5 * TILE + 123
+    t = np.full(n, ord("a"), dtype=np.uint8)
+    noise = rng.choice(n, size=n // 1000, replace=False)
+    t[noise] = rng.integers(ord("b"), ord("z") + 1, size=noise.size, dtype=np.uint8)
+    tb = t.tobytes()
+    check(b"a" * m, tb)
+    check(b"a" * (m - 1) + b"b", tb)
+    check((b"ab" * m)[:m], (b"ab" * n)[:n])
+    check((b"abc" * m)[:m], (b"abc" * n)[:n] )
+    check(b"a" * m, b"a" * n)
+
+
+def test_sigma1_and_zero_bytes(cuda):
+    for m in (1, 2, 4, 7, 32, 100):
+        check(b"\x00" * m, b"\x00" * 3000)
+        check(b"\x00" * m, b"\x00" * 3000 + b"\x01" + b"\x00" * 50)
+
+
+@pytest.mark.parametrize("family,lo,hi", [("win4", 4, 40), ("aligned", 7, 200)])
+def test_forced_families(cuda, family, lo, hi):
+    for p, t in fuzz_cases(77, 150, lo, hi, n_max=3000):
+        check(p, t, family)
+
+
+def test_count_only_and_overflow(cuda):
+    rng = np.random.default_rng(5)
+    t = rand_bytes(rng, 2, 200000)
+    p = t[100:104]
+    want = oracle.search(p, t)
+    plan = engine.Plan(p)
+    d = torch.from_numpy(np.frombuffer(t, dtype=np.uint8).copy()).cuda()
+    assert engine.count(plan, d) == want.size
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = torch.full((100,), -1, dtype=torch.int64, device="cuda")
+    engine.find_into(plan, d, out, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == want.size
+    assert np.array_equal(out.cpu().numpy(), want[:100])
+
+
+def test_batch_csr(cuda):
+    rng = np.random.default_rng(9)
+    t = rand_bytes(rng, 8, 300000)
+    pats = [t[i : i + m] for i, m in zip(rng.integers(0, 290000, 40), rng.integers(1, 300, 40))]
+    pats += [b"\x07\x07", b"\x01" * 9, b"zzz" * 50]
+    res = mb.search_many(pats, t)
+    for p, r in zip(pats, res):
+        assert r == oracle.search(p, t).tolist()
+
+
+def test_host_entry(cuda):
+    rng = np.random.default_rng(11)
+    t = np.frombuffer(rand_bytes(rng, 4, 100000), dtype=np.uint8)
+    for m in (3, 9, 70):
+        p = t[500 : 500 + m].tobytes()
+        assert np.array_equal(engine.search_host(p, t, cap=4), oracle.search(p, t))
+
+
+def test_histogram_alphabet(cuda):
+    rng = np.random.default_rng(12)
+    t = rand_bytes(rng, 37, 100000)
+    h = engine.histogram(t).cpu().numpy()
+    assert np.array_equal(h, np.bincount(np.frombuffer(t, np.uint8), minlength=256))
+    assert mb.Text(t).alphabet_size() == len(set(t))
+
+
+def test_instrumented_text_rejected(cuda):
+    with pytest.raises(TypeError):
+        mb.search_hor(b"ab", mb.InstrumentedText(b"abab"))
