@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Headline benchmark: text GB/s scanned (all matches emitted) and % of the HBM roofline.
+
+Workload (default, BASELINE.json config 4 -- the config the north-star roofline
+target is quoted on): a 16 GiB i.i.d. uniform sigma=256 text resident in HBM,
+one pattern per m in {2, 8, 32, 128, 1024} copied from a random text offset.
+A step scans the whole text once per pattern through the C ABI (mb_find) and
+writes every position to HBM.  Other configs are parity cases (tests/), or
+`--workload cfg1|cfg2|cfg3|cfg5` for ad-hoc runs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU: each rank scans its own 16 GiB
+stripe of one (N x 16 GiB) text (weak scaling; a (m-1)-byte halo keeps
+boundary matches exact) and the ranks all_gather their counts (NCCL) to place
+their positions in the global output -- the path's only exchange.
+`--impl reference` times the reference algorithms' CPU restatement (oracle/,
+the auto-selected searcher per m, all host threads) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "text GB/s scanned (all matches emitted) vs m and σ; % of HBM roofline"
+CFG4_LENGTHS = (2, 8, 32, 128, 1024)
+PEAK_FALLBACK = 6650.0  # B200_PROFILING.md fallback, GB/s
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=("cfg4", "cfg1", "cfg3", "cfg5"), default="cfg4")
+    ap.add_argument("--n", type=int, default=0, help="text bytes per GPU (default: the config's size)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=2 << 30, help="bytes of text in the CPU baseline sample")
+    return ap.parse_args()
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs (copy)"
+    except Exception:
+        return PEAK_FALLBACK, "B200_PROFILING.md fallback"
+
+
+def ncu_traffic(workload):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workloads
+def build_workload(args, rank, world):
+    """Host text (pinned) + patterns for this rank; returns dict."""
+    import numpy as np
+    import torch
+
+    from paper_1012_2547_b200 import inputs
+
+    if args.workload == "cfg4":
+        n = args.n or (16 << 30)
+        n = (n // inputs.STRIPE) * inputs.STRIPE if n >= inputs.STRIPE else n
+        halo = 1023 if rank < world - 1 else 0
+        host = torch.empty(n + halo, dtype=torch.uint8, pin_memory=True)
+        h = host.numpy()
+        stripe0 = rank * max(n // inputs.STRIPE, 1)
+        _cfg4_stripes(h[:n], stripe0, n)
+        if halo:
+            nxt = np.empty(inputs.STRIPE if n >= inputs.STRIPE else n, dtype=np.uint8)
+            _cfg4_stripes(nxt, stripe0 + max(n // inputs.STRIPE, 1), nxt.size)
+            h[n:] = nxt[:halo]
+        pats = inputs.config4_patterns(h[:n]) if rank == 0 else None
+        desc = (f"cfg4: {n / 2**30:.0f} GiB i.i.d. uniform sigma=256 text per GPU, 1 pattern per m in "
+                f"{list(CFG4_LENGTHS)} copied from a random offset")
+        sigma = 256
+    elif args.workload == "cfg1":
+        t, pats = inputs.config1()
+        n, halo = t.size, 0
+        host = torch.from_numpy(t).pin_memory()
+        desc = "cfg1: 1 MiB sigma=4, one m=8 pattern"
+        sigma = 4
+    elif args.workload == "cfg3":
+        n = args.n or (64 << 20)
+        t = inputs.zipf_text(n, inputs.derive_seed(inputs.ROOT_SEED, "cfg3", "text"))
+        host, halo = torch.from_numpy(t).pin_memory(), 0
+        pats = [inputs.config3_patterns(t, m, 1)[0] for m in (4, 16, 64, 256, 1024)]
+        desc = "cfg3: 64 MiB Zipf text (95 printable symbols), 1 pattern per m in [4,16,64,256,1024]"
+        sigma = 95
+    else:  # cfg5
+        n = args.n or (256 << 20)
+        t = inputs.dense_text(n, inputs.derive_seed(inputs.ROOT_SEED, "cfg5", "text"))
+        host, halo = torch.from_numpy(t).pin_memory(), 0
+        pats = inputs.config5_patterns()
+        desc = "cfg5: 256 MiB 99.9% 'a' text, patterns a^m and a^(m-1)b for m in [2,16,128,1024]"
+        sigma = 26
+    if world > 1:
+        import torch.distributed as dist
+
+        obj = [pats]
+        dist.broadcast_object_list(obj, src=0)
+        pats = obj[0]
+    return {"host": host, "n": n, "halo": halo, "patterns": pats, "desc": desc, "sigma": sigma}
+
+
+def _cfg4_stripes(out, first_stripe, n):
+    import concurrent.futures as cf
+
+    from paper_1012_2547_b200 import inputs
+
+    S = inputs.STRIPE
+    k = max((n + S - 1) // S, 1)
+
+    def one(i):
+        lo, hi = i * S, min(n, (i + 1) * S)
+        inputs.rand_text_np(256, hi - lo, inputs.derive_seed(inputs.ROOT_SEED, "cfg4", "text", first_stripe + i),
+                            out=out[lo:hi])
+
+    with cf.ThreadPoolExecutor(min(32, os.cpu_count() or 4)) as ex:
+        list(ex.map(one, range(k)))
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    """The reference's algorithms (CPU restatement in oracle/, auto-selected per
+    m as `matchbench search --algo auto` does, registry.py:209-222) on all host
+    threads, over a bounded prefix sample of the same workload."""
+    import numpy as np
+
+    if rank != 0:
+        return
+    import oracle
+    from paper_1012_2547_b200 import inputs
+    from paper_1012_2547_b200.registry import select_applicable
+
+    threads = os.cpu_count() or 1
+    sample = min(args.cpu_sample, args.n or (16 << 30)) if args.workload == "cfg4" else 0
+    if args.workload == "cfg4":
+        sample = max(inputs.STRIPE, (sample // inputs.STRIPE) * inputs.STRIPE) if sample >= inputs.STRIPE else sample
+        t = np.empty(sample, dtype=np.uint8)
+        _cfg4_stripes(t, 0, sample)
+        pats = inputs.config4_patterns(t)
+        sigma = 256
+    else:
+        wl = build_workload(args, 0, 1)
+        t = wl["host"].numpy()[: wl["n"]]
+        pats, sigma = wl["patterns"], wl["sigma"]
+        sample = t.size
+    algos = [select_applicable(sigma, len(p)).id for p in pats]
+
+    def step():
+        for p, a in zip(pats, algos):
+            oracle.count(p, t, a, threads=threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = len(pats) * sample / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": args.workload, "sample_bytes": int(sample), "patterns_m": [len(p) for p in pats]},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample / 2**20:.0f} MiB prefix x {len(pats)} patterns, algorithms {algos} "
+                                   f"(oracle/oracle.c restatement, {threads} threads, halo-overlapped chunks)"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(wl, sample_bytes):
+    """Single-core reference-path baseline on a bounded prefix (bench.py:171-181
+    time-mode semantics: compile untimed, 1 warm-up, timed run)."""
+    import oracle
+    from paper_1012_2547_b200.registry import select_applicable
+
+    t = wl["host"].numpy()[: min(wl["n"], sample_bytes)]
+    total_t, total_b, used = 0.0, 0, []
+    for p in wl["patterns"]:
+        a = select_applicable(wl["sigma"], len(p)).id
+        oracle.count(p, t[: 1 << 20], a)  # warm-up
+        t0 = time.perf_counter()
+        oracle.count(p, t, a)
+        total_t += time.perf_counter() - t0
+        total_b += t.size
+        used.append(a)
+    return {"value": round(total_b / total_t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"{t.size / 2**20:.0f} MiB prefix x {len(wl['patterns'])} patterns, reference auto path "
+                      f"{used} restated in C (oracle/), 1 thread of {os.cpu_count()} host cores"}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_1012_2547_b200 import engine
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    wl = build_workload(args, rank, world)
+    n, halo, pats = wl["n"], wl["halo"], wl["patterns"]
+    d_text = torch.empty(n + halo, dtype=torch.uint8, device=dev)
+    d_text.copy_(wl["host"], non_blocking=False)
+    plans = [engine.Plan(p) for p in pats]
+    views = [d_text[: min(n + len(p) - 1, n + halo)] for p in pats]  # starts < n on this rank
+    # output capacity: count first (untimed), then allocate
+    cnts = [engine.count(pl, v) for pl, v in zip(plans, views)]
+    out = torch.empty(max(max(cnts), 1), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(len(plans), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+    K = len(plans)
+
+    def step(ev=None):
+        for i, (pl, v) in enumerate(zip(plans, views)):
+            if ev is not None:
+                ev[i][0].record(stream)
+            engine.find_into(pl, v, out, cnt[i : i + 1], stream)
+            if ev is not None:
+                ev[i][1].record(stream)
+        if dist is not None:  # exchange: global output offsets from per-rank counts
+            allc = [torch.empty_like(cnt) for _ in range(world)]
+            dist.all_gather(allc, cnt)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(K)]
+           for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if clk:
+        clk.start()
+        time.sleep(0.25)
+    l0 = engine.launch_count()
+    torch.cuda.synchronize()
+    t_start.record(stream)
+    for s in range(args.steps):
+        step(evs[s])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    launches = engine.launch_count() - l0
+    clocks = clk.stop() if clk else None
+    ms = t_start.elapsed_time(t_end) / args.steps
+    if dist is not None:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    counts = cnt.cpu().tolist()
+    per_launch = [[evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(args.steps)] for i in range(K)]
+    bytes_scanned = [v.numel() for v in views]
+    value = world * sum(min(b, n) for b in bytes_scanned) / (ms * 1e-3) / 1e9
+
+    # roofline of the scan kernel: algorithmic bytes (text + 8 B per position + count) / launch time
+    alg_bytes = [b + 8 * c + 8 for b, c in zip(bytes_scanned, counts)]
+    avg_ms = [statistics.mean(x) for x in per_launch]
+    achieved = sum(alg_bytes) / (sum(avg_ms) * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic(args.workload)
+    per_m = [{"m": len(p), "count": c, "ms": round(a, 4), "text_gbps": round(b / (a * 1e-3) / 1e9, 1),
+              "hbm_frac": round((ab / (a * 1e-3) / 1e9) / peak, 4)}
+             for p, c, a, b, ab in zip(pats, counts, avg_ms, bytes_scanned, alg_bytes)]
+
+    parity = None
+    if not args.no_parity and rank == 0:
+        import oracle
+
+        h = wl["host"].numpy()
+        ok = True
+        for i, (p, v) in enumerate(zip(pats, views)):
+            want = oracle.search(p, h[: v.numel()], "BF", threads=os.cpu_count() or 1)
+            engine.find_into(plans[i], v, out, cnt[i : i + 1], stream)
+            got = out[: int(cnt[i].item())].cpu().numpy()
+            ok = ok and np.array_equal(got, want)
+        parity = "bit-exact vs oracle (all positions, all patterns)" if ok else "MISMATCH"
+
+    e2e = None
+    if not args.no_e2e:
+        # reference-facing C ABI with HOST buffers: H2D of the text, scan of all
+        # patterns, D2H of every position -- inside the timed region
+        host_np = wl["host"].numpy()[:n]  # single-GPU host entry has no halo semantics
+        total_pos = sum(cnts) if world == 1 else sum(cnts)
+        h_out = torch.empty(max(total_pos, 1), dtype=torch.int64, pin_memory=True).numpy()
+        h_offs = np.zeros(K + 1, dtype=np.int64)
+        engine.search_batch_host(pats, host_np, h_out, h_offs)  # warm-up (buffers, plans)
+        times = []
+        for _ in range(max(args.e2e_steps, 1)):
+            if dist is not None:
+                dist.barrier()
+            t0 = time.perf_counter()
+            rc = engine.search_batch_host(pats, host_np, h_out, h_offs)
+            times.append(time.perf_counter() - t0)
+        dt = statistics.median(times)
+        if dist is not None:
+            tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": round(world * K * n / dt / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(n + sum(map(len, pats))),
+               "d2h_bytes_per_step": int(8 * int(h_offs[-1]) + 8 * (K + 1)), "ms_per_step": round(dt * 1e3, 2),
+               "api": "mb_search_batch_host (C ABI, pinned host text in, host positions out)", "rc": int(rc)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, 1 << 30)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl["desc"], "text_bytes_per_gpu": int(n), "patterns_m": [len(p) for p in pats],
+                       "l2": "inputs larger than L2 (text >> 126 MB), no flush needed" if n > (512 << 20)
+                       else "L2-resident text (no flush)", "parallelism": f"dp{world} (text stripes, count all_gather)"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "scan_kernel (per-pattern launch)",
+                         "algorithmic_bytes": "n + 8*count + 8 per launch (SURVEY.md 8(d))"},
+            "per_m": per_m,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -181,7 +181,7 @@ __device__ void build_breaks(const uint8_t* Y0, int per, int nwords, uint32_t* b
   __syncthreads();
 }
 
-// ---------------------------------------------------------------- kernel
+// ---------------------------------------------------------------- kernel 1: scan
 template <class Filt>
 __global__ void __launch_bounds__(NT) scan_kernel(const ScanParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -192,14 +192,14 @@ __global__ void __launch_bounds__(NT) scan_kernel(const ScanParams P) {
   uint32_t* bm = (uint32_t*)(tail + SM_BM);
   uint32_t* brk = (uint32_t*)(tail + SM_BRK);
   int32_t* nbw = (int32_t*)(tail + SM_BRK + 4 * P.brk_words);
-  int64_t* red = (int64_t*)(tail + SM_BRK + 8 * P.brk_words + 16);  // per-warp slots + [32] broadcast
-  uint8_t* spat = (uint8_t*)(red + 40);                               // pattern copy
+  uint32_t* red = (uint32_t*)(tail + SM_BRK + 8 * P.brk_words + 16);  // per-warp slots
+  uint8_t* spat = (uint8_t*)(red + 16);                                 // pattern copy
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  auto issue = [&](int s) {  // thread 0 only
-    unsigned long long tk = atomicAdd(P.ticket, 1ULL);
-    if ((int64_t)tk >= P.total_tickets) {
+  auto issue = [&](int s) {  // thread 0 only: next tile ticket -> TMA into stage s
+    unsigned long long tk = atomicAdd(&P.ticket[0], 1ULL);
+    if ((int64_t)tk >= P.total_tiles) {
       stage_tk[s] = -1;
       return;
     }
@@ -222,7 +222,6 @@ __global__ void __launch_bounds__(NT) scan_kernel(const ScanParams P) {
   }
   __syncthreads();
 
-  const int64_t obase = P.out_base ? *P.out_base : 0;
   int cur_k = -1;
   for (int it = 0;; it++) {
     const int s = it % STAGES;
@@ -263,98 +262,40 @@ __global__ void __launch_bounds__(NT) scan_kernel(const ScanParams P) {
     }
     const int any_tile = __syncthreads_or(anyc);
 
-    // ---- verify phase
-    if (any_tile && !pd.exact) {
-      const int m = (int)pd.m;
-      const uint8_t* Y0 = S - pd.delta;  // Y0[b_local] = text byte at start position of bit b_local
-      if (pd.periodic) {
-        const int nwords = (TILE + pd.L + 31) / 32;
-        build_breaks(Y0, pd.per, nwords, brk, nbw);
-      }
-      for (int wi = 2 * tid; wi < 2 * tid + 2; wi++) {
-        uint32_t cw = bm[wi], mw = 0;
-        while (cw) {
-          const int i = __ffs(cw) - 1;
-          cw &= cw - 1;
-          const int rel = 32 * wi + i;
-          bool ok;
-          if (pd.periodic) {
-            ok = verify_direct(Y0 + rel, spat, pd.per);
-            if (ok) {
-              const uint32_t x = brk[rel >> 5] >> (rel & 31);
-              const int nb = x ? rel + __ffs(x) - 1 : nbw[(rel >> 5) + 1];
-              ok = nb >= rel + pd.L;
-            }
-          } else {
-            ok = verify_direct(Y0 + rel, spat, m);
-          }
-          if (ok) mw |= 1u << i;
-        }
-        bm[wi] = mw;
-      }
-      __syncthreads();
-    }
-
-    // ---- count
-    int64_t tile_cnt = 0;
+    uint32_t tile_cnt = 0;
     if (any_tile) {
-      uint32_t c2 = __popc(bm[2 * tid]) + __popc(bm[2 * tid + 1]);
-      uint32_t ws = __reduce_add_sync(0xffffffffu, c2);
-      if (lane == 0) red[warp] = ws;
-      __syncthreads();
-      for (int q = 0; q < NWARP; q++) tile_cnt += red[q];
-    }
-
-    // ---- decoupled look-back (warp 0): exclusive prefix over all tickets < tk
-    if (warp == 0) {
-      int64_t excl = 0;
-      if (tk == 0) {
-        if (lane == 0) st_relaxed(&P.state[0], pack_state(P.epoch, ST_INCL, (uint64_t)tile_cnt));
-      } else {
-        if (lane == 0) st_relaxed(&P.state[tk], pack_state(P.epoch, ST_AGG, (uint64_t)tile_cnt));
-        int64_t j = tk - 1;
-        while (true) {
-          const int64_t idx = j - lane;
-          uint64_t v;
-          if (idx < 0) {
-            v = pack_state(P.epoch, ST_INCL, 0);
-          } else {
-            int spins = 0;
-            while (true) {
-              v = ld_relaxed(&P.state[idx]);
-              if ((uint32_t)(v >> 40) == P.epoch && ((v >> 38) & 3)) break;
-              if (++spins > 8) __nanosleep(32);
-            }
-          }
-          const uint64_t st = (v >> 38) & 3;
-          const int64_t val = (int64_t)(v & ((1ULL << 38) - 1));
-          const uint32_t incl = __ballot_sync(0xffffffffu, st == ST_INCL);
-          if (incl) {
-            const int first = __ffs(incl) - 1;
-            int64_t contrib = lane <= first ? val : 0;
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
-            excl += contrib;
-            break;
-          }
-          int64_t contrib = val;
-#pragma unroll
-          for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
-          excl += contrib;
-          j -= 32;
+      // ---- verify phase
+      if (!pd.exact) {
+        const int m = (int)pd.m;
+        const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of bit rel
+        if (pd.periodic) {
+          const int nwords = (TILE + pd.L + 31) / 32;
+          build_breaks(Y0, pd.per, nwords, brk, nbw);
         }
-        if (lane == 0) st_relaxed(&P.state[tk], pack_state(P.epoch, ST_INCL, (uint64_t)(excl + tile_cnt)));
+        for (int wi = 2 * tid; wi < 2 * tid + 2; wi++) {
+          uint32_t cw = bm[wi], mw = 0;
+          while (cw) {
+            const int i = __ffs(cw) - 1;
+            cw &= cw - 1;
+            const int rel = 32 * wi + i;
+            bool ok;
+            if (pd.periodic) {
+              ok = verify_direct(Y0 + rel, spat, pd.per);
+              if (ok) {
+                const uint32_t x = brk[rel >> 5] >> (rel & 31);
+                const int nb = x ? rel + __ffs(x) - 1 : nbw[(rel >> 5) + 1];
+                ok = nb >= rel + pd.L;
+              }
+            } else {
+              ok = verify_direct(Y0 + rel, spat, m);
+            }
+            if (ok) mw |= 1u << i;
+          }
+          bm[wi] = mw;
+        }
+        __syncthreads();
       }
-      if (lane == 0) {
-        red[32] = excl;
-        if (tau == P.ntiles - 1) P.offsets_plus1[k] = obase + excl + tile_cnt;
-      }
-    }
-    __syncthreads();
-
-    // ---- expansion: ascending positions at out[excl + ...]
-    if (tile_cnt > 0 && P.out) {
-      const int64_t excl = obase + red[32];
+      // ---- count + compact store
       const uint32_t w0 = bm[2 * tid], w1 = bm[2 * tid + 1];
       const uint32_t c2 = __popc(w0) + __popc(w1);
       uint32_t inc = c2;
@@ -363,22 +304,171 @@ __global__ void __launch_bounds__(NT) scan_kernel(const ScanParams P) {
         uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
         if (lane >= d) inc += o;
       }
-      if (lane == 31) red[warp] = inc;  // safe: red[0..7] no longer read
+      if (lane == 31) red[warp] = inc;
       __syncthreads();
-      int64_t base = excl;
-      for (int q = 0; q < warp; q++) base += red[q];
-      base += inc - c2;
-      const int64_t pos0 = B0 + 64 * tid - pd.delta - P.off;
-      uint64_t bits = ((uint64_t)w1 << 32) | w0;
-      while (bits) {
-        const int i = __ffsll((long long)bits) - 1;
-        bits &= bits - 1;
-        if (base < P.cap) P.out[base] = pos0 + i;
-        base++;
+      uint32_t before = 0;
+      for (int q = 0; q < NWARP; q++) {
+        const uint32_t v = red[q];
+        tile_cnt += v;
+        before += q < warp ? v : 0;
+      }
+      if (tile_cnt <= LIST_CAP) {
+        uint32_t j = before + inc - c2;
+        uint16_t* L = P.lists + (size_t)tk * LIST_CAP;
+        uint64_t bits = ((uint64_t)w1 << 32) | w0;
+        while (bits) {
+          const int i = __ffsll((long long)bits) - 1;
+          bits &= bits - 1;
+          L[j++] = (uint16_t)(64 * tid + i);
+        }
+      } else {
+        uint2* dst = reinterpret_cast<uint2*>(P.bitmaps + (size_t)tk * BM_WORDS);
+        dst[tid] = make_uint2(w0, w1);
       }
     }
+    if (tid == 0) P.counts[tk] = tile_cnt;
     __syncthreads();  // stage s, bm, red free
     if (tid == 0) issue(s);
+  }
+}
+
+// ------------------------------------------------ kernel 2: tile offsets (scan)
+// Exclusive scan of per-tile counts in SCAN_CHUNK pieces; chunk order = ticket
+// order taken at CTA start (no prefetch), so each chunk only waits on chunks
+// that are already running -- the decoupled look-back never stalls on a
+// queued predecessor.
+__global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
+  __shared__ int64_t wsum[NWARP];
+  __shared__ int64_t s_excl;
+  __shared__ int64_t s_chunk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_chunk = (int64_t)atomicAdd(&P.ticket[1], 1ULL);
+  __syncthreads();
+  const int64_t ch = s_chunk;
+  const int64_t base = ch * SCAN_CHUNK;
+  constexpr int PER = SCAN_CHUNK / NT;  // 16 counts per thread
+  uint32_t v[PER];
+  int64_t tsum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const int64_t t = base + (int64_t)tid * PER + q;
+    v[q] = t < P.total_tiles ? P.counts[t] : 0u;
+    tsum += v[q];
+  }
+  int64_t inc = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int64_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  int64_t chunk_total = 0, wbefore = 0;
+  for (int q = 0; q < NWARP; q++) {
+    chunk_total += wsum[q];
+    wbefore += q < warp ? wsum[q] : 0;
+  }
+  if (warp == 0) {
+    int64_t excl = 0;
+    if (ch == 0) {
+      if (lane == 0) st_relaxed(&P.state[0], pack_state(P.epoch, ST_INCL, (uint64_t)chunk_total));
+    } else {
+      if (lane == 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_AGG, (uint64_t)chunk_total));
+      int64_t j = ch - 1;
+      while (true) {
+        const int64_t idx = j - lane;
+        uint64_t sv;
+        if (idx < 0) {
+          sv = pack_state(P.epoch, ST_INCL, 0);
+        } else {
+          while (true) {
+            sv = ld_relaxed(&P.state[idx]);
+            if ((uint32_t)(sv >> 40) == P.epoch && ((sv >> 38) & 3)) break;
+            __nanosleep(20);
+          }
+        }
+        const uint64_t st = (sv >> 38) & 3;
+        const int64_t val = (int64_t)(sv & ((1ULL << 38) - 1));
+        const uint32_t incl = __ballot_sync(0xffffffffu, st == ST_INCL);
+        int64_t contrib = val;
+        if (incl) contrib = lane <= __ffs(incl) - 1 ? val : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
+        excl += contrib;
+        if (incl) break;
+        j -= 32;
+      }
+      if (lane == 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_INCL, (uint64_t)(excl + chunk_total)));
+    }
+    if (lane == 0) s_excl = excl + (P.out_base ? *P.out_base : 0);
+  }
+  __syncthreads();
+  int64_t run = s_excl + wbefore + inc - tsum;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const int64_t t = base + (int64_t)tid * PER + q;
+    if (t < P.total_tiles) {
+      P.toff[t] = run;
+      if (t % P.ntiles == P.ntiles - 1) P.offsets_plus1[t / P.ntiles] = run + v[q];
+    }
+    run += v[q];
+  }
+}
+
+// ------------------------------------------------ kernel 3: expansion
+// One warp per tile (grid-stride).  Sparse tiles copy their uint16 list;
+// dense tiles expand the bitmap 32 words at a time through a per-warp smem
+// staging buffer so every global store is a coalesced 256-byte run.
+constexpr int EXP_WARPS = 4;
+__global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
+  __shared__ int64_t stage[EXP_WARPS][1024];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * EXP_WARPS + warp;
+  const int64_t nw = (int64_t)gridDim.x * EXP_WARPS;
+  int cur_k = -1;
+  int64_t shift = 0;
+  for (int64_t t = gw; t < P.total_tiles; t += nw) {
+    const uint32_t c = P.counts[t];
+    if (c == 0) continue;
+    const int k = (int)(t / P.ntiles);
+    if (k != cur_k) {
+      shift = P.pats[k].delta + P.off;
+      cur_k = k;
+    }
+    const int64_t pos0 = (t % P.ntiles) * TILE - shift;
+    const int64_t o = P.toff[t];
+    if (o >= P.cap) continue;
+    if (c <= LIST_CAP) {
+      if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + P.lists[t * LIST_CAP + lane];
+      continue;
+    }
+    const uint32_t* bmw = P.bitmaps + (size_t)t * BM_WORDS;
+    int64_t w_out = o;
+    for (int wb = 0; wb < BM_WORDS; wb += 32) {
+      const uint32_t x = bmw[wb + lane];
+      const uint32_t pc = __popc(x);
+      uint32_t inc = pc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+      if (total == 0) continue;
+      uint32_t j = inc - pc;
+      uint32_t xx = x;
+      const int64_t pb = pos0 + 32 * (wb + lane);
+      while (xx) {
+        const int i = __ffs(xx) - 1;
+        xx &= xx - 1;
+        stage[warp][j++] = pb + i;
+      }
+      __syncwarp();
+      for (uint32_t q = lane; q < total; q += 32)
+        if (w_out + q < P.cap) P.out[w_out + q] = stage[warp][q];
+      __syncwarp();
+      w_out += total;
+    }
   }
 }
 
@@ -460,6 +550,14 @@ struct mb_ctx {
   int nsm = 0;
   uint64_t* state = nullptr;
   int64_t state_cap = 0;
+  uint32_t* counts = nullptr;
+  int64_t counts_cap = 0;
+  uint16_t* lists = nullptr;
+  int64_t lists_cap = 0;
+  uint32_t* bitmaps = nullptr;
+  int64_t bitmaps_cap = 0;
+  int64_t* toff = nullptr;
+  int64_t toff_cap = 0;
   uint32_t epoch = 0;
   unsigned long long* ticket = nullptr;
   PatDev* d_pats = nullptr;
@@ -558,7 +656,7 @@ int mb_ctx_create(int device, mb_ctx** out) {
   mb_ctx* c = new mb_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMalloc(&c->ticket, sizeof(unsigned long long)) != cudaSuccess) {
+  if (cudaMalloc(&c->ticket, 2 * sizeof(unsigned long long)) != cudaSuccess) {
     delete c;
     return fail(MB_ENOMEM, "ticket alloc");
   }
@@ -569,6 +667,10 @@ int mb_ctx_create(int device, mb_ctx** out) {
 void mb_ctx_destroy(mb_ctx* c) {
   if (!c) return;
   cudaFree(c->state);
+  cudaFree(c->counts);
+  cudaFree(c->lists);
+  cudaFree(c->bitmaps);
+  cudaFree(c->toff);
   cudaFree(c->ticket);
   cudaFree(c->d_pats);
   cudaFree(c->d_text);
@@ -579,6 +681,21 @@ void mb_ctx_destroy(mb_ctx* c) {
 }
 
 }  // extern "C"
+
+// grow-only device scratch
+template <class T>
+static int grow(T** p, int64_t* cap, int64_t need, const char* what) {
+  if (need <= *cap) return MB_OK;
+  cudaFree(*p);
+  *p = nullptr;
+  int64_t ncap = std::max<int64_t>(need, 1024);
+  if (cudaMalloc(p, sizeof(T) * ncap) != cudaSuccess) {
+    *cap = 0;
+    return fail(MB_ENOMEM, std::string("scratch alloc: ") + what);
+  }
+  *cap = ncap;
+  return MB_OK;
+}
 
 template <class F>
 static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
@@ -612,7 +729,7 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
     return MB_OK;
   }
   P.ntiles = (nbits + TILE - 1) / TILE;
-  P.total_tickets = P.ntiles * K;
+  P.total_tiles = P.ntiles * K;
   P.pats = d_pats;
   P.K = K;
   P.pre = pre;
@@ -620,20 +737,22 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
   P.stage_bytes = (pre + TILE + post + 127) & ~127;
   P.brk_words = (((TILE + maxL + 63) / 32) + 3) & ~3;
   P.pat_cap = (int)((maxm + 15) & ~15) + 16;
-  if (P.total_tickets > c->state_cap || c->epoch >= (1u << 24) - 1) {
-    if (P.total_tickets > c->state_cap) {
-      cudaFree(c->state);
-      c->state = nullptr;
-      int64_t ncap = std::max<int64_t>(P.total_tickets, 1 << 16);
-      if (cudaMalloc(&c->state, sizeof(uint64_t) * ncap) != cudaSuccess) {
-        c->state_cap = 0;
-        return fail(MB_ENOMEM, "look-back state alloc");
-      }
-      c->state_cap = ncap;
-    }
+  const int64_t T = P.total_tiles;
+  const int64_t nchunks = (T + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  int rc;
+  if ((rc = grow(&c->counts, &c->counts_cap, T, "counts"))) return rc;
+  if ((rc = grow(&c->lists, &c->lists_cap, T * LIST_CAP, "lists"))) return rc;
+  if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * BM_WORDS, "bitmaps"))) return rc;
+  if ((rc = grow(&c->toff, &c->toff_cap, T, "tile offsets"))) return rc;
+  if (nchunks > c->state_cap || c->epoch >= (1u << 24) - 1) {
+    if ((rc = grow(&c->state, &c->state_cap, nchunks, "look-back state"))) return rc;
     CUDA_TRY(cudaMemsetAsync(c->state, 0, sizeof(uint64_t) * c->state_cap, st));
     c->epoch = 0;
   }
+  P.counts = c->counts;
+  P.lists = c->lists;
+  P.bitmaps = c->bitmaps;
+  P.toff = c->toff;
   P.state = c->state;
   P.epoch = ++c->epoch;
   P.ticket = c->ticket;
@@ -641,12 +760,13 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
   P.cap = d_out ? cap : 0;
   P.offsets_plus1 = offsets_plus1;
   P.out_base = out_base;
-  CUDA_TRY(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned long long), st));
+  CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 2 * sizeof(unsigned long long), st));
 
-  size_t smem = (size_t)STAGES * P.stage_bytes + SM_BRK + 8 * P.brk_words + 16 + 8 * 40 + P.pat_cap;
+  size_t smem = (size_t)STAGES * P.stage_bytes + SM_BRK + 8 * P.brk_words + 16 + 4 * 16 + P.pat_cap;
   static std::mutex mu;
   static bool attr_done = false;
-  static int per_sm_cache[4] = {0, 0, 0, 0};  // keyed by stage-size class
+  static size_t occ_smem = 0;
+  static int occ_val = 0;
   int per_sm = 0;
   {
     std::lock_guard<std::mutex> g(mu);
@@ -654,18 +774,26 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
       CUDA_TRY(cudaFuncSetAttribute(scan_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr_done = true;
     }
-    int cls = smem <= 70000 ? 0 : smem <= 76000 ? 1 : smem <= 82000 ? 2 : 3;
-    if (!per_sm_cache[cls] || cls == 3) {
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_kernel<F>, NT, smem));
-      per_sm_cache[cls] = per_sm;
+    if (occ_smem != smem) {
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val, scan_kernel<F>, NT, smem));
+      occ_smem = smem;
     }
-    per_sm = per_sm_cache[cls];
+    per_sm = occ_val;
   }
   if (per_sm < 1) return fail(MB_ECUDA, "scan kernel does not fit on an SM");
-  int64_t grid = std::min<int64_t>(P.total_tickets, (int64_t)c->nsm * per_sm);
+  int64_t grid = std::min<int64_t>(T, (int64_t)c->nsm * per_sm);
   scan_kernel<F><<<(int)grid, NT, smem, st>>>(P);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
+  offsets_kernel<<<(int)nchunks, NT, 0, st>>>(P);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  if (d_out && cap > 0) {
+    int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS, (int64_t)c->nsm * 16);
+    expand_kernel<<<(int)eg, EXP_WARPS * 32, 0, st>>>(P);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+  }
   return MB_OK;
 }
 

@@ -1,16 +1,19 @@
-// scan.cuh -- the sm_100a scan kernel: (pattern(s), text) -> ordered positions.
+// scan.h -- launch parameters of the sm_100a search pipeline.
 //
-// One persistent kernel family, templated on the filter (K1/K3 of SURVEY.md 2):
+// A search (or a batch of K patterns over one text) is three kernels:
 //
-//   tile ticket (atomic, global order)                    [decoupled look-back order]
-//     -> TMA 1D bulk copy of the tile + halo into a 4-stage smem ring (mbarrier)
-//     -> filter phase: each lane scans 16 bytes/round from smem, packed-word
-//        compare -> candidate bits (16 per lane) -> tile bitmap in smem
-//     -> verify phase (only if any candidate and the filter is not exact):
-//        candidate bits re-checked against the staged text in smem, either
-//        directly or by the period/break-run test for periodic patterns
-//     -> block popcount -> warp-parallel decoupled look-back -> exclusive offset
-//     -> expansion: set bits -> int64 positions, ascending, at out[offset ..]
+//  1. scan_kernel<Filter>  (persistent, dynamic tile tickets, no inter-CTA waits)
+//       TMA 1D bulk copy of tile + halo into a 4-stage smem ring (mbarrier)
+//       -> filter: each lane scans 16 staged bytes per round (packed-word
+//          compare) -> candidate bits -> tile bitmap in smem
+//       -> verify (only if a candidate exists and the filter is not exact):
+//          direct window compare, or period/break-run test, in smem
+//       -> per-tile count; matches stored compactly: <= LIST_CAP tile-local
+//          uint16 offsets, else the tile's 2 KiB bitmap
+//  2. offsets_kernel  exclusive scan of tile counts (decoupled look-back over
+//       4096-count chunks) -> global output offset per tile, CSR pattern ends
+//  3. expand_kernel   warp per tile: list / bitmap -> ascending int64
+//       positions at out[offset ..]
 //
 // Bitmap coordinates: tile tau of a pattern covers bitmap indices
 // b in [tau*TILE, (tau+1)*TILE); index b stands for start position
@@ -30,6 +33,9 @@ constexpr int NWARP = NT / 32;
 constexpr int STAGES = 4;         // TMA ring depth
 constexpr int ROUNDS = TILE / (NWARP * 512);  // 512 positions per warp-round
 constexpr int BM_WORDS = TILE / 32;
+constexpr int LIST_CAP = 32;      // sparse tiles keep <= 32 uint16 offsets
+constexpr int SCAN_CHUNK = 4096;  // tile counts per offsets_kernel CTA
+
 // shared-memory tail after the stage ring: [bars][tickets][bitmap][breaks]
 // [next-break][reduction][pattern]; break/pattern sizes are per launch.
 constexpr int SM_BARS = 0;
@@ -43,20 +49,24 @@ struct ScanParams {
   int64_t n;            // text length
   int64_t nv16;         // round_up(off + n, 16): bytes readable from base
   int64_t ntiles;       // tiles per pattern
-  int64_t total_tickets;
+  int64_t total_tiles;  // K * ntiles
   const PatDev* pats;   // K entries
   int K;
   int pre, post;        // max margins over the batch
   int stage_bytes;
   int brk_words;        // break-bitmap words (multiple of 4)
   int pat_cap;          // pattern bytes reserved in smem (multiple of 16)
-  uint64_t* state;      // look-back flags, >= total_tickets entries
+  unsigned long long* ticket;  // [0]: scan tiles, [1]: offsets chunks
+  uint32_t* counts;     // per tile
+  uint16_t* lists;      // per tile LIST_CAP entries
+  uint32_t* bitmaps;    // per tile BM_WORDS words (dense tiles only)
+  int64_t* toff;        // per tile exclusive output offset
+  uint64_t* state;      // look-back flags of offsets_kernel (per chunk)
   uint32_t epoch;
-  unsigned long long* ticket;
   int64_t* out;         // positions (may be null: count only)
   int64_t cap;
-  int64_t* offsets_plus1;  // entry k <- inclusive prefix after pattern k
-  const int64_t* out_base; // device: output index where this launch starts (null = 0)
+  int64_t* offsets_plus1;   // entry k <- inclusive prefix after pattern k
+  const int64_t* out_base;  // device: output index where this launch starts (null = 0)
 };
 
 }  // namespace mb

@@ -104,8 +104,31 @@ def config3_patterns(text: np.ndarray, m: int, count: int = 500, seed: int = ROO
     return sample_patterns(text, m, count, derive_seed(seed, "cfg3", m))
 
 
-def config4_text(n: int = 16 << 30, seed: int = ROOT_SEED, out: np.ndarray | None = None) -> np.ndarray:
-    return rand_text_np(256, n, derive_seed(seed, "cfg4", "text"), out=out)
+STRIPE = 256 << 20  # config-4 text is generated in independent 256 MiB stripes
+
+
+def config4_text(n: int = 16 << 30, seed: int = ROOT_SEED, out: np.ndarray | None = None,
+                 threads: int | None = None) -> np.ndarray:
+    """Config 4: i.i.d. uniform sigma=256.  Stripe i (256 MiB) is
+    generate_rand_text(256, 256 MiB, derive_seed(seed, "cfg4", "text", i)) of the
+    reference (bench.py:86-100); stripes are drawn in parallel threads (numpy
+    releases the GIL), so 16 GiB takes seconds instead of a minute."""
+    import concurrent.futures as cf
+    import os
+
+    if out is None:
+        out = np.empty(n, dtype=np.uint8)
+    nstripes = (n + STRIPE - 1) // STRIPE
+
+    def one(i):
+        lo = i * STRIPE
+        hi = min(n, lo + STRIPE)
+        rand_text_np(256, hi - lo, derive_seed(seed, "cfg4", "text", i), out=out[lo:hi])
+
+    workers = threads or min(32, os.cpu_count() or 4)
+    with cf.ThreadPoolExecutor(workers) as ex:
+        list(ex.map(one, range(nstripes)))
+    return out
 
 
 def config4_patterns(text: np.ndarray, lengths=(2, 8, 32, 128, 1024), seed: int = ROOT_SEED):

@@ -144,7 +144,7 @@ def configs():
             rows3.append([m, i, len(r), digest(r)])
     res["cfg3_4MiB"] = {"text": tdigest(t3.tobytes()), "rows": rows3}
     # config 4 -- 4 MiB prefix of the sigma=256 stream
-    t4 = rbench.generate_rand_text(256, 4 << 20, inputs.derive_seed(inputs.ROOT_SEED, "cfg4", "text"))
+    t4 = rbench.generate_rand_text(256, 4 << 20, inputs.derive_seed(inputs.ROOT_SEED, "cfg4", "text", 0))
     rows4 = []
     for m in (2, 8, 32, 128, 1024):
         (i,) = rbench.sample_positions(t4, m, 1, inputs.derive_seed(inputs.ROOT_SEED, "cfg4p", m))

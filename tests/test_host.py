@@ -1,0 +1,199 @@
+"""CPU: the C-ABI library loads and exports every declared symbol; the host-side
+mirror of the reference interface (bounds, errors, registry, selection map,
+inputs, sharding) behaves like the reference -- no GPU compute here."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1012_2547_b200 as mb
+from paper_1012_2547_b200 import engine, inputs, registry, searchers
+from paper_1012_2547_b200.core import ApplicabilityError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "matchb200.h")).read()
+    declared = set(re.findall(r"\b(mb_[a-z_0-9]+)\s*\(", hdr))
+    assert declared == set(engine.EXPORTS)
+    lib = ctypes.CDLL(engine.LIB_PATH)
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    assert b"sm_100a" in engine.load_library().mb_version()
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", engine.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_oracle_on_product_path():
+    pkg = os.path.join(ROOT, "paper_1012_2547_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cpp", ".h")):
+                src = open(os.path.join(dirpath, fn)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), fn
+                assert "liboracle" not in src, fn
+
+
+def test_search_without_gpu_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(Exception):
+        mb.search_hor(b"ab", b"abab")
+
+
+def test_bounds_and_errors_mirror_reference():
+    # ApplicabilityError at compile time, with the reference's message format (core.py:23)
+    with pytest.raises(ApplicabilityError, match=r"SSEF is not applicable at m=16: requires m >= 32"):
+        mb.search_ssef(b"x" * 16, b"whatever")
+    with pytest.raises(ApplicabilityError, match="m >= 32"):
+        searchers.compile_ssef(b"x" * 31)
+    with pytest.raises(ApplicabilityError):
+        mb.search_hashq(5, b"abcd", b"whatever")
+    with pytest.raises(ValueError):
+        mb.search_hashq(4, b"abcd", b"whatever")
+    with pytest.raises(ApplicabilityError, match=r"requires m <= w \(64\)"):
+        mb.search_bndm(b"x" * 65, b"whatever")
+    with pytest.raises(ApplicabilityError, match=r"m <= w-1 \(63\)"):
+        mb.search_fsbndm(b"x" * 64, b"whatever")
+    with pytest.raises(ApplicabilityError):
+        mb.search_sbndmq(8, b"abcd", b"whatever")
+    with pytest.raises(ValueError):
+        mb.search_sbndmq(3, b"abc", b"whatever")
+    with pytest.raises(ApplicabilityError):
+        mb.search_ebom(b"a", b"aaa")
+    with pytest.raises(ValueError):
+        mb.brute_force_search(b"", b"abc")
+    with pytest.raises(ValueError):
+        mb.Pattern(b"")
+    e = ApplicabilityError("X", 3, "m >= 5")
+    assert isinstance(e, ValueError) and (e.algorithm, e.m, e.bound) == ("X", 3, "m >= 5")
+    w32 = registry.build_registry(mb.WordSpec(32))
+    d = {a.id: a for a in w32}
+    assert d["BNDM"].m_max == 32 and d["FSBNDM"].m_max == 31
+    with pytest.raises(ApplicabilityError):
+        d["BNDM"].compile(b"x" * 33)
+
+
+def test_registry_mirror():
+    ids = [a.id for a in mb.REGISTRY]
+    assert ids == ["HOR", "QS", "BR", "TVSBS", "FJS", "HASH3", "HASH5", "HASH8", "SSEF", "BOM", "EBOM", "SO",
+                   "SA", "BNDM", "SBNDM", "LBNDM", "SBNDM-BMH", "BMH-SBNDM", "FSBNDM", "SBNDMq2", "SBNDMq4",
+                   "SBNDMq6", "SBNDMq8"]
+    assert "B200" not in ids and mb.get_algorithm("b200") is mb.B200
+    assert mb.get_algorithm("hor").id == "HOR"
+    with pytest.raises(KeyError):
+        mb.get_algorithm("nope")
+    assert {a.id for a in mb.applicable_algorithms(4)} >= {"HOR", "SO", "SA", "BNDM", "HASH3", "SBNDMq4"}
+    assert not any(a.needs_word for a in mb.applicable_algorithms(2048))
+    with pytest.raises(ValueError):
+        mb.applicable_algorithms(0)
+
+
+def test_selection_map_matches_reference_cells():
+    sel = mb.select_applicable
+    # SURVEY.md 8(d) auto-path picks
+    assert [sel(256, m).id for m in (2, 8, 32, 128, 1024)] == ["FJS", "EBOM", "EBOM", "SSEF", "LBNDM"]
+    assert [sel(95, m).id for m in (4, 16, 64, 256, 1024)] == ["FJS", "EBOM", "TVSBS", "TVSBS", "SSEF"]
+    assert sel(4, 8).id == "HASH5"
+    assert mb.classify(128, 4) == mb.SizeClasses("very_large", "very_short")
+    csv = mb.DEFAULT_SELECTION_MAP.to_csv().strip().splitlines()
+    assert len(csv) == 17 and "very_small,short,HASH5,derived-fill" in csv
+
+
+def test_descriptor_substitution_seam():
+    from dataclasses import replace
+
+    gpu = replace(mb.get_algorithm("HOR"), id="B200-HOR", compile=searchers.compile_engine)
+    assert gpu.id == "B200-HOR" and gpu.m_min == 1 and gpu.applicable(5000)
+    wrapped = registry.b200_descriptor_for(mb.get_algorithm("SSEF"))
+    with pytest.raises(ApplicabilityError):
+        wrapped.compile(b"x" * 5)
+
+
+def test_plan_info_families():
+    cases = {1: "swar", 3: "swar", 4: "win4", 6: "win4", 7: "aligned", 1024: "aligned", 8192: "aligned"}
+    for m, fam in cases.items():
+        assert engine.Plan(b"\x05" * (m - 1) + b"\x07").info().family == fam
+    assert engine.Plan(b"a" * 100).info().periodic
+    assert not engine.Plan(b"a" * 99 + b"b").info().periodic
+    with pytest.raises(ValueError):
+        engine.Plan(b"x" * 8193)
+    with pytest.raises(ValueError):
+        engine.Plan(b"abc", family="aligned")
+    # anchor choice keeps the rare byte of a^(m-1)b inside the anchor window
+    info = engine.Plan(b"a" * 127 + b"b").info()
+    assert info.anchor <= 127 <= info.anchor + 6
+
+
+def test_inputs_mirror_reference_generators():
+    rng_bytes = np.random.Generator(np.random.PCG64(7)).integers(0, 4, size=10007, dtype=np.uint8)
+    assert np.array_equal(inputs.rand_text_np(4, 10007, 7, chunk=4096), rng_bytes)
+    assert inputs.sample_positions(1000, 10, 3, 5) == np.random.Generator(np.random.PCG64(5)).integers(0, 991, size=3).tolist()
+    assert inputs.derive_seed(1, "rand", 4) == inputs.derive_seed("1", "rand", "4")
+    t = inputs.dense_text(100000, 3)
+    assert (t != ord("a")).sum() == 100 and t.max() <= ord("z")
+    z = inputs.zipf_text(200000, 3)
+    assert z.min() >= 0x20 and z.max() <= 0x7E and abs((z == 0x20).mean() - 0.195) < 0.01
+
+
+def _shard_worker(rank, world, port, text, pats, q):
+    import torch.distributed as dist
+
+    import oracle
+    from paper_1012_2547_b200 import shard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = []
+    for p in pats:
+        lo, hi, rhi = shard.shard_bounds(len(text), len(p), world, rank)
+        local, off, total = shard.sharded_search(p, text[lo:rhi], len(text), lambda a, b: oracle.search(a, b))
+        res.append((rank, off, total, local.tolist()))
+    q.put(res)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_search_gloo(world):
+    import multiprocessing as mp
+    import socket
+
+    import oracle
+
+    rng = np.random.default_rng(world)
+    text = rng.integers(0, 2, 5000, dtype=np.uint8).tobytes()
+    pats = [text[100:104], text[2500:2540], b"\x00" * 3, b"\x01" * 11, text[4990:5000]]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, text, pats, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    by_rank = {o[0][0]: o for o in outs}
+    for k, p in enumerate(pats):
+        want = oracle.search(p, text).tolist()
+        merged, offs = [], []
+        for r in range(world):
+            rank, off, total, local = by_rank[r][k]
+            assert total == len(want)
+            assert off == len(merged)
+            merged += local
+        assert merged == want
