@@ -30,6 +30,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 // TMA 1D bulk copy global -> shared, completion counted on the mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile(
@@ -73,17 +76,18 @@ __device__ __forceinline__ uint32_t shr8(uint32_t lo, uint32_t hi, int k) {
 // -------------------------------------------------------------- filters
 // Each filter looks at the 16 staged bytes of one lane (w[0..3]) plus the
 // next word (w[4]) and returns the candidate mask over the lane's 16 bitmap
-// positions.  `any` is the cheap existence test; `mask` the exact bit set.
+// positions: a cheap existence test first, the exact bit set only on a hit.
 
-// K1 / m <= 3: byte d of x_k is zero iff t[v..v+m) == p (v = 4k+d).
+// K1 / m <= 3: byte d of x_k is zero iff t[v..v+m) == p (v = 4k + d).
+template <int M>
 struct FiltSWAR {
   __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
     uint32_t x[4], acc = 0;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       uint32_t v = w[k] ^ P.G[0];
-      if (P.m >= 2) v |= shr8(w[k], w[k + 1], 1) ^ P.G[1];
-      if (P.m >= 3) v |= shr8(w[k], w[k + 1], 2) ^ P.G[2];
+      if (M >= 2) v |= shr8(w[k], w[k + 1], 1) ^ P.G[1];
+      if (M >= 3) v |= shr8(w[k], w[k + 1], 2) ^ P.G[2];
       x[k] = v;
       acc |= (v - 0x01010101u) & ~v;
     }
@@ -144,110 +148,122 @@ __device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* p
   return true;
 }
 
-// Break bitmap of the tile: bit y set iff t[y] != t[y + per] (y relative to
-// the tile's first start position).  nbw[k] = first break at or after word k.
-__device__ void build_breaks(const uint8_t* Y0, int per, int nwords, uint32_t* brk, int32_t* nbw) {
-  for (int k = threadIdx.x; k < nwords; k += NT) {
-    const uint8_t* q = Y0 + 32 * k;
+// Per-warp break bitmap of a segment: bit q of word i set iff
+// t[y] != t[y + per] for y = y0 + 32 i + q (y relative to the segment's first
+// start position).  nbw[i] = first break at or after word i (relative to y0).
+__device__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* brk, int32_t* nbw) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < nwords; i += 32) {
+    const uint8_t* q = Yseg + 32 * i;
     uint32_t bits = 0;
 #pragma unroll 8
-    for (int i = 0; i < 32; i++) bits |= (uint32_t)(q[i] != q[i + per]) << i;
-    brk[k] = bits;
+    for (int b = 0; b < 32; b++) bits |= (uint32_t)(q[b] != q[b + per]) << b;
+    brk[i] = bits;
   }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    const int seg = (nwords + 31) / 32;
-    const int lo = lane * seg, hi = min(nwords, lo + seg);
-    int first = 0x7fffffff;
-    for (int k = hi - 1; k >= lo; k--)
-      if (brk[k]) first = 32 * k + __ffs(brk[k]) - 1;
-    // exclusive suffix-min over lanes
-    int suf = first;
+  __syncwarp();
+  const int seg = (nwords + 31) / 32;
+  const int lo = lane * seg, hi = min(nwords, lo + seg);
+  int first = 0x7fffffff;
+  for (int i = hi - 1; i >= lo; i--)
+    if (brk[i]) first = 32 * i + __ffs(brk[i]) - 1;
+  int suf = first;  // inclusive suffix-min over lanes
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      int o = __shfl_down_sync(0xffffffffu, suf, d);
-      if (lane + d < 32) suf = min(suf, o);
-    }
-    int excl = __shfl_down_sync(0xffffffffu, suf, 1);
-    if (lane == 31) excl = 0x7fffffff;
-    int cur = excl;
-    for (int k = hi - 1; k >= lo; k--) {
-      if (brk[k]) cur = 32 * k + __ffs(brk[k]) - 1;
-      nbw[k] = cur;
-    }
-    if (lane == 0) nbw[nwords] = 0x7fffffff;
+  for (int d = 1; d < 32; d <<= 1) {
+    int o = __shfl_down_sync(0xffffffffu, suf, d);
+    if (lane + d < 32) suf = min(suf, o);
   }
-  __syncthreads();
+  int cur = __shfl_down_sync(0xffffffffu, suf, 1);
+  if (lane == 31) cur = 0x7fffffff;
+  for (int i = hi - 1; i >= lo; i--) {
+    if (brk[i]) cur = 32 * i + __ffs(brk[i]) - 1;
+    nbw[i] = cur;
+  }
+  if (lane == 0) nbw[nwords] = 0x7fffffff;
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- kernel 1: scan
+// Warp-specialised: warp NWARP is the TMA producer (ticket -> bulk copies of
+// the tile+halo and of the pattern into a free stage), warps 0..NWARP-1 are
+// consumers that each own one SEG-position segment of every tile.  Stages are
+// handed over through full/empty mbarriers; there is no block-wide barrier in
+// the loop, so warps drift independently within the ring.
 template <class Filt>
-__global__ void __launch_bounds__(NT) scan_kernel(const ScanParams P) {
+__global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* stages = smem;
-  uint8_t* tail = smem + STAGES * P.stage_bytes;
-  uint64_t* bars = (uint64_t*)(tail + SM_BARS);
-  int64_t* stage_tk = (int64_t*)(tail + SM_TK);
-  uint32_t* bm = (uint32_t*)(tail + SM_BM);
-  uint32_t* brk = (uint32_t*)(tail + SM_BRK);
-  int32_t* nbw = (int32_t*)(tail + SM_BRK + 4 * P.brk_words);
-  uint32_t* red = (uint32_t*)(tail + SM_BRK + 8 * P.brk_words + 16);  // per-warp slots
-  uint8_t* spat = (uint8_t*)(red + 16);                                 // pattern copy
-
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
+  uint8_t* stages = smem + SM_STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  auto issue = [&](int s) {  // thread 0 only: next tile ticket -> TMA into stage s
-    unsigned long long tk = atomicAdd(&P.ticket[0], 1ULL);
-    if ((int64_t)tk >= P.total_tiles) {
-      stage_tk[s] = -1;
-      return;
-    }
-    stage_tk[s] = (int64_t)tk;
-    int64_t tau = (int64_t)tk % P.ntiles;
-    int64_t start = tau * TILE - P.pre;
-    int64_t end = tau * TILE + TILE + P.post;
-    int64_t cs = start < 0 ? 0 : start;
-    int64_t ce = end > P.nv16 ? P.nv16 : end;
-    uint32_t bytes = ce > cs ? (uint32_t)(ce - cs) : 0u;
-    uint8_t* dst = stages + s * P.stage_bytes + (cs - start);
-    mbar_expect_tx(&bars[s], bytes);
-    if (bytes) bulk_g2s(dst, P.text + cs, bytes, &bars[s]);
-  };
+  uint32_t* bm = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes) + warp * SEG_WORDS;
+  uint32_t* brk = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4) +
+                  warp * 2 * (P.brk_words + 4);
+  int32_t* nbw = reinterpret_cast<int32_t*>(brk + P.brk_words + 4);
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) mbar_init(&bars[s], 1);
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < STAGES; s++) issue(s);
   }
   __syncthreads();
 
-  int cur_k = -1;
+  if (warp == NWARP) {  // ---------------- producer
+    if (lane == 0) {
+      for (int it = 0;; it++) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
+        const unsigned long long tk = atomicAdd(&P.ticket[0], 1ULL);
+        if ((int64_t)tk >= P.total_tiles) {
+          hdr[s].tk = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        const int k = (int)((int64_t)tk / P.ntiles);
+        const int64_t tau = (int64_t)tk - (int64_t)k * P.ntiles;
+        hdr[s].tk = (int64_t)tk;
+        hdr[s].k = k;
+        hdr[s].tau = tau;
+        const int64_t start = tau * TILE - P.pre;
+        const int64_t end = tau * TILE + TILE + P.post;
+        const int64_t cs = start < 0 ? 0 : start;
+        const int64_t ce = end > P.nv16 ? P.nv16 : end;
+        const uint32_t tb = ce > cs ? (uint32_t)(ce - cs) : 0u;
+        const PatDev* pd = P.pats + k;
+        const uint32_t pb = (uint32_t)((pd->m + 15) & ~15LL);
+        uint8_t* st = stages + s * P.stage_bytes;
+        mbar_expect_tx(&full[s], tb + pb);
+        bulk_g2s(st, pd->bytes, pb, &full[s]);
+        if (tb) bulk_g2s(st + P.pat_cap + (cs - start), P.text + cs, tb, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int c0 = warp * SEG;  // this warp's segment of every tile
   for (int it = 0;; it++) {
     const int s = it % STAGES;
-    const int64_t tk = stage_tk[s];
+    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+    const int64_t tk = hdr[s].tk;
     if (tk < 0) break;
-    const int k = (int)(tk / P.ntiles);
-    const int64_t tau = tk % P.ntiles;
-    const int64_t B0 = tau * TILE;
+    const int k = hdr[s].k;
+    const int64_t B0 = hdr[s].tau * TILE;
     const PatDev pd = P.pats[k];
-    if (k != cur_k) {  // stage this pattern's bytes (used after the next barrier)
-      for (int i = tid; i < pd.m; i += NT) spat[i] = pd.bytes[i];
-      cur_k = k;
-    }
-    // valid bitmap range for this pattern: b - delta - off in [0, n - m]
-    const int64_t blo = P.off + pd.delta;
+    const uint8_t* spat = stages + s * P.stage_bytes;
+    const uint8_t* S = spat + P.pat_cap + P.pre;  // S[c] = virtual text byte B0 + c
+    const int64_t blo = P.off + pd.delta;               // valid bits: s = b - delta - off in [0, n-m]
     const int64_t bhi = P.off + pd.delta + P.n - pd.m;  // inclusive (may be < blo)
-    mbar_wait(&bars[s], (uint32_t)(it / STAGES) & 1u);
-    const uint8_t* S = stages + s * P.stage_bytes + P.pre;  // S[c] = virtual byte B0 + c
 
-    // ---- filter phase
+    // ---- filter: 4 rounds of 512 positions (16 per lane)
     bool anyc = false;
 #pragma unroll
-    for (int r = 0; r < ROUNDS; r++) {
-      const int c = warp * (ROUNDS * 512) + r * 512 + lane * 16;
-      uint4 X = *reinterpret_cast<const uint4*>(S + c);
-      uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
+    for (int r = 0; r < SEG / 512; r++) {
+      const int c = c0 + r * 512 + lane * 16;
+      const uint4 X = *reinterpret_cast<const uint4*>(S + c);
+      const uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
       uint32_t mk = Filt::run(w, pd);
       const int64_t b = B0 + c;
       if (b < blo || b + 15 > bhi) {  // boundary chunk: keep only valid positions
@@ -257,86 +273,78 @@ __global__ void __launch_bounds__(NT) scan_kernel(const ScanParams P) {
         mk &= vm;
       }
       anyc |= (mk != 0);
-      uint32_t other = __shfl_down_sync(0xffffffffu, mk, 1);
-      if (!(lane & 1)) bm[c >> 5] = mk | (other << 16);
+      const uint32_t other = __shfl_down_sync(0xffffffffu, mk, 1);
+      if (!(lane & 1)) bm[r * 16 + (lane >> 1)] = mk | (other << 16);
     }
-    const int any_tile = __syncthreads_or(anyc);
-
-    uint32_t tile_cnt = 0;
-    if (any_tile) {
-      // ---- verify phase
+    uint32_t cnt = 0;
+    if (__any_sync(0xffffffffu, anyc)) {
+      __syncwarp();
+      uint32_t w0 = bm[2 * lane], w1 = bm[2 * lane + 1];
+      // ---- verify (exact filters skip this)
       if (!pd.exact) {
-        const int m = (int)pd.m;
-        const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of bit rel
-        if (pd.periodic) {
-          const int nwords = (TILE + pd.L + 31) / 32;
-          build_breaks(Y0, pd.per, nwords, brk, nbw);
-        }
-        for (int wi = 2 * tid; wi < 2 * tid + 2; wi++) {
-          uint32_t cw = bm[wi], mw = 0;
+        const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
+        if (pd.periodic) warp_breaks(Y0 + c0, pd.per, (SEG + pd.L + 31) / 32, brk, nbw);
+        uint32_t ws[2] = {w0, w1};
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          uint32_t cw = ws[h], mw = 0;
           while (cw) {
             const int i = __ffs(cw) - 1;
             cw &= cw - 1;
-            const int rel = 32 * wi + i;
+            const int rel = c0 + 32 * (2 * lane + h) + i;
             bool ok;
             if (pd.periodic) {
               ok = verify_direct(Y0 + rel, spat, pd.per);
               if (ok) {
-                const uint32_t x = brk[rel >> 5] >> (rel & 31);
-                const int nb = x ? rel + __ffs(x) - 1 : nbw[(rel >> 5) + 1];
-                ok = nb >= rel + pd.L;
+                const int q = rel - c0;
+                const uint32_t x = brk[q >> 5] >> (q & 31);
+                const int nb = x ? q + __ffs(x) - 1 : nbw[(q >> 5) + 1];
+                ok = nb >= q + pd.L;
               }
             } else {
-              ok = verify_direct(Y0 + rel, spat, m);
+              ok = verify_direct(Y0 + rel, spat, (int)pd.m);
             }
             if (ok) mw |= 1u << i;
           }
-          bm[wi] = mw;
+          ws[h] = mw;
         }
-        __syncthreads();
+        w0 = ws[0];
+        w1 = ws[1];
       }
-      // ---- count + compact store
-      const uint32_t w0 = bm[2 * tid], w1 = bm[2 * tid + 1];
+      // ---- count + compact store (segment g = tile * NWARP + warp)
       const uint32_t c2 = __popc(w0) + __popc(w1);
       uint32_t inc = c2;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
         if (lane >= d) inc += o;
       }
-      if (lane == 31) red[warp] = inc;
-      __syncthreads();
-      uint32_t before = 0;
-      for (int q = 0; q < NWARP; q++) {
-        const uint32_t v = red[q];
-        tile_cnt += v;
-        before += q < warp ? v : 0;
-      }
-      if (tile_cnt <= LIST_CAP) {
-        uint32_t j = before + inc - c2;
-        uint16_t* L = P.lists + (size_t)tk * LIST_CAP;
+      cnt = __shfl_sync(0xffffffffu, inc, 31);
+      const int64_t g = tk * NWARP + warp;
+      if (cnt <= LIST_CAP) {
+        uint32_t j = inc - c2;
+        uint16_t* L = P.lists + g * LIST_CAP;
         uint64_t bits = ((uint64_t)w1 << 32) | w0;
         while (bits) {
           const int i = __ffsll((long long)bits) - 1;
           bits &= bits - 1;
-          L[j++] = (uint16_t)(64 * tid + i);
+          L[j++] = (uint16_t)(c0 + 64 * lane + i);
         }
-      } else {
-        uint2* dst = reinterpret_cast<uint2*>(P.bitmaps + (size_t)tk * BM_WORDS);
-        dst[tid] = make_uint2(w0, w1);
+      } else if (cnt) {
+        reinterpret_cast<uint2*>(P.bitmaps + g * SEG_WORDS)[lane] = make_uint2(w0, w1);
       }
     }
-    if (tid == 0) P.counts[tk] = tile_cnt;
-    __syncthreads();  // stage s, bm, red free
-    if (tid == 0) issue(s);
+    if (lane == 0) P.counts[tk * NWARP + warp] = cnt;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
-// ------------------------------------------------ kernel 2: tile offsets (scan)
-// Exclusive scan of per-tile counts in SCAN_CHUNK pieces; chunk order = ticket
-// order taken at CTA start (no prefetch), so each chunk only waits on chunks
-// that are already running -- the decoupled look-back never stalls on a
-// queued predecessor.
+// ------------------------------------------------ kernel 2: segment offsets (scan)
+// Exclusive scan of per-segment counts in SCAN_CHUNK pieces; chunk order =
+// ticket order taken at CTA start (no prefetch), so each chunk only waits on
+// chunks already running -- the decoupled look-back never stalls on a queued
+// predecessor.
 __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   __shared__ int64_t wsum[NWARP];
   __shared__ int64_t s_excl;
@@ -345,6 +353,7 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   if (tid == 0) s_chunk = (int64_t)atomicAdd(&P.ticket[1], 1ULL);
   __syncthreads();
   const int64_t ch = s_chunk;
+  const int64_t nseg = P.total_tiles * NWARP;
   const int64_t base = ch * SCAN_CHUNK;
   constexpr int PER = SCAN_CHUNK / NT;  // 16 counts per thread
   uint32_t v[PER];
@@ -352,13 +361,13 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
 #pragma unroll
   for (int q = 0; q < PER; q++) {
     const int64_t t = base + (int64_t)tid * PER + q;
-    v[q] = t < P.total_tiles ? P.counts[t] : 0u;
+    v[q] = t < nseg ? P.counts[t] : 0u;
     tsum += v[q];
   }
   int64_t inc = tsum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    int64_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    const int64_t o = __shfl_up_sync(0xffffffffu, inc, d);
     if (lane >= d) inc += o;
   }
   if (lane == 31) wsum[warp] = inc;
@@ -404,60 +413,64 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   }
   __syncthreads();
   int64_t run = s_excl + wbefore + inc - tsum;
+  const int64_t seg_per_pat = P.ntiles * NWARP;
 #pragma unroll
   for (int q = 0; q < PER; q++) {
     const int64_t t = base + (int64_t)tid * PER + q;
-    if (t < P.total_tiles) {
+    if (t < nseg) {
       P.toff[t] = run;
-      if (t % P.ntiles == P.ntiles - 1) P.offsets_plus1[t / P.ntiles] = run + v[q];
+      if (t % seg_per_pat == seg_per_pat - 1) P.offsets_plus1[t / seg_per_pat] = run + v[q];
     }
     run += v[q];
   }
 }
 
 // ------------------------------------------------ kernel 3: expansion
-// One warp per tile (grid-stride).  Sparse tiles copy their uint16 list;
-// dense tiles expand the bitmap 32 words at a time through a per-warp smem
-// staging buffer so every global store is a coalesced 256-byte run.
+// One warp per segment (grid-stride).  Sparse segments copy their uint16
+// list; dense ones expand the 64-word bitmap 32 words at a time through a
+// per-warp smem staging buffer so every global store is a coalesced run.
 constexpr int EXP_WARPS = 4;
 __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
   __shared__ int64_t stage[EXP_WARPS][1024];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * EXP_WARPS + warp;
   const int64_t nw = (int64_t)gridDim.x * EXP_WARPS;
+  const int64_t nseg = P.total_tiles * NWARP;
   int cur_k = -1;
   int64_t shift = 0;
-  for (int64_t t = gw; t < P.total_tiles; t += nw) {
-    const uint32_t c = P.counts[t];
+  for (int64_t g = gw; g < nseg; g += nw) {
+    const uint32_t c = P.counts[g];
     if (c == 0) continue;
-    const int k = (int)(t / P.ntiles);
+    const int64_t tile = g / NWARP;
+    const int k = (int)(tile / P.ntiles);
     if (k != cur_k) {
       shift = P.pats[k].delta + P.off;
       cur_k = k;
     }
-    const int64_t pos0 = (t % P.ntiles) * TILE - shift;
-    const int64_t o = P.toff[t];
+    const int64_t pos0 = (tile % P.ntiles) * TILE - shift;  // tile-relative offsets below
+    const int64_t o = P.toff[g];
     if (o >= P.cap) continue;
     if (c <= LIST_CAP) {
-      if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + P.lists[t * LIST_CAP + lane];
+      if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + P.lists[g * LIST_CAP + lane];
       continue;
     }
-    const uint32_t* bmw = P.bitmaps + (size_t)t * BM_WORDS;
+    const uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
+    const int64_t segpos = pos0 + (g % NWARP) * SEG;
     int64_t w_out = o;
-    for (int wb = 0; wb < BM_WORDS; wb += 32) {
+    for (int wb = 0; wb < SEG_WORDS; wb += 32) {
       const uint32_t x = bmw[wb + lane];
       const uint32_t pc = __popc(x);
       uint32_t inc = pc;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
         if (lane >= d) inc += v;
       }
       const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
       if (total == 0) continue;
       uint32_t j = inc - pc;
       uint32_t xx = x;
-      const int64_t pb = pos0 + 32 * (wb + lane);
+      const int64_t pb = segpos + 32 * (wb + lane);
       while (xx) {
         const int i = __ffs(xx) - 1;
         xx &= xx - 1;
@@ -734,15 +747,17 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
   P.K = K;
   P.pre = pre;
   P.post = post;
-  P.stage_bytes = (pre + TILE + post + 127) & ~127;
-  P.brk_words = (((TILE + maxL + 63) / 32) + 3) & ~3;
-  P.pat_cap = (int)((maxm + 15) & ~15) + 16;
-  const int64_t T = P.total_tiles;
+  P.pat_cap = (int)((maxm + 15) & ~15);
+  P.stage_bytes = (P.pat_cap + pre + TILE + post + 127) & ~127;
+  bool any_periodic = false;
+  for (int k = 0; k < K; k++) any_periodic |= h_pats[k].periodic != 0;
+  P.brk_words = any_periodic ? ((((SEG + maxL + 31) / 32) + 1 + 3) & ~3) : 0;
+  const int64_t T = P.total_tiles * NWARP;  // segments
   const int64_t nchunks = (T + SCAN_CHUNK - 1) / SCAN_CHUNK;
   int rc;
   if ((rc = grow(&c->counts, &c->counts_cap, T, "counts"))) return rc;
   if ((rc = grow(&c->lists, &c->lists_cap, T * LIST_CAP, "lists"))) return rc;
-  if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * BM_WORDS, "bitmaps"))) return rc;
+  if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * SEG_WORDS, "bitmaps"))) return rc;
   if ((rc = grow(&c->toff, &c->toff_cap, T, "tile offsets"))) return rc;
   if (nchunks > c->state_cap || c->epoch >= (1u << 24) - 1) {
     if ((rc = grow(&c->state, &c->state_cap, nchunks, "look-back state"))) return rc;
@@ -762,7 +777,8 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
   P.out_base = out_base;
   CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 2 * sizeof(unsigned long long), st));
 
-  size_t smem = (size_t)STAGES * P.stage_bytes + SM_BRK + 8 * P.brk_words + 16 + 4 * 16 + P.pat_cap;
+  size_t smem = (size_t)SM_STAGES + (size_t)STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
+                (size_t)NWARP * 2 * (P.brk_words + 4) * 4;
   static std::mutex mu;
   static bool attr_done = false;
   static size_t occ_smem = 0;
@@ -775,14 +791,14 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
       attr_done = true;
     }
     if (occ_smem != smem) {
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val, scan_kernel<F>, NT, smem));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val, scan_kernel<F>, NT + 32, smem));
       occ_smem = smem;
     }
     per_sm = occ_val;
   }
   if (per_sm < 1) return fail(MB_ECUDA, "scan kernel does not fit on an SM");
-  int64_t grid = std::min<int64_t>(T, (int64_t)c->nsm * per_sm);
-  scan_kernel<F><<<(int)grid, NT, smem, st>>>(P);
+  int64_t grid = std::min<int64_t>(P.total_tiles, (int64_t)c->nsm * per_sm);
+  scan_kernel<F><<<(int)grid, NT + 32, smem, st>>>(P);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   offsets_kernel<<<(int)nchunks, NT, 0, st>>>(P);
@@ -801,7 +817,12 @@ static int dispatch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K
                     int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, const int64_t* out_base,
                     cudaStream_t st) {
   switch (h_pats[0].family) {
-    case MB_FAM_SWAR: return launch_scan<FiltSWAR>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
+    case MB_FAM_SWAR:
+      if (h_pats[0].m == 1)
+        return launch_scan<FiltSWAR<1>>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
+      if (h_pats[0].m == 2)
+        return launch_scan<FiltSWAR<2>>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
+      return launch_scan<FiltSWAR<3>>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
     case MB_FAM_WIN4: return launch_scan<FiltWIN4>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
     case MB_FAM_ALIGNED:
       return launch_scan<FiltALIGNED>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
@@ -858,7 +879,9 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
   int k0 = 0;
   while (k0 < K) {
     int k1 = k0 + 1;
-    while (k1 < K && c->h_pats[k1].family == c->h_pats[k0].family) k1++;
+    while (k1 < K && c->h_pats[k1].family == c->h_pats[k0].family &&
+           (c->h_pats[k0].family != MB_FAM_SWAR || c->h_pats[k1].m == c->h_pats[k0].m))
+      k1++;
     // group g starts where group g-1 ended: d_offsets[k0] is its output base
     int rc = dispatch(c, c->d_pats + k0, c->h_pats.data() + k0, k1 - k0, d_text, n, d_out, cap,
                       d_offsets + 1 + k0, d_offsets + k0, st);

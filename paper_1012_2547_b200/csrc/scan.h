@@ -27,21 +27,27 @@
 
 namespace mb {
 
-constexpr int TILE = 16384;       // bitmap positions per tile
-constexpr int NT = 256;           // threads per CTA (8 warps)
-constexpr int NWARP = NT / 32;
+constexpr int TILE = 16384;       // bitmap positions per tile (one TMA stage)
+constexpr int NWARP = 8;          // consumer warps; warp NWARP is the TMA producer
+constexpr int NT = NWARP * 32;    // consumer threads
+constexpr int SEG = TILE / NWARP; // positions per consumer-warp segment
+constexpr int SEG_WORDS = SEG / 32;
 constexpr int STAGES = 4;         // TMA ring depth
-constexpr int ROUNDS = TILE / (NWARP * 512);  // 512 positions per warp-round
-constexpr int BM_WORDS = TILE / 32;
-constexpr int LIST_CAP = 32;      // sparse tiles keep <= 32 uint16 offsets
-constexpr int SCAN_CHUNK = 4096;  // tile counts per offsets_kernel CTA
+constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offsets
+constexpr int SCAN_CHUNK = 4096;  // segment counts per offsets_kernel CTA
 
-// shared-memory tail after the stage ring: [bars][tickets][bitmap][breaks]
-// [next-break][reduction][pattern]; break/pattern sizes are per launch.
-constexpr int SM_BARS = 0;
-constexpr int SM_TK = SM_BARS + 8 * STAGES;
-constexpr int SM_BM = SM_TK + 8 * STAGES;
-constexpr int SM_BRK = SM_BM + 4 * BM_WORDS;
+struct StageHdr {
+  int64_t tk;   // global tile ticket (-1: no more work)
+  int64_t tau;  // tile index within the pattern
+  int32_t k;    // pattern index
+  int32_t pad;
+};
+// dynamic smem: [hdr x STAGES][full x STAGES][empty x STAGES] | stages | per-warp
+// segment bitmaps | per-warp break / next-break arrays
+constexpr int SM_HDR = 0;
+constexpr int SM_FULL = SM_HDR + 32 * STAGES;
+constexpr int SM_EMPTY = SM_FULL + 8 * STAGES;
+constexpr int SM_STAGES = 256;  // stage s: [pattern pat_cap][text pre + TILE + post]
 
 struct ScanParams {
   const uint8_t* text;  // 16-byte aligned base (text pointer rounded down)
@@ -54,13 +60,13 @@ struct ScanParams {
   int K;
   int pre, post;        // max margins over the batch
   int stage_bytes;
-  int brk_words;        // break-bitmap words (multiple of 4)
+  int brk_words;        // per-warp break-bitmap words (multiple of 4; 0 if no periodic pattern)
   int pat_cap;          // pattern bytes reserved in smem (multiple of 16)
   unsigned long long* ticket;  // [0]: scan tiles, [1]: offsets chunks
-  uint32_t* counts;     // per tile
-  uint16_t* lists;      // per tile LIST_CAP entries
-  uint32_t* bitmaps;    // per tile BM_WORDS words (dense tiles only)
-  int64_t* toff;        // per tile exclusive output offset
+  uint32_t* counts;     // per segment (tile * NWARP + warp)
+  uint16_t* lists;      // per segment LIST_CAP tile-relative offsets
+  uint32_t* bitmaps;    // per segment SEG_WORDS words (dense segments only)
+  int64_t* toff;        // per segment exclusive output offset
   uint64_t* state;      // look-back flags of offsets_kernel (per chunk)
   uint32_t epoch;
   int64_t* out;         // positions (may be null: count only)
