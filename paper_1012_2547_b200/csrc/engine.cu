@@ -244,44 +244,58 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
 
   // ------------------------------------------------------------ consumers
   const int c0 = warp * SEG;  // this warp's segment of every tile
+  int cur_k = -1;
+  PatDev pd;
+  int64_t blo = 0, bhi = -1;
   for (int it = 0;; it++) {
     const int s = it % STAGES;
     mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
     const int64_t tk = hdr[s].tk;
     if (tk < 0) break;
     const int k = hdr[s].k;
+    if (k != cur_k) {  // per-pattern parameters stay in registers across tiles
+      pd = P.pats[k];
+      blo = P.off + pd.delta;               // valid bits: s = b - delta - off in [0, n-m]
+      bhi = P.off + pd.delta + P.n - pd.m;  // inclusive (may be < blo)
+      cur_k = k;
+    }
     const int64_t B0 = hdr[s].tau * TILE;
-    const PatDev pd = P.pats[k];
     const uint8_t* spat = stages + s * P.stage_bytes;
     const uint8_t* S = spat + P.pat_cap + P.pre;  // S[c] = virtual text byte B0 + c
-    const int64_t blo = P.off + pd.delta;               // valid bits: s = b - delta - off in [0, n-m]
-    const int64_t bhi = P.off + pd.delta + P.n - pd.m;  // inclusive (may be < blo)
 
-    // ---- filter: 4 rounds of 512 positions (16 per lane)
+    // ---- filter (fast path): 4 rounds of 512 positions, 16 per lane, masks kept in registers
+    uint32_t mk[SEG / 512];
     bool anyc = false;
 #pragma unroll
     for (int r = 0; r < SEG / 512; r++) {
       const int c = c0 + r * 512 + lane * 16;
       const uint4 X = *reinterpret_cast<const uint4*>(S + c);
       const uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
-      uint32_t mk = Filt::run(w, pd);
-      const int64_t b = B0 + c;
-      if (b < blo || b + 15 > bhi) {  // boundary chunk: keep only valid positions
-        uint32_t vm = 0;
-        for (int i = 0; i < 16; i++)
-          if (b + i >= blo && b + i <= bhi) vm |= 1u << i;
-        mk &= vm;
-      }
-      anyc |= (mk != 0);
-      const uint32_t other = __shfl_down_sync(0xffffffffu, mk, 1);
-      if (!(lane & 1)) bm[r * 16 + (lane >> 1)] = mk | (other << 16);
+      mk[r] = Filt::run(w, pd);
+      anyc |= (mk[r] != 0);
     }
     uint32_t cnt = 0;
     if (__any_sync(0xffffffffu, anyc)) {
+      // ---- slow path: validity mask at text edges, linear segment bitmap
+      const int64_t segb = B0 + c0;
+      const bool interior = segb >= blo && segb + SEG - 1 <= bhi;
+#pragma unroll
+      for (int r = 0; r < SEG / 512; r++) {
+        uint32_t m = mk[r];
+        if (!interior) {
+          const int64_t b = segb + r * 512 + lane * 16;
+          uint32_t vm = 0;
+          for (int i = 0; i < 16; i++)
+            if (b + i >= blo && b + i <= bhi) vm |= 1u << i;
+          m &= vm;
+        }
+        const uint32_t other = __shfl_down_sync(0xffffffffu, m, 1);
+        if (!(lane & 1)) bm[r * 16 + (lane >> 1)] = m | (other << 16);
+      }
       __syncwarp();
       uint32_t w0 = bm[2 * lane], w1 = bm[2 * lane + 1];
       // ---- verify (exact filters skip this)
-      if (!pd.exact) {
+      if (!pd.exact && __any_sync(0xffffffffu, (w0 | w1) != 0)) {
         const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
         if (pd.periodic) warp_breaks(Y0 + c0, pd.per, (SEG + pd.L + 31) / 32, brk, nbw);
         uint32_t ws[2] = {w0, w1};
@@ -330,13 +344,15 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
           bits &= bits - 1;
           L[j++] = (uint16_t)(c0 + 64 * lane + i);
         }
-      } else if (cnt) {
+      } else {
         reinterpret_cast<uint2*>(P.bitmaps + g * SEG_WORDS)[lane] = make_uint2(w0, w1);
       }
+      __syncwarp();
     }
-    if (lane == 0) P.counts[tk * NWARP + warp] = cnt;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) {
+      P.counts[tk * NWARP + warp] = (uint16_t)cnt;
+      mbar_arrive(&empty[s]);
+    }
   }
 }
 
@@ -361,7 +377,7 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
 #pragma unroll
   for (int q = 0; q < PER; q++) {
     const int64_t t = base + (int64_t)tid * PER + q;
-    v[q] = t < nseg ? P.counts[t] : 0u;
+    v[q] = t < nseg ? (uint32_t)P.counts[t] : 0u;
     tsum += v[q];
   }
   int64_t inc = tsum;
@@ -418,7 +434,7 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   for (int q = 0; q < PER; q++) {
     const int64_t t = base + (int64_t)tid * PER + q;
     if (t < nseg) {
-      P.toff[t] = run;
+      if (v[q]) P.toff[t] = run;  // read only for non-empty segments
       if (t % seg_per_pat == seg_per_pat - 1) P.offsets_plus1[t / seg_per_pat] = run + v[q];
     }
     run += v[q];
@@ -563,7 +579,7 @@ struct mb_ctx {
   int nsm = 0;
   uint64_t* state = nullptr;
   int64_t state_cap = 0;
-  uint32_t* counts = nullptr;
+  uint16_t* counts = nullptr;
   int64_t counts_cap = 0;
   uint16_t* lists = nullptr;
   int64_t lists_cap = 0;

@@ -63,7 +63,7 @@ struct ScanParams {
   int brk_words;        // per-warp break-bitmap words (multiple of 4; 0 if no periodic pattern)
   int pat_cap;          // pattern bytes reserved in smem (multiple of 16)
   unsigned long long* ticket;  // [0]: scan tiles, [1]: offsets chunks
-  uint32_t* counts;     // per segment (tile * NWARP + warp)
+  uint16_t* counts;     // per segment (tile * NWARP + warp); <= SEG
   uint16_t* lists;      // per segment LIST_CAP tile-relative offsets
   uint32_t* bitmaps;    // per segment SEG_WORDS words (dense segments only)
   int64_t* toff;        // per segment exclusive output offset
