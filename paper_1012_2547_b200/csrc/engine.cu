@@ -442,61 +442,69 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
 }
 
 // ------------------------------------------------ kernel 3: expansion
-// One warp per segment (grid-stride).  Sparse segments copy their uint16
-// list; dense ones expand the 64-word bitmap 32 words at a time through a
-// per-warp smem staging buffer so every global store is a coalesced run.
+// A warp takes 32 consecutive segments per step: one coalesced load of their
+// counts, a ballot of the non-empty ones, then a warp-cooperative expansion of
+// each: sparse segments copy their uint16 list, dense ones expand the 64-word
+// bitmap 32 words at a time through a per-warp smem staging buffer so every
+// global store is a coalesced run.
 constexpr int EXP_WARPS = 4;
 __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
   __shared__ int64_t stage[EXP_WARPS][1024];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * EXP_WARPS + warp;
-  const int64_t nw = (int64_t)gridDim.x * EXP_WARPS;
   const int64_t nseg = P.total_tiles * NWARP;
+  const int64_t ngroups = (nseg + 31) / 32;
   int cur_k = -1;
   int64_t shift = 0;
-  for (int64_t g = gw; g < nseg; g += nw) {
-    const uint32_t c = P.counts[g];
-    if (c == 0) continue;
-    const int64_t tile = g / NWARP;
-    const int k = (int)(tile / P.ntiles);
-    if (k != cur_k) {
-      shift = P.pats[k].delta + P.off;
-      cur_k = k;
-    }
-    const int64_t pos0 = (tile % P.ntiles) * TILE - shift;  // tile-relative offsets below
-    const int64_t o = P.toff[g];
-    if (o >= P.cap) continue;
-    if (c <= LIST_CAP) {
-      if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + P.lists[g * LIST_CAP + lane];
-      continue;
-    }
-    const uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
-    const int64_t segpos = pos0 + (g % NWARP) * SEG;
-    int64_t w_out = o;
-    for (int wb = 0; wb < SEG_WORDS; wb += 32) {
-      const uint32_t x = bmw[wb + lane];
-      const uint32_t pc = __popc(x);
-      uint32_t inc = pc;
+  for (int64_t grp = (int64_t)blockIdx.x * EXP_WARPS + warp; grp < ngroups; grp += (int64_t)gridDim.x * EXP_WARPS) {
+    const int64_t gl = grp * 32 + lane;
+    const uint32_t myc = gl < nseg ? (uint32_t)P.counts[gl] : 0u;
+    uint32_t todo = __ballot_sync(0xffffffffu, myc != 0);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t g = grp * 32 + src;
+      const uint32_t c = __shfl_sync(0xffffffffu, myc, src);
+      const int64_t tile = g / NWARP;
+      const int k = (int)(tile / P.ntiles);
+      if (k != cur_k) {
+        shift = P.pats[k].delta + P.off;
+        cur_k = k;
+      }
+      const int64_t pos0 = (tile % P.ntiles) * TILE - shift;  // tile-relative offsets below
+      const int64_t o = P.toff[g];
+      if (o >= P.cap) continue;
+      if (c <= LIST_CAP) {
+        if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + P.lists[g * LIST_CAP + lane];
+        continue;
+      }
+      const uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
+      const int64_t segpos = pos0 + (g % NWARP) * SEG;
+      int64_t w_out = o;
+      for (int wb = 0; wb < SEG_WORDS; wb += 32) {
+        const uint32_t x = bmw[wb + lane];
+        const uint32_t pc = __popc(x);
+        uint32_t inc = pc;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += v;
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
+          if (lane >= d) inc += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+        if (total == 0) continue;
+        uint32_t j = inc - pc;
+        uint32_t xx = x;
+        const int64_t pb = segpos + 32 * (wb + lane);
+        while (xx) {
+          const int i = __ffs(xx) - 1;
+          xx &= xx - 1;
+          stage[warp][j++] = pb + i;
+        }
+        __syncwarp();
+        for (uint32_t q = lane; q < total; q += 32)
+          if (w_out + q < P.cap) P.out[w_out + q] = stage[warp][q];
+        __syncwarp();
+        w_out += total;
       }
-      const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-      if (total == 0) continue;
-      uint32_t j = inc - pc;
-      uint32_t xx = x;
-      const int64_t pb = segpos + 32 * (wb + lane);
-      while (xx) {
-        const int i = __ffs(xx) - 1;
-        xx &= xx - 1;
-        stage[warp][j++] = pb + i;
-      }
-      __syncwarp();
-      for (uint32_t q = lane; q < total; q += 32)
-        if (w_out + q < P.cap) P.out[w_out + q] = stage[warp][q];
-      __syncwarp();
-      w_out += total;
     }
   }
 }
@@ -821,7 +829,7 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   if (d_out && cap > 0) {
-    int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS, (int64_t)c->nsm * 16);
+    int64_t eg = std::min<int64_t>((T + 32 * EXP_WARPS - 1) / (32 * EXP_WARPS), (int64_t)c->nsm * 16);
     expand_kernel<<<(int)eg, EXP_WARPS * 32, 0, st>>>(P);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
