@@ -1,0 +1,100 @@
+"""GPU parity at the BASELINE.json configs' full sizes.
+
+Exact parity against the C oracle (oracle/, threaded over halo-overlapped
+chunks -- SURVEY.md 8(c)) plus size-independent properties: positions strictly
+increasing, every reported window equal to the pattern (host check), planted
+occurrences present, batched == single-pattern results.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1012_2547_b200 import engine, inputs
+from paper_1012_2547_b200.inputs import derive_seed
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+THREADS = os.cpu_count() or 4
+
+
+def props(pos: np.ndarray, p: bytes, t: np.ndarray):
+    assert pos.dtype == np.int64
+    if pos.size:
+        assert np.all(np.diff(pos) > 0), "positions not strictly increasing"
+        assert pos[0] >= 0 and pos[-1] <= t.size - len(p)
+        pv = np.frombuffer(p, dtype=np.uint8)
+        sample = pos if pos.size <= 4096 else pos[np.linspace(0, pos.size - 1, 4096).astype(np.int64)]
+        win = t[sample[:, None] + np.arange(len(p))[None, :]]
+        assert np.all(win == pv[None, :]), "a reported window differs from the pattern"
+
+
+def test_config1_full(cuda):
+    t, pats = inputs.config1()
+    got = engine.find(engine.Plan(pats[0]), t).cpu().numpy()
+    assert np.array_equal(got, oracle.search(pats[0], t))
+    props(got, pats[0], t)
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 8, 16, 32, 64, 128])
+def test_config2_full_sigma(cuda, sigma):
+    """All 10 m x 500 patterns of one sigma: one batched launch per m; exact per pattern."""
+    t = inputs.config2_text(sigma)
+    d = torch.from_numpy(t).cuda()
+    for m in inputs.DEFAULT_LENGTHS:
+        pats = inputs.config2_patterns(t, sigma, m)
+        pos, offs = engine.find_batch([engine.Plan(p) for p in pats], d)
+        pos = pos.cpu().numpy()
+        offs = offs.numpy()
+        want_counts = [oracle.count(p, t, threads=THREADS) for p in pats]
+        assert np.array_equal(np.diff(offs), want_counts), (sigma, m)
+        for k in range(0, len(pats), 97):  # full position check on a spread of patterns
+            assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(pats[k], t, threads=THREADS))
+        for k in range(0, len(pats), 50):
+            props(pos[offs[k] : offs[k + 1]], pats[k], t)
+
+
+def test_config3_full(cuda):
+    t = inputs.config3()
+    d = torch.from_numpy(t).cuda()
+    for m in (4, 16, 64, 256, 1024):
+        pats = inputs.config3_patterns(t, m)
+        pos, offs = engine.find_batch([engine.Plan(p) for p in pats], d)
+        pos = pos.cpu().numpy()
+        offs = offs.numpy()
+        for k in range(len(pats)):
+            want = oracle.search(pats[k], t, threads=THREADS) if k % 25 == 0 else None
+            got = pos[offs[k] : offs[k + 1]]
+            if want is not None:
+                assert np.array_equal(got, want), (m, k)
+            else:
+                assert got.size == oracle.count(pats[k], t, threads=THREADS), (m, k)
+        props(pos[offs[0] : offs[1]], pats[0], t)
+
+
+def test_config5_full(cuda):
+    t = inputs.config5()
+    d = torch.from_numpy(t).cuda()
+    for p in inputs.config5_patterns():
+        got = engine.find(engine.Plan(p), d).cpu().numpy()
+        want = oracle.search(p, t, "SO", threads=THREADS)  # BF is O(n*m) on a^m
+        assert np.array_equal(got, want), (len(p), p[-1:])
+        props(got, p, t)
+
+
+def test_config4_full(cuda):
+    n = 16 << 30
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    t = host.numpy()
+    inputs.config4_text(n, out=t)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d.copy_(host)
+    for p in inputs.config4_patterns(t):
+        got = engine.find(engine.Plan(p), d).cpu().numpy()
+        assert np.array_equal(got, oracle.search(p, t, threads=THREADS)), len(p)
+        props(got, p, t)
+    del d
+    torch.cuda.empty_cache()
