@@ -46,6 +46,7 @@ extern "C" {
 #define MB_FAM_WIN4 2    /* K1, 4 <= m <= 6: packed 32-bit window compare */
 #define MB_FAM_ALIGNED 3 /* K1/K3, m >= 7: aligned-word q-gram anchor + smem verify */
 #define MB_FAM_SHIFTOR 4 /* K2, m <= 64: per-thread bit-parallel shift-or */
+#define MB_FAM_SAMPLED 5 /* K3, m >= 272: sampled q-gram hash filter, sublinear DRAM reads */
 
 typedef struct mb_plan mb_plan;
 typedef struct mb_ctx mb_ctx;
@@ -63,6 +64,8 @@ typedef struct {
   int delta;      /* bitmap index shift: bit b <-> position b - delta */
   int period;     /* smallest period of the pattern (== m if aperiodic) */
   int periodic;   /* 1 if verification uses the period/break-run test */
+  int stride;     /* K3 sampling stride S in bytes (0 unless family == MB_FAM_SAMPLED) */
+  int gram;       /* K3 gram length q in bytes (0 unless family == MB_FAM_SAMPLED) */
 } mb_plan_info_t;
 
 /* ---- plans: the compile_X(p) analogue (comparison.py:70-352 preprocessing) ---- */

@@ -215,15 +215,16 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
       for (int it = 0;; it++) {
         const int s = it % STAGES;
         if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
-        const unsigned long long tk = atomicAdd(&P.ticket[0], 1ULL);
-        if ((int64_t)tk >= P.total_tiles) {
+        const unsigned long long tk = atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
+        if ((int64_t)tk >= P.group_tiles) {
           hdr[s].tk = -1;
           mbar_arrive(&full[s]);
           break;
         }
-        const int k = (int)((int64_t)tk / P.ntiles);
-        const int64_t tau = (int64_t)tk - (int64_t)k * P.ntiles;
-        hdr[s].tk = (int64_t)tk;
+        const int kg = (int)((int64_t)tk / P.ntiles);
+        const int k = P.plist ? P.plist[kg] : kg;  // this launch's family group -> batch index
+        const int64_t tau = (int64_t)tk - (int64_t)kg * P.ntiles;
+        hdr[s].tk = (int64_t)k * P.ntiles + tau;   // global tile id (segment index base)
         hdr[s].k = k;
         hdr[s].tau = tau;
         const int64_t start = tau * TILE - P.pre;
@@ -356,6 +357,155 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   }
 }
 
+// ------------------------------------------------ kernel 1b: sampled q-gram scan (K3)
+// For long, non-periodic patterns: only the q-gram at every
+// S-th text position is read (one 128-byte DRAM line per sample instead of S
+// bytes); a bloom filter + bucketed offset lists in smem map a gram to the
+// pattern offsets j where it occurs, each giving a candidate start s = x - j
+// that is verified against the text in global memory.  A warp owns SMP_SEGS
+// consecutive segments (8 tiles) and reads every sample whose bit range
+// [S*i, S*i + S) meets them, 4 independent 16-byte loads per lane in flight.
+// Output (segment counts, uint16 tile-relative lists) is the scan kernel's, so
+// offsets/expand are shared.
+constexpr int SMP_SEGS = 64;     // segments per warp unit (= 8 tiles)
+constexpr int SMP_LIST = 1024;   // per-warp match capacity per unit (bound: 131072/per + 2 < 1024)
+constexpr int SMP_ILP = 4;       // samples per lane per batch
+__device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& pd, const uint32_t* bloom,
+                                             const uint16_t* bstart, const uint16_t* bent, const uint8_t* spat,
+                                             const uint32_t* w, int64_t x, int64_t ulo, int64_t uhi, int64_t blo,
+                                             int64_t bhi, uint32_t* found) {
+  const uint32_t h = gram_mix(w, pd.q >> 2);
+  if (!((bloom[h >> 21] >> ((h >> 16) & 31)) & 1u)) return 0;
+  int nf = 0;
+  const uint32_t bk = h >> (32 - pd.B);
+  for (int e = bstart[bk]; e < bstart[bk + 1] && nf < 4; e++) {
+    const int j = bent[e];
+    bool eq = true;
+    for (int c = 0; c < pd.q && eq; c++) eq = spat[j + c] == (uint8_t)(w[c >> 2] >> (8 * (c & 3)));
+    if (!eq) continue;
+    const int64_t sv = x - j;           // virtual start
+    const int64_t bit = sv + pd.delta;  // = x - j + S - 1, inside [x, x + S)
+    if (bit < ulo || bit >= uhi || bit < blo || bit > bhi) continue;
+    const uint8_t* tp = P.text + sv;
+    bool ok = true;
+    for (int c = 0; c < pd.m && ok; c++) ok = __ldg(tp + c) == spat[c];
+    if (ok) found[nf++] = (uint32_t)(bit - ulo);
+  }
+  return nf;
+}
+
+__global__ void __launch_bounds__(NT) sampled_kernel(const ScanParams P) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* bloom = reinterpret_cast<uint32_t*>(smem);                 // 2048 words
+  uint16_t* bstart = reinterpret_cast<uint16_t*>(smem + 8192);         // <= 1025
+  uint16_t* bent = reinterpret_cast<uint16_t*>(smem + 8192 + 2064);    // <= 4096
+  uint32_t* lists = reinterpret_cast<uint32_t*>(smem + 8192 + 2064 + 8192);  // [NWARP][SMP_LIST]
+  int64_t* s_ticket = reinterpret_cast<int64_t*>(lists + NWARP * SMP_LIST);
+  uint8_t* spat = reinterpret_cast<uint8_t*>(s_ticket + 2);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t segs = P.ntiles * NWARP;                                   // segments per pattern
+  const int64_t wunits = (segs + SMP_SEGS - 1) / SMP_SEGS;                 // warp units per pattern
+  const int64_t units = (wunits + NWARP - 1) / NWARP;                      // CTA units per pattern
+  const int64_t total = units * P.group_k;
+  int cur_k = -1;
+  PatDev pd;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_ticket[0] = (int64_t)atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
+    __syncthreads();
+    const int64_t t = s_ticket[0];
+    if (t >= total) break;
+    const int kg = (int)(t / units);
+    const int k = P.plist ? P.plist[kg] : kg;  // family group -> batch index
+    const int64_t u = t - (int64_t)kg * units;
+    if (k != cur_k) {  // load this pattern's tables (uniform across the CTA)
+      pd = P.pats[k];
+      const int nb = (1 << pd.B) + 1;
+      for (int i = tid; i < 2048; i += NT) bloom[i] = pd.bloom[i];
+      for (int i = tid; i < nb; i += NT) bstart[i] = pd.bstart[i];
+      for (int i = tid; i < pd.S; i += NT) bent[i] = pd.bent[i];
+      for (int i = tid; i < pd.m; i += NT) spat[i] = pd.bytes[i];
+      cur_k = k;
+      __syncthreads();
+    }
+    const int64_t wu = u * NWARP + warp;
+    if (wu >= wunits) continue;
+    const int64_t seg0 = wu * SMP_SEGS;
+    const int nsegs = (int)(segs - seg0 < SMP_SEGS ? segs - seg0 : SMP_SEGS);
+    const int64_t ulo = seg0 * SEG, uhi = ulo + (int64_t)nsegs * SEG;  // bits of this unit
+    const int64_t blo = P.off + pd.delta, bhi = P.off + pd.delta + P.n - pd.m;
+    const int64_t S = pd.S;
+    const int q = pd.q;
+    const int64_t tlimit = P.off + P.n;  // virtual end of the text
+    const int64_t i0 = ulo / S, i1 = (uhi - 1) / S;
+    uint32_t* wl = lists + warp * SMP_LIST;
+    uint32_t nmatch = 0;
+    for (int64_t ib = i0; ib <= i1; ib += 32 * SMP_ILP) {
+      uint4 g[SMP_ILP], g2[SMP_ILP];
+#pragma unroll
+      for (int r = 0; r < SMP_ILP; r++) {  // issue every load of the batch first
+        const int64_t i = ib + r * 32 + lane;
+        const int64_t x = S * i;
+        if (i <= i1 && x + q <= tlimit) {
+          g[r] = __ldcs(reinterpret_cast<const uint4*>(P.text + x));
+          if (q == 32) g2[r] = __ldcs(reinterpret_cast<const uint4*>(P.text + x + 16));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < SMP_ILP; r++) {
+        const int64_t i = ib + r * 32 + lane;
+        const int64_t x = S * i;
+        uint32_t found[4];
+        int nf = 0;
+        if (i <= i1 && x + q <= tlimit) {
+          const uint32_t w[8] = {g[r].x, g[r].y, g[r].z, g[r].w, g2[r].x, g2[r].y, g2[r].z, g2[r].w};
+          nf = sampled_probe(P, pd, bloom, bstart, bent, spat, w, x, ulo, uhi, blo, bhi, found);
+        }
+        // ascending: lanes own disjoint increasing bit ranges; bucket entries are in ascending start order
+        const uint32_t any = __ballot_sync(0xffffffffu, nf != 0);
+        if (any) {
+          uint32_t inc = nf;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+          }
+          const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+          const uint32_t pos = nmatch + inc - nf;
+          for (int f = 0; f < nf; f++)
+            if (pos + f < SMP_LIST) wl[pos + f] = found[f];
+          nmatch += tot;
+        }
+      }
+    }
+    if (nmatch > SMP_LIST) __trap();  // impossible for the plans that choose K3 (see plan.cpp)
+    __syncwarp();
+    // per-segment counts and uint16 tile-relative lists, as scan_kernel writes them
+    for (int sl = lane; sl < nsegs; sl += 32) {
+      const uint32_t lo = sl * SEG, hi = lo + SEG;
+      uint32_t c = 0, first = 0;
+      for (uint32_t e = 0; e < nmatch; e++) {
+        const uint32_t v = wl[e];
+        if (v < lo) first = e + 1;
+        else if (v < hi) c++;
+      }
+      const int64_t g = (int64_t)k * segs + seg0 + sl;
+      P.counts[g] = (uint16_t)c;
+      const uint32_t tile_rel = (uint32_t)(((seg0 + sl) % NWARP) * SEG);  // segment start within its tile
+      if (c <= LIST_CAP) {
+        for (uint32_t e = 0; e < c; e++) P.lists[g * LIST_CAP + e] = (uint16_t)(wl[first + e] - lo + tile_rel);
+      } else {
+        uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
+        for (int q2 = 0; q2 < SEG_WORDS; q2++) bmw[q2] = 0;
+        for (uint32_t e = 0; e < c; e++) {
+          const uint32_t r = wl[first + e] - lo;
+          bmw[r >> 5] |= 1u << (r & 31);
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------ kernel 2: segment offsets (scan)
 // Exclusive scan of per-segment counts in SCAN_CHUNK pieces; chunk order =
 // ticket order taken at CTA start (no prefetch), so each chunk only waits on
@@ -366,7 +516,7 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   __shared__ int64_t s_excl;
   __shared__ int64_t s_chunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_chunk = (int64_t)atomicAdd(&P.ticket[1], 1ULL);
+  if (tid == 0) s_chunk = (int64_t)atomicAdd(&P.ticket[TICKET_OFFSETS], 1ULL);
   __syncthreads();
   const int64_t ch = s_chunk;
   const int64_t nseg = P.total_tiles * NWARP;
@@ -547,8 +697,9 @@ struct mb_plan {
   // device copy, uploaded on first use (plans are creatable without a GPU so
   // the host tables can be inspected anywhere); guarded for shared use
   mutable std::mutex mu;
-  mutable uint8_t* d_bytes = nullptr;
+  mutable uint8_t* d_buf = nullptr;  // [pattern | bloom | bucket starts | bucket entries]
   mutable PatDev* d_dev = nullptr;
+  mutable PatDev dview;              // PatDev with device pointers (host copy)
   mutable int device = -1;
 };
 
@@ -562,21 +713,36 @@ static int plan_device(const mb_plan* p, const PatDev** out) {
     return MB_OK;
   }
   if (p->d_dev) {  // used from another device: re-upload there
-    cudaFree(p->d_bytes);
+    cudaFree(p->d_buf);
     cudaFree(p->d_dev);
-    p->d_bytes = nullptr;
+    p->d_buf = nullptr;
     p->d_dev = nullptr;
   }
-  if (cudaMalloc(&p->d_bytes, p->h.m + 16) != cudaSuccess) return fail(MB_ENOMEM, "plan bytes alloc");
+  const PlanHost& h = p->h;
+  const size_t pat_bytes = (size_t)((h.m + 16 + 15) & ~15LL);
+  const size_t bloom_bytes = h.bloom.size() * 4;
+  const size_t bs_bytes = (h.bstart.size() * 2 + 15) & ~(size_t)15;
+  const size_t be_bytes = (h.bent.size() * 2 + 15) & ~(size_t)15;
+  const size_t total = pat_bytes + bloom_bytes + bs_bytes + be_bytes;
+  if (cudaMalloc(&p->d_buf, total) != cudaSuccess) return fail(MB_ENOMEM, "plan upload alloc");
   if (cudaMalloc(&p->d_dev, sizeof(PatDev)) != cudaSuccess) {
-    cudaFree(p->d_bytes);
-    p->d_bytes = nullptr;
+    cudaFree(p->d_buf);
+    p->d_buf = nullptr;
     return fail(MB_ENOMEM, "plan params alloc");
   }
-  CUDA_TRY(cudaMemcpy(p->d_bytes, p->h.pat.data(), p->h.m, cudaMemcpyHostToDevice));
-  PatDev d = p->h.dev;
-  d.bytes = p->d_bytes;
+  std::vector<uint8_t> img(total, 0);
+  memcpy(img.data(), h.pat.data(), h.m);
+  if (bloom_bytes) memcpy(img.data() + pat_bytes, h.bloom.data(), bloom_bytes);
+  if (!h.bstart.empty()) memcpy(img.data() + pat_bytes + bloom_bytes, h.bstart.data(), h.bstart.size() * 2);
+  if (!h.bent.empty()) memcpy(img.data() + pat_bytes + bloom_bytes + bs_bytes, h.bent.data(), h.bent.size() * 2);
+  CUDA_TRY(cudaMemcpy(p->d_buf, img.data(), total, cudaMemcpyHostToDevice));
+  PatDev d = h.dev;
+  d.bytes = p->d_buf;
+  d.bloom = bloom_bytes ? reinterpret_cast<const uint32_t*>(p->d_buf + pat_bytes) : nullptr;
+  d.bstart = bloom_bytes ? reinterpret_cast<const uint16_t*>(p->d_buf + pat_bytes + bloom_bytes) : nullptr;
+  d.bent = bloom_bytes ? reinterpret_cast<const uint16_t*>(p->d_buf + pat_bytes + bloom_bytes + bs_bytes) : nullptr;
   CUDA_TRY(cudaMemcpy(p->d_dev, &d, sizeof(PatDev), cudaMemcpyHostToDevice));
+  p->dview = d;
   p->device = dev;
   *out = p->d_dev;
   return MB_OK;
@@ -595,6 +761,9 @@ struct mb_ctx {
   int64_t bitmaps_cap = 0;
   int64_t* toff = nullptr;
   int64_t toff_cap = 0;
+  int32_t* plist = nullptr;
+  int64_t plist_cap = 0;
+  std::vector<int32_t> h_plist;
   uint32_t epoch = 0;
   unsigned long long* ticket = nullptr;
   PatDev* d_pats = nullptr;
@@ -639,7 +808,7 @@ int mb_plan_create(const uint8_t* h_pattern, int64_t m, const mb_plan_opts* opts
 
 void mb_plan_destroy(mb_plan* p) {
   if (!p) return;
-  cudaFree(p->d_bytes);
+  cudaFree(p->d_buf);
   cudaFree(p->d_dev);
   delete p;
 }
@@ -652,6 +821,8 @@ int mb_plan_info(const mb_plan* p, mb_plan_info_t* info) {
   info->delta = p->h.dev.delta;
   info->period = p->h.period;
   info->periodic = p->h.dev.periodic;
+  info->stride = p->h.family == MB_FAM_SAMPLED ? p->h.dev.S : 0;
+  info->gram = p->h.family == MB_FAM_SAMPLED ? p->h.dev.q : 0;
   return MB_OK;
 }
 
@@ -693,7 +864,7 @@ int mb_ctx_create(int device, mb_ctx** out) {
   mb_ctx* c = new mb_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMalloc(&c->ticket, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+  if (cudaMalloc(&c->ticket, 8 * sizeof(unsigned long long)) != cudaSuccess) {
     delete c;
     return fail(MB_ENOMEM, "ticket alloc");
   }
@@ -708,6 +879,7 @@ void mb_ctx_destroy(mb_ctx* c) {
   cudaFree(c->lists);
   cudaFree(c->bitmaps);
   cudaFree(c->toff);
+  cudaFree(c->plist);
   cudaFree(c->ticket);
   cudaFree(c->d_pats);
   cudaFree(c->d_text);
@@ -734,48 +906,128 @@ static int grow(T** p, int64_t* cap, int64_t need, const char* what) {
   return MB_OK;
 }
 
+struct SampledTag {};
+
+// Launch the count-producing kernel of one family group: patterns
+// plist[0..gk) of the batch (indices into P.pats), ticket counter `slot`.
 template <class F>
-static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
-                       int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, const int64_t* out_base,
-                       cudaStream_t st) {
+static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int32_t* h_idx, const int32_t* d_idx,
+                        int gk, int slot, cudaStream_t st) {
+  int pre = 0, post = 0, maxL = 0;
+  int64_t maxm = 1;
+  bool any_periodic = false;
+  for (int i = 0; i < gk; i++) {
+    const PatDev& d = h_pats[h_idx[i]];
+    maxm = std::max<int64_t>(maxm, d.m);
+    if (d.periodic) maxL = std::max(maxL, d.L), any_periodic = true;
+    pre = std::max(pre, d.pre);
+    post = std::max(post, d.post);
+  }
+  P.plist = d_idx;
+  P.group_k = gk;
+  P.group_tiles = P.ntiles * gk;
+  P.ticket_slot = slot;
+  P.pre = pre;
+  P.post = post;
+  P.pat_cap = (int)((maxm + 15) & ~15);
+  P.stage_bytes = (P.pat_cap + pre + TILE + post + 127) & ~127;
+  P.brk_words = any_periodic ? ((((SEG + maxL + 31) / 32) + 1 + 3) & ~3) : 0;
+  if constexpr (std::is_same<F, SampledTag>::value) {
+    const size_t smem_s = 8192 + 2064 + 8192 + NWARP * SMP_LIST * 4 + 16 + P.pat_cap + 16;
+    static std::mutex mu_s;
+    static bool attr_s = false;
+    static size_t occ_smem_s = 0;
+    static int occ_s = 0;
+    int per_sm_s = 0;
+    {
+      std::lock_guard<std::mutex> g(mu_s);
+      if (!attr_s) {
+        CUDA_TRY(cudaFuncSetAttribute(sampled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_s = true;
+      }
+      if (occ_smem_s != smem_s) {
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, sampled_kernel, NT, smem_s));
+        occ_smem_s = smem_s;
+      }
+      per_sm_s = occ_s;
+    }
+    if (per_sm_s < 1) return fail(MB_ECUDA, "sampled kernel does not fit on an SM");
+    const int64_t wunits = (P.ntiles * NWARP + SMP_SEGS - 1) / SMP_SEGS;
+    const int64_t units = ((wunits + NWARP - 1) / NWARP) * gk;
+    const int64_t grid_s = std::min<int64_t>(units, (int64_t)c->nsm * per_sm_s);
+    sampled_kernel<<<(int)grid_s, NT, smem_s, st>>>(P);
+  } else {
+    const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
+                        (size_t)NWARP * 2 * (P.brk_words + 4) * 4;
+    static std::mutex mu;
+    static bool attr_done = false;
+    static size_t occ_smem = 0;
+    static int occ_val = 0;
+    int per_sm = 0;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (!attr_done) {
+        CUDA_TRY(cudaFuncSetAttribute(scan_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_done = true;
+      }
+      if (occ_smem != smem) {
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val, scan_kernel<F>, NT + 32, smem));
+        occ_smem = smem;
+      }
+      per_sm = occ_val;
+    }
+    if (per_sm < 1) return fail(MB_ECUDA, "scan kernel does not fit on an SM");
+    const int64_t grid = std::min<int64_t>(P.group_tiles, (int64_t)c->nsm * per_sm);
+    scan_kernel<F><<<(int)grid, NT + 32, smem, st>>>(P);
+  }
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+// family key: patterns sharing a key share one count-kernel launch
+static int family_key(const PatDev& d) {
+  return d.family == MB_FAM_SWAR ? (int)(10 + d.m) : d.family;
+}
+
+static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, const int32_t* h_idx,
+                         const int32_t* d_idx, int gk, int slot, cudaStream_t st) {
+  const PatDev& d = h_pats[h_idx[0]];
+  switch (d.family) {
+    case MB_FAM_SWAR:
+      if (d.m == 1) return launch_group<FiltSWAR<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+      if (d.m == 2) return launch_group<FiltSWAR<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+      return launch_group<FiltSWAR<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+    case MB_FAM_WIN4: return launch_group<FiltWIN4>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+    case MB_FAM_ALIGNED: return launch_group<FiltALIGNED>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+    case MB_FAM_SAMPLED: return launch_group<SampledTag>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+  }
+  return fail(MB_EINVAL, "unknown kernel family");
+}
+
+// One search (K = 1) or batch: per family group one count kernel, then one
+// offsets and one expand launch over all K patterns' segments, so the output
+// is CSR in the caller's pattern order whatever the family mix.
+static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
+                      int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st) {
   ScanParams P;
   memset(&P, 0, sizeof(P));
-  uintptr_t addr = (uintptr_t)d_text;
+  const uintptr_t addr = (uintptr_t)d_text;
   P.text = (const uint8_t*)(addr & ~(uintptr_t)15);
   P.off = (int64_t)(addr & 15);
   P.n = n;
   P.nv16 = (P.off + n + 15) & ~(int64_t)15;
   int64_t nbits = 0;
-  int pre = 0, post = 0, maxL = 0;
-  int64_t maxm = 1;
-  for (int k = 0; k < K; k++) {
-    const PatDev& d = h_pats[k];
-    maxm = std::max<int64_t>(maxm, d.m);
-    if (d.periodic) maxL = std::max(maxL, d.L);
-    if (d.m <= n) nbits = std::max<int64_t>(nbits, P.off + d.delta + n - d.m + 1);
-    pre = std::max(pre, d.pre);
-    post = std::max(post, d.post);
-  }
-  if (nbits == 0) {  // every pattern longer than the text: offsets stay at the base
-    if (out_base) {
-      for (int k = 0; k < K; k++)
-        CUDA_TRY(cudaMemcpyAsync(offsets_plus1 + k, out_base, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    } else {
-      CUDA_TRY(cudaMemsetAsync(offsets_plus1, 0, sizeof(int64_t) * K, st));
-    }
+  for (int k = 0; k < K; k++)
+    if (h_pats[k].m <= n) nbits = std::max<int64_t>(nbits, P.off + h_pats[k].delta + n - h_pats[k].m + 1);
+  if (nbits == 0) {  // every pattern longer than the text
+    CUDA_TRY(cudaMemsetAsync(offsets_plus1, 0, sizeof(int64_t) * K, st));
     return MB_OK;
   }
   P.ntiles = (nbits + TILE - 1) / TILE;
   P.total_tiles = P.ntiles * K;
   P.pats = d_pats;
   P.K = K;
-  P.pre = pre;
-  P.post = post;
-  P.pat_cap = (int)((maxm + 15) & ~15);
-  P.stage_bytes = (P.pat_cap + pre + TILE + post + 127) & ~127;
-  bool any_periodic = false;
-  for (int k = 0; k < K; k++) any_periodic |= h_pats[k].periodic != 0;
-  P.brk_words = any_periodic ? ((((SEG + maxL + 31) / 32) + 1 + 3) & ~3) : 0;
   const int64_t T = P.total_tiles * NWARP;  // segments
   const int64_t nchunks = (T + SCAN_CHUNK - 1) / SCAN_CHUNK;
   int rc;
@@ -798,60 +1050,47 @@ static int launch_scan(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, in
   P.out = d_out;
   P.cap = d_out ? cap : 0;
   P.offsets_plus1 = offsets_plus1;
-  P.out_base = out_base;
-  CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 2 * sizeof(unsigned long long), st));
+  P.out_base = nullptr;
+  CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 8 * sizeof(unsigned long long), st));
 
-  size_t smem = (size_t)SM_STAGES + (size_t)STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
-                (size_t)NWARP * 2 * (P.brk_words + 4) * 4;
-  static std::mutex mu;
-  static bool attr_done = false;
-  static size_t occ_smem = 0;
-  static int occ_val = 0;
-  int per_sm = 0;
-  {
-    std::lock_guard<std::mutex> g(mu);
-    if (!attr_done) {
-      CUDA_TRY(cudaFuncSetAttribute(scan_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr_done = true;
+  // group patterns by family key (stable); a single group needs no index list
+  std::vector<int> keys;
+  std::vector<std::vector<int32_t>> groups;
+  for (int k = 0; k < K; k++) {
+    const int key = family_key(h_pats[k]);
+    size_t g = 0;
+    while (g < keys.size() && keys[g] != key) g++;
+    if (g == keys.size()) {
+      keys.push_back(key);
+      groups.emplace_back();
     }
-    if (occ_smem != smem) {
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val, scan_kernel<F>, NT + 32, smem));
-      occ_smem = smem;
-    }
-    per_sm = occ_val;
+    groups[g].push_back(k);
   }
-  if (per_sm < 1) return fail(MB_ECUDA, "scan kernel does not fit on an SM");
-  int64_t grid = std::min<int64_t>(P.total_tiles, (int64_t)c->nsm * per_sm);
-  scan_kernel<F><<<(int)grid, NT + 32, smem, st>>>(P);
-  g_launches++;
-  CUDA_TRY(cudaGetLastError());
+  if ((int)groups.size() > MAX_GROUPS) return fail(MB_EINVAL, "too many kernel families in one batch");
+  if (groups.size() == 1) {
+    if ((rc = launch_family(c, P, h_pats, groups[0].data(), nullptr, K, 0, st))) return rc;
+  } else {
+    if ((rc = grow(&c->plist, &c->plist_cap, K, "family index lists"))) return rc;
+    c->h_plist.clear();
+    for (auto& g : groups) c->h_plist.insert(c->h_plist.end(), g.begin(), g.end());
+    CUDA_TRY(cudaMemcpyAsync(c->plist, c->h_plist.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, st));
+    int base = 0;
+    for (size_t g = 0; g < groups.size(); g++) {
+      if ((rc = launch_family(c, P, h_pats, groups[g].data(), c->plist + base, (int)groups[g].size(), (int)g, st)))
+        return rc;
+      base += (int)groups[g].size();
+    }
+  }
   offsets_kernel<<<(int)nchunks, NT, 0, st>>>(P);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   if (d_out && cap > 0) {
-    int64_t eg = std::min<int64_t>((T + 32 * EXP_WARPS - 1) / (32 * EXP_WARPS), (int64_t)c->nsm * 16);
+    const int64_t eg = std::min<int64_t>((T + 32 * EXP_WARPS - 1) / (32 * EXP_WARPS), (int64_t)c->nsm * 16);
     expand_kernel<<<(int)eg, EXP_WARPS * 32, 0, st>>>(P);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
   }
   return MB_OK;
-}
-
-static int dispatch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
-                    int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, const int64_t* out_base,
-                    cudaStream_t st) {
-  switch (h_pats[0].family) {
-    case MB_FAM_SWAR:
-      if (h_pats[0].m == 1)
-        return launch_scan<FiltSWAR<1>>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
-      if (h_pats[0].m == 2)
-        return launch_scan<FiltSWAR<2>>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
-      return launch_scan<FiltSWAR<3>>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
-    case MB_FAM_WIN4: return launch_scan<FiltWIN4>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
-    case MB_FAM_ALIGNED:
-      return launch_scan<FiltALIGNED>(c, d_pats, h_pats, K, d_text, n, d_out, cap, offsets_plus1, out_base, st);
-  }
-  return fail(MB_EINVAL, "unknown kernel family");
 }
 
 extern "C" {
@@ -869,7 +1108,7 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
   const PatDev* dd = nullptr;
   int rc = plan_device(p, &dd);
   if (rc) return rc;
-  return dispatch(c, dd, &p->h.dev, 1, d_text, n, d_out, cap, d_count, nullptr, st);
+  return run_search(c, dd, &p->dview, 1, d_text, n, d_out, cap, d_count, st);
 }
 
 int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* d_text, int64_t n,
@@ -887,8 +1126,7 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
     const PatDev* dd = nullptr;
     int rc = plan_device(plans[k], &dd);
     if (rc) return rc;
-    c->h_pats[k] = plans[k]->h.dev;
-    c->h_pats[k].bytes = plans[k]->d_bytes;
+    c->h_pats[k] = plans[k]->dview;
   }
   if (K > c->pats_cap) {
     cudaFree(c->d_pats);
@@ -900,19 +1138,7 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
     c->pats_cap = K;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice, st));
-  int k0 = 0;
-  while (k0 < K) {
-    int k1 = k0 + 1;
-    while (k1 < K && c->h_pats[k1].family == c->h_pats[k0].family &&
-           (c->h_pats[k0].family != MB_FAM_SWAR || c->h_pats[k1].m == c->h_pats[k0].m))
-      k1++;
-    // group g starts where group g-1 ended: d_offsets[k0] is its output base
-    int rc = dispatch(c, c->d_pats + k0, c->h_pats.data() + k0, k1 - k0, d_text, n, d_out, cap,
-                      d_offsets + 1 + k0, d_offsets + k0, st);
-    if (rc) return rc;
-    k0 = k1;
-  }
-  return MB_OK;
+  return run_search(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets + 1, st);
 }
 
 int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, void* stream) {

@@ -11,6 +11,7 @@
 //     smallest period, staged-tile margins.
 #include "plan.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -87,6 +88,69 @@ static int choose_anchor(const uint8_t* p, int64_t m, int len, const int64_t* hi
   return best;
 }
 
+// K3 sampled q-gram filter: every occurrence of p contains the
+// q-gram at exactly one text position x = S*i (S <= m - q + 1), at pattern offset
+// j = x - s in [0, S).  The plan hashes the grams p[j..j+q), j in [0, S), into a
+// 65536-bit bloom filter and bucketed offset lists.  Chosen only where sampling
+// saves DRAM traffic (S >= 256: the fetch granule is a 128-byte line) and the
+// filter stays selective: q * entropy(p) >= log2(S) + 12 bits and no gram occurs
+// at more than 4 of the S offsets (periodic patterns keep the full scan).
+static bool build_sampled(const uint8_t* pat, int64_t m, PlanHost* ph) {
+  if (m < 272) return false;
+  double cnt[256] = {0}, H = 0;
+  for (int64_t i = 0; i < m; i++) cnt[pat[i]] += 1;
+  for (int c = 0; c < 256; c++)
+    if (cnt[c] > 0) H -= cnt[c] / m * std::log2(cnt[c] / m);
+  for (int q : {4, 8, 16, 32}) {
+    int64_t S = ((m - q + 1) / 16) * 16;
+    if (S > 4096) S = 4096;
+    if (S < 256) return false;
+    if (q * H < std::log2((double)S) + 12) continue;
+    const int nw = q / 4;
+    int B = 1;
+    while ((1 << B) < 2 * S && B < 10) B++;
+    std::vector<uint32_t> hs(S);
+    for (int64_t j = 0; j < S; j++) {
+      uint32_t w[8];
+      for (int k = 0; k < nw; k++) w[k] = load_le32(pat + j + 4 * k);
+      hs[j] = gram_mix(w, nw);
+    }
+    // multiplicity of identical grams among the S offsets
+    std::vector<int64_t> order(S);
+    for (int64_t j = 0; j < S; j++) order[j] = j;
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      int c = memcmp(pat + a, pat + b, q);
+      return c < 0 || (c == 0 && a < b);
+    });
+    int maxmul = 1, run = 1;
+    for (int64_t i = 1; i < S; i++) {
+      run = memcmp(pat + order[i - 1], pat + order[i], q) == 0 ? run + 1 : 1;
+      maxmul = std::max(maxmul, run);
+    }
+    if (maxmul > 4) continue;
+    ph->bloom.assign(2048, 0u);
+    ph->bstart.assign((1 << B) + 1, 0);
+    ph->bent.assign(S, 0);
+    std::vector<int> bc(1 << B, 0);
+    for (int64_t j = 0; j < S; j++) {
+      ph->bloom[hs[j] >> 21] |= 1u << ((hs[j] >> 16) & 31);
+      bc[hs[j] >> (32 - B)]++;
+    }
+    for (int b = 0; b < (1 << B); b++) ph->bstart[b + 1] = (uint16_t)(ph->bstart[b] + bc[b]);
+    std::vector<int> fillp(ph->bstart.begin(), ph->bstart.end() - 1);
+    for (int64_t j = S - 1; j >= 0; j--) {  // descending j inside a bucket -> ascending start
+      int b = hs[j] >> (32 - B);
+      ph->bent[fillp[b]++] = (uint16_t)j;
+    }
+    PatDev& d = ph->dev;
+    d.S = (int32_t)S;
+    d.q = q;
+    d.B = B;
+    return true;
+  }
+  return false;
+}
+
 int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost* ph, std::string* err) {
   if (m < 1) {
     *err = "pattern must have length >= 1";
@@ -114,6 +178,24 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
     else
       fam = MB_FAM_ALIGNED;
   }
+  bool sampled_ok = false;
+  if (fam == MB_FAM_AUTO || fam == MB_FAM_ALIGNED || fam == MB_FAM_SAMPLED) {
+    PlanHost tmp;
+    sampled_ok = build_sampled(pat, m, &tmp);
+    if (sampled_ok && (opts == nullptr || opts->family == MB_FAM_AUTO || opts->family == MB_FAM_SAMPLED)) {
+      fam = MB_FAM_SAMPLED;
+      ph->bloom.swap(tmp.bloom);
+      ph->bstart.swap(tmp.bstart);
+      ph->bent.swap(tmp.bent);
+      ph->dev.S = tmp.dev.S;
+      ph->dev.q = tmp.dev.q;
+      ph->dev.B = tmp.dev.B;
+    }
+  }
+  if (opts && opts->family == MB_FAM_SAMPLED && !sampled_ok) {
+    *err = "sampled q-gram family does not apply to this pattern (m < 272, low entropy or periodic)";
+    return MB_EINVAL;
+  }
   if ((fam == MB_FAM_SWAR && m > 3) || (fam == MB_FAM_WIN4 && m < 4) ||
       (fam == MB_FAM_ALIGNED && m < 7) || (fam == MB_FAM_SHIFTOR && m > 64)) {
     *err = "requested kernel family does not apply at this pattern length";
@@ -121,7 +203,13 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
   }
   ph->family = fam;
   PatDev& d = ph->dev;
-  memset(&d, 0, sizeof(d));
+  {
+    const int32_t S = d.S, q = d.q, B = d.B;
+    memset(&d, 0, sizeof(d));
+    d.S = S;
+    d.q = q;
+    d.B = B;
+  }
   d.m = m;
   d.per = ph->period;
   d.family = fam;
@@ -160,6 +248,12 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       ph->anchor = 0;
       d.delta = 0;
       d.exact = 1;
+      break;
+    case MB_FAM_SAMPLED:
+      // bit b of the sample at x = S*i covers b in [x, x + S): b = s + S - 1
+      ph->anchor = 0;
+      d.delta = d.S - 1;
+      d.exact = 0;
       break;
   }
   d.anchor = ph->anchor;

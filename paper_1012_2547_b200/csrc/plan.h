@@ -1,6 +1,10 @@
 // plan.h -- shared plan structures (host preprocessing <-> device scan).
 #pragma once
 #include <stdint.h>
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#endif
 
 #include <string>
 #include <vector>
@@ -24,7 +28,22 @@ struct PatDev {
   int32_t pre;      // staged bytes before the tile's first bit (multiple of 16)
   int32_t post;     // staged bytes after the tile's last bit (multiple of 16)
   uint32_t G[4];    // filter words (family specific)
+  // K3 sampled q-gram filter (family MB_FAM_SAMPLED)
+  int32_t S;        // sampling stride in bytes (multiple of 16, >= 256)
+  int32_t q;        // gram bytes (4, 8, 16 or 32)
+  int32_t B;        // log2 of the bucket count
+  int32_t pad_;
+  const uint32_t* bloom;   // 65536-bit filter over gram hashes (device)
+  const uint16_t* bstart;  // (1 << B) + 1 bucket starts (device)
+  const uint16_t* bent;    // S entries: pattern offsets j sorted by bucket (device)
 };
+
+// gram hash shared by host table build and device lookup (words little-endian)
+__host__ __device__ inline uint32_t gram_mix(const uint32_t* w, int nw) {
+  uint32_t h = 0x9E3779B9u;
+  for (int i = 0; i < nw; i++) h = (h ^ w[i]) * 0x85EBCA6Bu + (h >> 15);
+  return h ^ (h >> 13);
+}
 
 struct PlanHost {
   int64_t m = 0;
@@ -36,6 +55,9 @@ struct PlanHost {
   int family = 0;
   int anchor = 0;
   PatDev dev;
+  // K3 tables (host copies; uploaded with the pattern)
+  std::vector<uint32_t> bloom;
+  std::vector<uint16_t> bstart, bent;
 };
 
 void horspool_table(const uint8_t* p, int64_t m, int64_t* tbl);

@@ -35,6 +35,8 @@ constexpr int SEG_WORDS = SEG / 32;
 constexpr int STAGES = 4;         // TMA ring depth
 constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offsets
 constexpr int SCAN_CHUNK = 4096;  // segment counts per offsets_kernel CTA
+constexpr int TICKET_OFFSETS = 7; // ticket slot of offsets_kernel (slots 0..6: family groups)
+constexpr int MAX_GROUPS = 7;
 
 struct StageHdr {
   int64_t tk;   // global tile ticket (-1: no more work)
@@ -62,7 +64,11 @@ struct ScanParams {
   int stage_bytes;
   int brk_words;        // per-warp break-bitmap words (multiple of 4; 0 if no periodic pattern)
   int pat_cap;          // pattern bytes reserved in smem (multiple of 16)
-  unsigned long long* ticket;  // [0]: scan tiles, [1]: offsets chunks
+  unsigned long long* ticket;  // [g]: tile tickets of family group g, [TICKET_OFFSETS]: scan chunks
+  int ticket_slot;      // this launch's ticket counter
+  const int32_t* plist; // family group -> batch pattern index (null: identity)
+  int group_k;          // patterns in this launch's family group
+  int64_t group_tiles;  // group_k * ntiles
   uint16_t* counts;     // per segment (tile * NWARP + warp); <= SEG
   uint16_t* lists;      // per segment LIST_CAP tile-relative offsets
   uint32_t* bitmaps;    // per segment SEG_WORDS words (dense segments only)

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libmatchb200.so")
 
 MB_OK, MB_EINVAL, MB_ENOMEM, MB_ECUDA, MB_EOVERFLOW = 0, 1, 2, 3, 4
 MB_MAX_M = 8192
-FAMILIES = {"auto": 0, "swar": 1, "win4": 2, "aligned": 3, "shiftor": 4}
+FAMILIES = {"auto": 0, "swar": 1, "win4": 2, "aligned": 3, "shiftor": 4, "sampled": 5}
 FAMILY_NAMES = {v: k for k, v in FAMILIES.items()}
 
 # every symbol include/matchb200.h declares
@@ -44,7 +44,8 @@ class _PlanOpts(ctypes.Structure):
 
 class _PlanInfo(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int64), ("family", ctypes.c_int), ("anchor", ctypes.c_int),
-                ("delta", ctypes.c_int), ("period", ctypes.c_int), ("periodic", ctypes.c_int)]
+                ("delta", ctypes.c_int), ("period", ctypes.c_int), ("periodic", ctypes.c_int),
+                ("stride", ctypes.c_int), ("gram", ctypes.c_int)]
 
 
 _lib = None
@@ -127,6 +128,8 @@ class PlanInfo:
     delta: int
     period: int
     periodic: bool
+    stride: int = 0  # K3 sampling stride (bytes)
+    gram: int = 0    # K3 gram length (bytes)
 
 
 class Plan:
@@ -167,7 +170,8 @@ class Plan:
     def info(self) -> PlanInfo:
         i = _PlanInfo()
         _check(load_library().mb_plan_info(self._h, ctypes.byref(i)))
-        return PlanInfo(i.m, FAMILY_NAMES.get(i.family, str(i.family)), i.anchor, i.delta, i.period, bool(i.periodic))
+        return PlanInfo(i.m, FAMILY_NAMES.get(i.family, str(i.family)), i.anchor, i.delta, i.period, bool(i.periodic),
+                        i.stride, i.gram)
 
     # -- H1 host tables (bit-identical to the reference's functions) --
     def horspool_table(self) -> list[int]:

@@ -119,6 +119,40 @@ def test_forced_families(cuda, family, lo, hi):
         check(p, t, family)
 
 
+@pytest.mark.parametrize("sigmas", [(256,), (64, 128), (8, 16), (2, 4)])
+def test_sampled_family(cuda, sigmas):
+    """K3 sampled q-gram filter: whenever a plan picks it, results equal the oracle."""
+    used = 0
+    for p, t in fuzz_cases(500 + sigmas[0], 120, 272, 3000, sigmas=sigmas, n_max=60000):
+        try:
+            engine.Plan(p, "sampled")
+        except ValueError:
+            continue  # low entropy / periodic: the plan keeps the full scan
+        used += 1
+        check(p, t, "sampled")
+        check(p, t)
+    if sigmas[0] >= 8:
+        assert used > 50
+
+
+def test_sampled_plants_and_edges(cuda):
+    rng = np.random.default_rng(7)
+    for m in (272, 300, 1024, 2047, 4096):
+        p = rand_bytes(rng, 256, m)
+        assert engine.Plan(p).info().family == "sampled"
+        n = 3 * TILE + 4321
+        t = bytearray(rand_bytes(rng, 256, n))
+        for s in (0, 1, 15, 16, TILE - m, TILE - 1, TILE, 2 * TILE - 7, n - m - 1, n - m):
+            if 0 <= s <= n - m:
+                t[s : s + m] = p
+        check(p, bytes(t))
+        base = torch.from_numpy(np.frombuffer(bytes(t) + b"\0" * 32, dtype=np.uint8).copy()).cuda()
+        for off in (1, 7, 13):
+            view = base[off : off + n - off]
+            got = gpu_positions(p, view)
+            assert np.array_equal(got, oracle.search(p, bytes(t)[off:n])), (m, off)
+
+
 def test_count_only_and_overflow(cuda):
     rng = np.random.default_rng(5)
     t = rand_bytes(rng, 2, 200000)

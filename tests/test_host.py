@@ -135,6 +135,14 @@ def test_plan_info_families():
     # anchor choice keeps the rare byte of a^(m-1)b inside the anchor window
     info = engine.Plan(b"a" * 127 + b"b").info()
     assert info.anchor <= 127 <= info.anchor + 6
+    rng = np.random.default_rng(1)
+    long_random = rng.integers(0, 256, 1024, dtype=np.uint8).tobytes()
+    assert engine.Plan(long_random).info().family == "sampled"
+    assert engine.Plan(long_random[:271]).info().family == "aligned"
+    assert engine.Plan(b"ab" * 512).info().family == "aligned"  # periodic: full scan
+    assert engine.Plan(long_random, family="aligned").info().family == "aligned"
+    with pytest.raises(ValueError):
+        engine.Plan(b"a" * 1024, family="sampled")
 
 
 def test_inputs_mirror_reference_generators():
