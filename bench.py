@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2 << 30, help="bytes of text in the CPU baseline sample")
+    ap.add_argument("--family", default="auto", help="force a kernel family where it applies (experiments)")
     return ap.parse_args()
 
 
@@ -447,7 +448,12 @@ def run_batched_sweep(args, rank, world, local_rank):
         if key not in dtexts:
             dtexts[key] = torch.from_numpy(t).to(dev)
         d = dtexts[key]
-        plans = [engine.Plan(p) for p in pats]
+        plans = []
+        for p in pats:
+            try:
+                plans.append(engine.Plan(p, args.family))
+            except ValueError:
+                plans.append(engine.Plan(p))
         offs = torch.zeros(len(plans) + 1, dtype=torch.int64, device=dev)
         engine.find_batch_into(plans, d, None, offs, stream)  # count pass sizes the output (untimed)
         total = int(offs[-1].item())

@@ -140,6 +140,44 @@ struct FiltALIGNED {
   }
 };
 
+// K2 / 7 <= m <= 64, small alphabets (bitparallel.py:41-63 compile_so): per-lane
+// bit-parallel Shift-Or over a 64-position run of the segment (+ m-1 bytes of
+// look-ahead).  Exact, no verification.  W = 32 or 64 bits of state.
+template <int W>
+struct FiltSO {
+  static constexpr bool kShiftOr = true;
+  static constexpr int kW = W;
+};
+template <class F, class = void>
+struct is_shiftor : std::false_type {};
+template <class F>
+struct is_shiftor<F, std::void_t<decltype(F::kShiftOr)>> : std::true_type {};
+
+template <int W>
+__device__ __forceinline__ void shiftor_lane(const uint8_t* q, int m, const uint64_t* masks, uint32_t& w0,
+                                             uint32_t& w1) {
+  using T = typename std::conditional<W == 32, uint32_t, uint64_t>::type;
+  T D = ~T(0);
+  uint64_t acc = 0;  // shift register of match bits; after 64 + m - 1 bytes holds positions 0..63
+  const int total = 64 + m - 1;
+  const int hb = m - 1;
+  int y = 0;
+  for (; y + 4 <= total; y += 4) {
+    const uint32_t word = *reinterpret_cast<const uint32_t*>(q + y);
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      D = (D << 1) | (T)masks[(word >> (8 * b)) & 0xFFu];
+      acc = (acc >> 1) | ((uint64_t)((~D >> hb) & 1u) << 63);
+    }
+  }
+  for (; y < total; y++) {
+    D = (D << 1) | (T)masks[q[y]];
+    acc = (acc >> 1) | ((uint64_t)((~D >> hb) & 1u) << 63);
+  }
+  w0 = (uint32_t)acc;
+  w1 = (uint32_t)(acc >> 32);
+}
+
 // ------------------------------------------------------------ verification
 // Direct window compare in shared memory (core.py:131-136 match_at).
 __device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* pat, int m) {
@@ -200,6 +238,9 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   uint32_t* brk = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4) +
                   warp * 2 * (P.brk_words + 4);
   int32_t* nbw = reinterpret_cast<int32_t*>(brk + P.brk_words + 4);
+  uint64_t* so_s = reinterpret_cast<uint64_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
+                                               NWARP * 2 * (P.brk_words + 4) * 4) +
+                   warp * 256;  // K2 only: per-warp shift-or masks
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; s++) {
@@ -259,42 +300,67 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
       blo = P.off + pd.delta;               // valid bits: s = b - delta - off in [0, n-m]
       bhi = P.off + pd.delta + P.n - pd.m;  // inclusive (may be < blo)
       cur_k = k;
+      if constexpr (is_shiftor<Filt>::value) {  // this warp's copy of the 256 shift-or masks
+        for (int i = lane; i < 256; i += 32) so_s[i] = pd.so_masks[i];
+        __syncwarp();
+      }
     }
     const int64_t B0 = hdr[s].tau * TILE;
     const uint8_t* spat = stages + s * P.stage_bytes;
     const uint8_t* S = spat + P.pat_cap + P.pre;  // S[c] = virtual text byte B0 + c
+    const int64_t segb = B0 + c0;
+    const bool interior = segb >= blo && segb + SEG - 1 <= bhi;
 
-    // ---- filter (fast path): 4 rounds of 512 positions, 16 per lane, masks kept in registers
-    uint32_t mk[SEG / 512];
-    bool anyc = false;
-#pragma unroll
-    for (int r = 0; r < SEG / 512; r++) {
-      const int c = c0 + r * 512 + lane * 16;
-      const uint4 X = *reinterpret_cast<const uint4*>(S + c);
-      const uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
-      mk[r] = Filt::run(w, pd);
-      anyc |= (mk[r] != 0);
-    }
-    uint32_t cnt = 0;
-    if (__any_sync(0xffffffffu, anyc)) {
-      // ---- slow path: validity mask at text edges, linear segment bitmap
-      const int64_t segb = B0 + c0;
-      const bool interior = segb >= blo && segb + SEG - 1 <= bhi;
+    // this lane's 64 positions of the segment: linear bitmap words 2*lane, 2*lane+1
+    uint32_t w0 = 0, w1 = 0;
+    bool have;
+    if constexpr (is_shiftor<Filt>::value) {
+      // ---- K2: exact per-lane shift-or over positions [c0 + 64 lane, +64)
+      shiftor_lane<Filt::kW>(S + c0 + 64 * lane, (int)pd.m, so_s, w0, w1);
+      if (!interior) {
+        const int64_t b = segb + 64 * lane;
+        uint64_t vm = 0;
+        for (int i = 0; i < 64; i++)
+          if (b + i >= blo && b + i <= bhi) vm |= 1ULL << i;
+        w0 &= (uint32_t)vm;
+        w1 &= (uint32_t)(vm >> 32);
+      }
+      have = __any_sync(0xffffffffu, (w0 | w1) != 0);
+    } else {
+      // ---- filter (fast path): 4 rounds of 512 positions, 16 per lane, masks kept in registers
+      uint32_t mk[SEG / 512];
+      bool anyc = false;
 #pragma unroll
       for (int r = 0; r < SEG / 512; r++) {
-        uint32_t m = mk[r];
-        if (!interior) {
-          const int64_t b = segb + r * 512 + lane * 16;
-          uint32_t vm = 0;
-          for (int i = 0; i < 16; i++)
-            if (b + i >= blo && b + i <= bhi) vm |= 1u << i;
-          m &= vm;
-        }
-        const uint32_t other = __shfl_down_sync(0xffffffffu, m, 1);
-        if (!(lane & 1)) bm[r * 16 + (lane >> 1)] = m | (other << 16);
+        const int c = c0 + r * 512 + lane * 16;
+        const uint4 X = *reinterpret_cast<const uint4*>(S + c);
+        const uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
+        mk[r] = Filt::run(w, pd);
+        anyc |= (mk[r] != 0);
       }
-      __syncwarp();
-      uint32_t w0 = bm[2 * lane], w1 = bm[2 * lane + 1];
+      have = __any_sync(0xffffffffu, anyc);
+      if (have) {
+        // ---- slow path: validity mask at text edges, linear segment bitmap
+#pragma unroll
+        for (int r = 0; r < SEG / 512; r++) {
+          uint32_t m = mk[r];
+          if (!interior) {
+            const int64_t b = segb + r * 512 + lane * 16;
+            uint32_t vm = 0;
+            for (int i = 0; i < 16; i++)
+              if (b + i >= blo && b + i <= bhi) vm |= 1u << i;
+            m &= vm;
+          }
+          const uint32_t other = __shfl_down_sync(0xffffffffu, m, 1);
+          if (!(lane & 1)) bm[r * 16 + (lane >> 1)] = m | (other << 16);
+        }
+        __syncwarp();
+        w0 = bm[2 * lane];
+        w1 = bm[2 * lane + 1];
+      }
+    }
+    uint32_t cnt = 0;
+    if (have) {
       // ---- verify (exact filters skip this)
       if (!pd.exact && __any_sync(0xffffffffu, (w0 | w1) != 0)) {
         const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
@@ -723,7 +789,8 @@ static int plan_device(const mb_plan* p, const PatDev** out) {
   const size_t bloom_bytes = h.bloom.size() * 4;
   const size_t bs_bytes = (h.bstart.size() * 2 + 15) & ~(size_t)15;
   const size_t be_bytes = (h.bent.size() * 2 + 15) & ~(size_t)15;
-  const size_t total = pat_bytes + bloom_bytes + bs_bytes + be_bytes;
+  const size_t so_bytes = h.so_masks.size() * 8;
+  const size_t total = pat_bytes + bloom_bytes + bs_bytes + be_bytes + so_bytes;
   if (cudaMalloc(&p->d_buf, total) != cudaSuccess) return fail(MB_ENOMEM, "plan upload alloc");
   if (cudaMalloc(&p->d_dev, sizeof(PatDev)) != cudaSuccess) {
     cudaFree(p->d_buf);
@@ -735,12 +802,15 @@ static int plan_device(const mb_plan* p, const PatDev** out) {
   if (bloom_bytes) memcpy(img.data() + pat_bytes, h.bloom.data(), bloom_bytes);
   if (!h.bstart.empty()) memcpy(img.data() + pat_bytes + bloom_bytes, h.bstart.data(), h.bstart.size() * 2);
   if (!h.bent.empty()) memcpy(img.data() + pat_bytes + bloom_bytes + bs_bytes, h.bent.data(), h.bent.size() * 2);
+  if (so_bytes) memcpy(img.data() + pat_bytes + bloom_bytes + bs_bytes + be_bytes, h.so_masks.data(), so_bytes);
   CUDA_TRY(cudaMemcpy(p->d_buf, img.data(), total, cudaMemcpyHostToDevice));
   PatDev d = h.dev;
   d.bytes = p->d_buf;
   d.bloom = bloom_bytes ? reinterpret_cast<const uint32_t*>(p->d_buf + pat_bytes) : nullptr;
   d.bstart = bloom_bytes ? reinterpret_cast<const uint16_t*>(p->d_buf + pat_bytes + bloom_bytes) : nullptr;
   d.bent = bloom_bytes ? reinterpret_cast<const uint16_t*>(p->d_buf + pat_bytes + bloom_bytes + bs_bytes) : nullptr;
+  d.so_masks = so_bytes ? reinterpret_cast<const uint64_t*>(p->d_buf + pat_bytes + bloom_bytes + bs_bytes + be_bytes)
+                        : nullptr;
   CUDA_TRY(cudaMemcpy(p->d_dev, &d, sizeof(PatDev), cudaMemcpyHostToDevice));
   p->dview = d;
   p->device = dev;
@@ -797,10 +867,6 @@ int mb_plan_create(const uint8_t* h_pattern, int64_t m, const mb_plan_opts* opts
   if (rc) {
     delete p;
     return fail(rc, err);
-  }
-  if (p->h.family == MB_FAM_SHIFTOR) {
-    delete p;
-    return fail(MB_EINVAL, "shift-or family not built in this version");
   }
   *out = p;
   return MB_OK;
@@ -958,7 +1024,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
     sampled_kernel<<<(int)grid_s, NT, smem_s, st>>>(P);
   } else {
     const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
-                        (size_t)NWARP * 2 * (P.brk_words + 4) * 4;
+                        (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * 256 * 8 : 0);
     static std::mutex mu;
     static bool attr_done = false;
     static size_t occ_smem = 0;
@@ -987,7 +1053,9 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
 
 // family key: patterns sharing a key share one count-kernel launch
 static int family_key(const PatDev& d) {
-  return d.family == MB_FAM_SWAR ? (int)(10 + d.m) : d.family;
+  if (d.family == MB_FAM_SWAR) return (int)(10 + d.m);
+  if (d.family == MB_FAM_SHIFTOR) return d.m <= 32 ? 20 : 21;
+  return d.family;
 }
 
 static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, const int32_t* h_idx,
@@ -1001,6 +1069,12 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
     case MB_FAM_WIN4: return launch_group<FiltWIN4>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
     case MB_FAM_ALIGNED: return launch_group<FiltALIGNED>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
     case MB_FAM_SAMPLED: return launch_group<SampledTag>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+    case MB_FAM_SHIFTOR: {
+      int64_t maxm = 0;
+      for (int i = 0; i < gk; i++) maxm = std::max<int64_t>(maxm, h_pats[h_idx[i]].m);
+      if (maxm <= 32) return launch_group<FiltSO<32>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+      return launch_group<FiltSO<64>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+    }
   }
   return fail(MB_EINVAL, "unknown kernel family");
 }

@@ -57,6 +57,15 @@ static inline uint32_t load_le32(const uint8_t* p) {
   return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
 }
 
+// K2 (per-lane shift-or) would be auto-chosen for 7 <= m <= 64 at pattern byte
+// entropies up to this many bits.  Measured on B200 (profiles/r1/
+// cfg2_family_sweep.json) it loses to the K1 anchor filter in every config-2
+// cell, even sigma = 2 (0.83-0.94 vs 1.09-1.42 TB/s aggregated): the per-byte
+// mask lookup + dependent D update chain costs more than verifying K1's
+// frequent candidates.  So auto never picks it (threshold < 0); it stays an
+// exact, tested family selectable through mb_plan_opts.family.
+constexpr double K2_MAX_ENTROPY = -1.0;
+
 static inline int round16(int64_t x) { return (int)((x + 15) & ~(int64_t)15); }
 
 // Anchor choice: the window of `len` pattern bytes whose bytes are rarest.  Byte
@@ -170,11 +179,20 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
 
   int fam = opts ? opts->family : MB_FAM_AUTO;
   const int64_t* hist = opts ? opts->hist : nullptr;
+  {
+    double cnt[256] = {0};
+    for (int64_t i = 0; i < m; i++) cnt[pat[i]] += 1;
+    ph->entropy = 0;
+    for (int c = 0; c < 256; c++)
+      if (cnt[c] > 0) ph->entropy -= cnt[c] / m * std::log2(cnt[c] / m);
+  }
   if (fam == MB_FAM_AUTO) {
     if (m <= 3)
       fam = MB_FAM_SWAR;
     else if (m <= 6)
       fam = MB_FAM_WIN4;
+    else if (m <= 64 && ph->entropy <= K2_MAX_ENTROPY)
+      fam = MB_FAM_SHIFTOR;  // small alphabet: 4-byte anchors are unselective, shift-or needs no verify
     else
       fam = MB_FAM_ALIGNED;
   }
@@ -244,11 +262,16 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       }
       break;
     }
-    case MB_FAM_SHIFTOR:
+    case MB_FAM_SHIFTOR: {
+      // bitparallel.py:41-63 compile_so: complemented forward masks over m bits
       ph->anchor = 0;
       d.delta = 0;
       d.exact = 1;
+      const uint64_t full = m == 64 ? ~0ULL : ((1ULL << m) - 1);
+      ph->so_masks.assign(256, full);
+      for (int64_t j = 0; j < m; j++) ph->so_masks[pat[j]] &= ~(1ULL << j);
       break;
+    }
     case MB_FAM_SAMPLED:
       // bit b of the sample at x = S*i covers b in [x, x + S): b = s + S - 1
       ph->anchor = 0;

@@ -36,6 +36,7 @@ struct PatDev {
   const uint32_t* bloom;   // 65536-bit filter over gram hashes (device)
   const uint16_t* bstart;  // (1 << B) + 1 bucket starts (device)
   const uint16_t* bent;    // S entries: pattern offsets j sorted by bucket (device)
+  const uint64_t* so_masks; // K2: 256 complemented shift-or masks (device), bit j clear iff p[j] == c
 };
 
 // gram hash shared by host table build and device lookup (words little-endian)
@@ -58,6 +59,8 @@ struct PlanHost {
   // K3 tables (host copies; uploaded with the pattern)
   std::vector<uint32_t> bloom;
   std::vector<uint16_t> bstart, bent;
+  std::vector<uint64_t> so_masks;  // K2 (bitparallel.py:47-49 convention)
+  double entropy = 0;              // bits per byte of the pattern's byte distribution
 };
 
 void horspool_table(const uint8_t* p, int64_t m, int64_t* tbl);

@@ -113,7 +113,7 @@ def test_sigma1_and_zero_bytes(cuda):
         check(b"\x00" * m, b"\x00" * 3000 + b"\x01" + b"\x00" * 50)
 
 
-@pytest.mark.parametrize("family,lo,hi", [("win4", 4, 40), ("aligned", 7, 200)])
+@pytest.mark.parametrize("family,lo,hi", [("win4", 4, 40), ("aligned", 7, 200), ("shiftor", 1, 64)])
 def test_forced_families(cuda, family, lo, hi):
     for p, t in fuzz_cases(77, 150, lo, hi, n_max=3000):
         check(p, t, family)
@@ -151,6 +151,22 @@ def test_sampled_plants_and_edges(cuda):
             view = base[off : off + n - off]
             got = gpu_positions(p, view)
             assert np.array_equal(got, oracle.search(p, bytes(t)[off:n])), (m, off)
+
+
+@pytest.mark.parametrize("m", [1, 7, 31, 32, 33, 63, 64])
+def test_shiftor_edges(cuda, m):
+    rng = np.random.default_rng(300 + m)
+    for sigma in (1, 2, 4, 256):
+        n = 2 * TILE + 777
+        t = bytearray(rand_bytes(rng, sigma, n))
+        p = rand_bytes(rng, sigma, m)
+        for s in (0, 5, TILE - m, TILE - 1, TILE, n - m):
+            t[s : s + m] = p
+        check(p, bytes(t), "shiftor")
+        base = torch.from_numpy(np.frombuffer(bytes(t) + b"\0" * 32, dtype=np.uint8).copy()).cuda()
+        for off in (3, 9):
+            got = engine.find(engine.Plan(p, "shiftor"), base[off:n]).cpu().numpy()
+            assert np.array_equal(got, oracle.search(p, bytes(t)[off:n])), (m, sigma, off)
 
 
 def test_count_only_and_overflow(cuda):

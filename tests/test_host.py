@@ -123,7 +123,8 @@ def test_descriptor_substitution_seam():
 
 
 def test_plan_info_families():
-    cases = {1: "swar", 3: "swar", 4: "win4", 6: "win4", 7: "aligned", 1024: "aligned", 8192: "aligned"}
+    cases = {1: "swar", 3: "swar", 4: "win4", 6: "win4", 7: "aligned", 64: "aligned", 65: "aligned",
+             1024: "aligned", 8192: "aligned"}
     for m, fam in cases.items():
         assert engine.Plan(b"\x05" * (m - 1) + b"\x07").info().family == fam
     assert engine.Plan(b"a" * 100).info().periodic
@@ -143,6 +144,11 @@ def test_plan_info_families():
     assert engine.Plan(long_random, family="aligned").info().family == "aligned"
     with pytest.raises(ValueError):
         engine.Plan(b"a" * 1024, family="sampled")
+    # K2 shift-or is exact and selectable, but auto keeps the faster K1 filter
+    assert engine.Plan(bytes(rng.integers(0, 4, 40, dtype=np.uint8))).info().family == "aligned"
+    assert engine.Plan(bytes(rng.integers(0, 4, 40, dtype=np.uint8)), family="shiftor").info().family == "shiftor"
+    with pytest.raises(ValueError):
+        engine.Plan(b"x" * 65, family="shiftor")
 
 
 def test_inputs_mirror_reference_generators():
