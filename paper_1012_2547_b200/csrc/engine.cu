@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <cmath>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
   uint8_t* stages = smem + SM_STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (P.run_if && *P.run_if == 0u) return;  // conditional fallback launch (MP did not overflow)
   uint32_t* bm = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes) + warp * SEG_WORDS;
   uint32_t* brk = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4) +
                   warp * 2 * (P.brk_words + 4);
@@ -690,7 +692,19 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
       const int64_t o = P.toff[g];
       if (o >= P.cap) continue;
       if (c <= LIST_CAP) {
-        if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + P.lists[g * LIST_CAP + lane];
+        uint32_t v = lane < (int)c ? (uint32_t)P.lists[g * LIST_CAP + lane] : 0xFFFFFFFFu;
+        if (P.unsorted_lists) {  // MP fills list slots atomically: warp bitonic sort of <= 32 offsets
+#pragma unroll
+          for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+              const uint32_t o2 = __shfl_xor_sync(0xffffffffu, v, jj);
+              const bool up = ((lane & kk) == 0);
+              const bool lower = ((lane & jj) == 0);
+              v = (lower == up) ? min(v, o2) : max(v, o2);
+            }
+        }
+        if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + v;
         continue;
       }
       const uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
@@ -722,6 +736,123 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
         w_out += total;
       }
     }
+  }
+}
+
+// ------------------------------------------------ kernel 1c: batched multi-pattern pass (K5 "MP")
+// One TMA pass over the text serves a whole batch of anchor-filter (K1
+// ALIGNED) patterns: each 4-aligned text word X is hashed once; a bloom bit
+// test in smem rejects almost every word, and a hit walks the bucket of
+// {gram, pattern, anchor+j} entries.  A verified occurrence (k, s) maps to the
+// same bitmap bit b = s + off + a_k + 3 as the single-pattern ALIGNED plan, so
+// it lands in the consumer's own segment of pattern k's segment layout: one
+// 16-bit atomic count and an (unordered) list slot; offsets/expand are shared
+// (expand sorts MP lists).  Segments above LIST_CAP set `overflow` and the
+// host re-runs the batch through the per-pattern path.
+__global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
+  uint8_t* stages = smem + SM_STAGES;
+  uint32_t* bloom = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes);
+  uint32_t* bstart = bloom + 2048;
+  uint2* ents = reinterpret_cast<uint2*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 2048; i += NT + 32) bloom[i] = P.bloom[i];
+  for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
+  for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents[i];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NWARP) {  // ---------------- producer: text tiles only
+    if (lane == 0) {
+      for (int it = 0;; it++) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
+        const unsigned long long tk = atomicAdd(P.ticket, 1ULL);
+        if ((int64_t)tk >= P.ntiles_text) {
+          hdr[s].tk = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        hdr[s].tk = (int64_t)tk;
+        hdr[s].tau = (int64_t)tk;
+        const int64_t start = (int64_t)tk * TILE - P.pre;
+        const int64_t end = (int64_t)tk * TILE + TILE + P.post;
+        const int64_t cs = start < 0 ? 0 : start;
+        const int64_t ce = end > P.nv16 ? P.nv16 : end;
+        const uint32_t tb = ce > cs ? (uint32_t)(ce - cs) : 0u;
+        uint8_t* st = stages + s * P.stage_bytes;
+        mbar_expect_tx(&full[s], tb);
+        if (tb) bulk_g2s(st + (cs - start), P.text + cs, tb, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int c0 = warp * SEG;
+  for (int it = 0;; it++) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+    const int64_t tau = hdr[s].tk;
+    if (tau < 0) break;
+    const int64_t B0 = tau * TILE;
+    const uint8_t* S = stages + s * P.stage_bytes + P.pre;  // S[c] = virtual byte B0 + c
+#pragma unroll 1
+    for (int r = 0; r < SEG / 512; r++) {
+      const int c = c0 + r * 512 + lane * 16;
+      const uint4 X4 = *reinterpret_cast<const uint4*>(S + c);
+      const uint32_t w[4] = {X4.x, X4.y, X4.z, X4.w};
+      uint32_t hits = 0;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint32_t h = w[q] * 0x9E3779B1u;
+        hits |= ((bloom[h >> 21] >> ((h >> 16) & 31)) & 1u) << q;
+      }
+      while (hits) {  // rare: bucket walk + verification
+        const int q = __ffs(hits) - 1;
+        hits &= hits - 1;
+        const uint32_t X = w[q];
+        const uint32_t h = X * 0x9E3779B1u;
+        const uint32_t bk = h >> (32 - P.B);
+        const int64_t x = B0 + c + 4 * q;  // virtual position of the word
+        for (uint32_t e = bstart[bk]; e < bstart[bk + 1]; e++) {
+          const uint2 en = ents[e];
+          if (en.x != X) continue;
+          const int kl = (int)(en.y >> 16);  // pattern within this chunk
+          const int aj = (int)(en.y & 0xFFFFu);
+          const int64_t sv = x - aj;  // virtual start
+          const int64_t spos = sv - P.off;
+          const PatDev* pd = P.pats + P.kbase + kl;
+          const int64_t m = pd->m;
+          if (spos < 0 || spos + m > P.n) continue;
+          const uint8_t* tp = S + (sv - B0);
+          const uint8_t* pp = pd->bytes;
+          bool ok = true;
+          for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);
+          if (!ok) continue;
+          // same bit as the single-pattern ALIGNED plan: b = sv + a + 3 -> this lane's chunk
+          const int64_t b = sv + pd->delta;
+          const int64_t g = ((int64_t)(P.kbase + kl) * P.ntiles + tau) * NWARP + warp;
+          unsigned int* wptr = reinterpret_cast<unsigned int*>(P.counts) + (g >> 1);
+          const unsigned int sh = 16u * (unsigned)(g & 1);
+          const unsigned int old = (atomicAdd(wptr, 1u << sh) >> sh) & 0xFFFFu;
+          if (old < (unsigned)LIST_CAP)
+            P.lists[g * LIST_CAP + old] = (uint16_t)(b - B0);
+          else
+            atomicExch(P.overflow, 1u);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -834,6 +965,10 @@ struct mb_ctx {
   int32_t* plist = nullptr;
   int64_t plist_cap = 0;
   std::vector<int32_t> h_plist;
+  uint32_t* mp_tab = nullptr;  // MP tables (bloom, bucket starts, entries) per chunk
+  int64_t mp_tab_cap = 0;
+  std::vector<uint32_t> h_mp;
+  std::vector<double> h_ent;
   uint32_t epoch = 0;
   unsigned long long* ticket = nullptr;
   PatDev* d_pats = nullptr;
@@ -930,7 +1065,7 @@ int mb_ctx_create(int device, mb_ctx** out) {
   mb_ctx* c = new mb_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMalloc(&c->ticket, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+  if (cudaMalloc(&c->ticket, 16 * sizeof(unsigned long long)) != cudaSuccess) {
     delete c;
     return fail(MB_ENOMEM, "ticket alloc");
   }
@@ -946,6 +1081,7 @@ void mb_ctx_destroy(mb_ctx* c) {
   cudaFree(c->bitmaps);
   cudaFree(c->toff);
   cudaFree(c->plist);
+  cudaFree(c->mp_tab);
   cudaFree(c->ticket);
   cudaFree(c->d_pats);
   cudaFree(c->d_text);
@@ -1079,11 +1215,56 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
   return fail(MB_EINVAL, "unknown kernel family");
 }
 
-// One search (K = 1) or batch: per family group one count kernel, then one
-// offsets and one expand launch over all K patterns' segments, so the output
-// is CSR in the caller's pattern order whatever the family mix.
+// MP eligibility (K5): a batch of >= 8 anchor-filter (ALIGNED) patterns whose
+// pooled anchors stay selective.  `rate` is the expected number of gram hits
+// per text word, sum over patterns k and j of prod_i p(G_kj[i]), with byte
+// probabilities p estimated from all pattern bytes of the batch (patterns are
+// drawn from the text); MP runs when rate <= 0.05.
+static bool mp_eligible(const PatDev* h_pats, const double* rate, int K) {
+  if (!rate || K < 8 || K > MP_CHUNK * MAX_GROUPS || *rate > 0.05) return false;
+  for (int k = 0; k < K; k++)
+    if (h_pats[k].family != MB_FAM_ALIGNED) return false;
+  return true;
+}
+
+// Host-built MP tables for patterns [k0, k0 + kc): bloom, bucket starts, entries.
+static void mp_tables(const PatDev* h_pats, int k0, int kc, int* Bout, std::vector<uint32_t>& img) {
+  const int nent = 4 * kc;
+  int B = 4;
+  while ((1 << B) < nent) B++;
+  const int nb = 1 << B;
+  const int bs_words = (nb + 1 + 3) & ~3;
+  img.assign(2048 + bs_words + 2 * nent, 0u);
+  uint32_t* bloom = img.data();
+  uint32_t* bstart = bloom + 2048;
+  std::vector<uint32_t> cnt(nb, 0);
+  for (int i = 0; i < kc; i++)
+    for (int j = 0; j < 4; j++) {
+      const uint32_t h = h_pats[k0 + i].G[j] * 0x9E3779B1u;
+      bloom[h >> 21] |= 1u << ((h >> 16) & 31);
+      cnt[h >> (32 - B)]++;
+    }
+  for (int b = 0; b < nb; b++) bstart[b + 1] = bstart[b] + cnt[b];
+  std::vector<uint32_t> fill(bstart, bstart + nb);
+  uint32_t* ents = bstart + bs_words;
+  for (int i = 0; i < kc; i++)
+    for (int j = 0; j < 4; j++) {
+      const uint32_t g = h_pats[k0 + i].G[j];
+      const uint32_t b = (g * 0x9E3779B1u) >> (32 - B);
+      const uint32_t e = fill[b]++;
+      ents[2 * e] = g;
+      ents[2 * e + 1] = ((uint32_t)i << 16) | (uint32_t)(h_pats[k0 + i].anchor + j);
+    }
+  *Bout = B;
+}
+
+// One search (K = 1) or batch: per family group one count kernel (or, for a
+// selective batch of anchor-filter patterns, one MP pass over the text), then
+// one offsets and one expand launch over all K patterns' segments, so the
+// output is CSR in the caller's pattern order whatever the family mix.
 static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
-                      int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st) {
+                      int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st,
+                      const double* mp_rate = nullptr) {
   ScanParams P;
   memset(&P, 0, sizeof(P));
   const uintptr_t addr = (uintptr_t)d_text;
@@ -1105,11 +1286,11 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   const int64_t T = P.total_tiles * NWARP;  // segments
   const int64_t nchunks = (T + SCAN_CHUNK - 1) / SCAN_CHUNK;
   int rc;
-  if ((rc = grow(&c->counts, &c->counts_cap, T, "counts"))) return rc;
+  if ((rc = grow(&c->counts, &c->counts_cap, T + 2, "counts"))) return rc;
   if ((rc = grow(&c->lists, &c->lists_cap, T * LIST_CAP, "lists"))) return rc;
   if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * SEG_WORDS, "bitmaps"))) return rc;
   if ((rc = grow(&c->toff, &c->toff_cap, T, "tile offsets"))) return rc;
-  if (nchunks > c->state_cap || c->epoch >= (1u << 24) - 1) {
+  if (nchunks > c->state_cap || c->epoch >= (1u << 24) - 4) {
     if ((rc = grow(&c->state, &c->state_cap, nchunks, "look-back state"))) return rc;
     CUDA_TRY(cudaMemsetAsync(c->state, 0, sizeof(uint64_t) * c->state_cap, st));
     c->epoch = 0;
@@ -1119,14 +1300,98 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.bitmaps = c->bitmaps;
   P.toff = c->toff;
   P.state = c->state;
-  P.epoch = ++c->epoch;
   P.ticket = c->ticket;
   P.out = d_out;
   P.cap = d_out ? cap : 0;
   P.offsets_plus1 = offsets_plus1;
   P.out_base = nullptr;
-  CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 8 * sizeof(unsigned long long), st));
 
+  auto finish = [&](bool unsorted) -> int {
+    P.epoch = ++c->epoch;
+    P.unsorted_lists = unsorted ? 1 : 0;
+    offsets_kernel<<<(int)nchunks, NT, 0, st>>>(P);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    if (d_out && cap > 0) {
+      const int64_t eg = std::min<int64_t>((T + 32 * EXP_WARPS - 1) / (32 * EXP_WARPS), (int64_t)c->nsm * 16);
+      expand_kernel<<<(int)eg, EXP_WARPS * 32, 0, st>>>(P);
+      g_launches++;
+      CUDA_TRY(cudaGetLastError());
+    }
+    return MB_OK;
+  };
+
+  bool mp_used = false;
+  if (mp_eligible(h_pats, mp_rate, K)) {
+    int pre = 0, post = 0;
+    for (int k = 0; k < K; k++) pre = std::max(pre, h_pats[k].pre), post = std::max(post, h_pats[k].post);
+    MPParams M;
+    memset(&M, 0, sizeof(M));
+    M.text = P.text;
+    M.off = P.off;
+    M.n = n;
+    M.nv16 = P.nv16;
+    M.ntiles_text = (P.nv16 + TILE - 1) / TILE;
+    M.ntiles = P.ntiles;
+    M.pre = pre;
+    M.post = post;
+    M.stage_bytes = (pre + TILE + post + 127) & ~127;
+    M.pats = d_pats;
+    M.counts = c->counts;
+    M.lists = c->lists;
+    if ((rc = grow(&c->mp_tab, &c->mp_tab_cap, (int64_t)(2048 + 4 * MP_CHUNK + 8 + 8 * MP_CHUNK) * MAX_GROUPS,
+                   "MP tables")))
+      return rc;
+    M.overflow = reinterpret_cast<unsigned int*>(c->counts + T);  // 4 spare bytes after the counts
+    CUDA_TRY(cudaMemsetAsync(c->counts, 0, sizeof(uint16_t) * (T + 2), st));
+    CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 16 * sizeof(unsigned long long), st));
+    c->h_mp.clear();
+    std::vector<std::pair<int64_t, int>> chunk_at;  // (table word offset, B) per chunk
+    for (int k0 = 0, ci = 0; k0 < K; k0 += MP_CHUNK, ci++) {
+      std::vector<uint32_t> img;
+      int B = 0;
+      mp_tables(h_pats, k0, std::min(MP_CHUNK, K - k0), &B, img);
+      chunk_at.push_back({(int64_t)c->h_mp.size(), B});
+      c->h_mp.insert(c->h_mp.end(), img.begin(), img.end());
+      while (c->h_mp.size() % 4) c->h_mp.push_back(0);
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->mp_tab, c->h_mp.data(), sizeof(uint32_t) * c->h_mp.size(), cudaMemcpyHostToDevice, st));
+    static std::mutex mu_mp;
+    static bool attr_mp = false;
+    {
+      std::lock_guard<std::mutex> g(mu_mp);
+      if (!attr_mp) {
+        CUDA_TRY(cudaFuncSetAttribute(mp_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_mp = true;
+      }
+    }
+    for (int k0 = 0, ci = 0; k0 < K; k0 += MP_CHUNK, ci++) {
+      const int kc = std::min(MP_CHUNK, K - k0);
+      const int B = chunk_at[ci].second;
+      const int bs_words = ((1 << B) + 1 + 3) & ~3;
+      M.bloom = c->mp_tab + chunk_at[ci].first;
+      M.bstart = M.bloom + 2048;
+      M.ents = reinterpret_cast<const uint2*>(M.bstart + bs_words);
+      M.B = B;
+      M.nents = 4 * kc;
+      M.kbase = k0;
+      M.ticket = c->ticket + TICKET_MP0 + ci;
+      const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * M.stage_bytes + 8192 + 4 * bs_words + 8 * M.nents;
+      int per_sm = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mp_scan_kernel, NT + 32, smem));
+      if (per_sm < 1) return fail(MB_ECUDA, "MP kernel does not fit on an SM");
+      const int64_t grid = std::min<int64_t>(M.ntiles_text, (int64_t)c->nsm * per_sm);
+      mp_scan_kernel<<<(int)grid, NT + 32, smem, st>>>(M);
+      g_launches++;
+      CUDA_TRY(cudaGetLastError());
+    }
+    // fallback without a host round trip: the per-pattern scan below runs only if
+    // a segment overflowed (kernels read the flag and exit otherwise); lists are
+    // sorted on expand either way (harmless for the already-sorted fallback lists)
+    P.run_if = M.overflow;
+    mp_used = true;
+  }
+  if (!mp_used) CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 16 * sizeof(unsigned long long), st));
   // group patterns by family key (stable); a single group needs no index list
   std::vector<int> keys;
   std::vector<std::vector<int32_t>> groups;
@@ -1155,16 +1420,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       base += (int)groups[g].size();
     }
   }
-  offsets_kernel<<<(int)nchunks, NT, 0, st>>>(P);
-  g_launches++;
-  CUDA_TRY(cudaGetLastError());
-  if (d_out && cap > 0) {
-    const int64_t eg = std::min<int64_t>((T + 32 * EXP_WARPS - 1) / (32 * EXP_WARPS), (int64_t)c->nsm * 16);
-    expand_kernel<<<(int)eg, EXP_WARPS * 32, 0, st>>>(P);
-    g_launches++;
-    CUDA_TRY(cudaGetLastError());
-  }
-  return MB_OK;
+  return finish(mp_used);
 }
 
 extern "C" {
@@ -1212,7 +1468,26 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
     c->pats_cap = K;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice, st));
-  return run_search(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets + 1, st);
+  double rate = 1e30;
+  bool all_aligned = K >= 8;
+  for (int k = 0; k < K && all_aligned; k++) all_aligned = c->h_pats[k].family == MB_FAM_ALIGNED;
+  if (all_aligned) {
+    rate = 0;
+    double hist[256] = {0}, tot = 0;
+    for (int k = 0; k < K; k++) {
+      const auto& pb = plans[k]->h.pat;
+      const size_t lim = std::min<size_t>(pb.size(), 64);
+      for (size_t i = 0; i < lim; i++) hist[pb[i]] += 1, tot += 1;
+    }
+    for (int k = 0; k < K; k++)
+      if (c->h_pats[k].family == MB_FAM_ALIGNED)
+        for (int j = 0; j < 4; j++) {
+          double pr = 1;
+          for (int i = 0; i < 4; i++) pr *= hist[(c->h_pats[k].G[j] >> (8 * i)) & 0xFF] / tot;
+          rate += pr;
+        }
+  }
+  return run_search(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets + 1, st, &rate);
 }
 
 int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, void* stream) {

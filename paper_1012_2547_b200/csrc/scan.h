@@ -37,6 +37,8 @@ constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offs
 constexpr int SCAN_CHUNK = 4096;  // segment counts per offsets_kernel CTA
 constexpr int TICKET_OFFSETS = 7; // ticket slot of offsets_kernel (slots 0..6: family groups)
 constexpr int MAX_GROUPS = 7;
+constexpr int TICKET_MP0 = 8;     // MP chunk tickets use slots 8..14 (ticket array has 16)
+constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 
 struct StageHdr {
   int64_t tk;   // global tile ticket (-1: no more work)
@@ -79,6 +81,28 @@ struct ScanParams {
   int64_t cap;
   int64_t* offsets_plus1;   // entry k <- inclusive prefix after pattern k
   const int64_t* out_base;  // device: output index where this launch starts (null = 0)
+  int unsorted_lists;       // lists were filled in arbitrary order (MP path): sort on expand
+  const unsigned int* run_if;  // count kernels exit at once unless *run_if != 0 (MP fallback)
+};
+
+// Batched multi-pattern single pass (K5 "MP"): every anchor gram of every
+// pattern of the batch in one smem table; one TMA pass over the text.
+struct MPParams {
+  const uint8_t* text;
+  int64_t off, n, nv16;
+  int64_t ntiles_text;  // tiles over the text (ticket range)
+  int64_t ntiles;       // tiles per pattern in the segment layout (= ScanParams.ntiles)
+  int pre, post, stage_bytes;
+  unsigned long long* ticket;
+  const uint32_t* bloom;   // 65536 bits over gram * 0x9E3779B1 >> 16
+  const uint32_t* bstart;  // (1 << B) + 1 bucket starts
+  const uint2* ents;       // {gram, (batch index << 16) | (anchor + j)} sorted by bucket
+  int B, nents;
+  int kbase;               // batch index of this chunk's first pattern
+  const PatDev* pats;      // whole batch
+  uint16_t* counts;        // segment layout, zeroed before the launch
+  uint16_t* lists;
+  unsigned int* overflow;  // set if a segment exceeds LIST_CAP (host re-runs the segment path)
 };
 
 }  // namespace mb

@@ -214,3 +214,31 @@ def test_histogram_alphabet(cuda):
 def test_instrumented_text_rejected(cuda):
     with pytest.raises(TypeError):
         mb.search_hor(b"ab", mb.InstrumentedText(b"abab"))
+
+
+@pytest.mark.parametrize("sigma,m", [(16, 8), (64, 16), (256, 9), (95, 40), (32, 200)])
+def test_mp_batched_single_pass(cuda, sigma, m):
+    """K5 multi-pattern pass (selective ALIGNED batches): CSR equals per-pattern oracle results,
+    including duplicate patterns, planted repeats and patterns longer than the text."""
+    rng = np.random.default_rng(sigma * 1000 + m)
+    n = 3 * TILE + 4099
+    t = bytearray(rand_bytes(rng, sigma, n))
+    pats = [bytes(t[i : i + m]) for i in rng.integers(0, n - m, 300)]
+    pats += [pats[0], pats[1], rand_bytes(rng, sigma, m)]
+    for s in (0, 7, TILE - 3, n - m):  # plant pattern 2 at edges / tile boundary
+        t[s : s + m] = pats[2]
+    t = bytes(t)
+    res = mb.search_many(pats, t)
+    for p, r in zip(pats, res):
+        assert r == oracle.search(p, t).tolist(), (len(p), p[:4])
+
+
+def test_mp_overflow_falls_back(cuda):
+    # a dense, selective-looking batch: every pattern occurs > LIST_CAP times per 2 KiB segment
+    rng = np.random.default_rng(5)
+    unit = rand_bytes(rng, 256, 40)
+    t = unit * 4000
+    pats = [unit[i:] + unit[:i] for i in range(16)]
+    res = mb.search_many(pats, t)
+    for p, r in zip(pats, res):
+        assert r == oracle.search(p, t).tolist()
