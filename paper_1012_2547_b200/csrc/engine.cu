@@ -648,11 +648,34 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   __syncthreads();
   int64_t run = s_excl + wbefore + inc - tsum;
   const int64_t seg_per_pat = P.ntiles * NWARP;
+  // Sorted sparse segments (<= LIST_CAP uint16 offsets) are expanded right here,
+  // their offsets never leave registers; dense or unsorted (MP) segments are
+  // queued for expand_kernel with their offset.
+  const bool fuse = P.out && !P.unsorted_lists;
+  int cur_k = -1;
+  int64_t shift = 0;
 #pragma unroll
   for (int q = 0; q < PER; q++) {
     const int64_t t = base + (int64_t)tid * PER + q;
     if (t < nseg) {
-      if (v[q]) P.toff[t] = run;  // read only for non-empty segments
+      if (v[q] && P.out) {
+        if (fuse && v[q] <= (uint32_t)LIST_CAP) {
+          const int64_t tile = t / NWARP;
+          const int k = (int)(tile / P.ntiles);
+          if (k != cur_k) {
+            shift = P.pats[k].delta + P.off;
+            cur_k = k;
+          }
+          const int64_t pos0 = (tile % P.ntiles) * TILE - shift;
+          const uint16_t* L = P.lists + t * LIST_CAP;
+          for (uint32_t e = 0; e < v[q]; e++)
+            if (run + e < P.cap) P.out[run + e] = pos0 + L[e];
+        } else {
+          P.toff[t] = run;
+          const unsigned long long slot = atomicAdd(&P.ticket[TICKET_DENSE], 1ULL);
+          P.seglist[slot] = t;
+        }
+      }
       if (t % seg_per_pat == seg_per_pat - 1) P.offsets_plus1[t / seg_per_pat] = run + v[q];
     }
     run += v[q];
@@ -660,28 +683,21 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
 }
 
 // ------------------------------------------------ kernel 3: expansion
-// A warp takes 32 consecutive segments per step: one coalesced load of their
-// counts, a ballot of the non-empty ones, then a warp-cooperative expansion of
-// each: sparse segments copy their uint16 list, dense ones expand the 64-word
-// bitmap 32 words at a time through a per-warp smem staging buffer so every
-// global store is a coalesced run.
+// The segments offsets_kernel queued (dense, or MP's unsorted lists), a warp
+// per segment: unsorted lists get a 32-lane bitonic sort, dense segments
+// expand their 64-word bitmap 32 words at a time through a per-warp smem
+// staging buffer so every global store is a coalesced run.
 constexpr int EXP_WARPS = 4;
 __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
   __shared__ int64_t stage[EXP_WARPS][1024];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nseg = P.total_tiles * NWARP;
-  const int64_t ngroups = (nseg + 31) / 32;
+  const int64_t nq = (int64_t)P.ticket[TICKET_DENSE];
   int cur_k = -1;
   int64_t shift = 0;
-  for (int64_t grp = (int64_t)blockIdx.x * EXP_WARPS + warp; grp < ngroups; grp += (int64_t)gridDim.x * EXP_WARPS) {
-    const int64_t gl = grp * 32 + lane;
-    const uint32_t myc = gl < nseg ? (uint32_t)P.counts[gl] : 0u;
-    uint32_t todo = __ballot_sync(0xffffffffu, myc != 0);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int64_t g = grp * 32 + src;
-      const uint32_t c = __shfl_sync(0xffffffffu, myc, src);
+  for (int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp; qi < nq; qi += (int64_t)gridDim.x * EXP_WARPS) {
+    {
+      const int64_t g = P.seglist[qi];
+      const uint32_t c = P.counts[g];
       const int64_t tile = g / NWARP;
       const int k = (int)(tile / P.ntiles);
       if (k != cur_k) {
@@ -962,6 +978,8 @@ struct mb_ctx {
   int64_t bitmaps_cap = 0;
   int64_t* toff = nullptr;
   int64_t toff_cap = 0;
+  int64_t* seglist = nullptr;
+  int64_t seglist_cap = 0;
   int32_t* plist = nullptr;
   int64_t plist_cap = 0;
   std::vector<int32_t> h_plist;
@@ -1080,6 +1098,7 @@ void mb_ctx_destroy(mb_ctx* c) {
   cudaFree(c->lists);
   cudaFree(c->bitmaps);
   cudaFree(c->toff);
+  cudaFree(c->seglist);
   cudaFree(c->plist);
   cudaFree(c->mp_tab);
   cudaFree(c->ticket);
@@ -1290,6 +1309,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   if ((rc = grow(&c->lists, &c->lists_cap, T * LIST_CAP, "lists"))) return rc;
   if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * SEG_WORDS, "bitmaps"))) return rc;
   if ((rc = grow(&c->toff, &c->toff_cap, T, "tile offsets"))) return rc;
+  if ((rc = grow(&c->seglist, &c->seglist_cap, T, "expand queue"))) return rc;
   if (nchunks > c->state_cap || c->epoch >= (1u << 24) - 4) {
     if ((rc = grow(&c->state, &c->state_cap, nchunks, "look-back state"))) return rc;
     CUDA_TRY(cudaMemsetAsync(c->state, 0, sizeof(uint64_t) * c->state_cap, st));
@@ -1299,6 +1319,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.lists = c->lists;
   P.bitmaps = c->bitmaps;
   P.toff = c->toff;
+  P.seglist = c->seglist;
   P.state = c->state;
   P.ticket = c->ticket;
   P.out = d_out;
@@ -1313,7 +1334,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     if (d_out && cap > 0) {
-      const int64_t eg = std::min<int64_t>((T + 32 * EXP_WARPS - 1) / (32 * EXP_WARPS), (int64_t)c->nsm * 16);
+      const int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS, (int64_t)c->nsm * 16);
       expand_kernel<<<(int)eg, EXP_WARPS * 32, 0, st>>>(P);
       g_launches++;
       CUDA_TRY(cudaGetLastError());

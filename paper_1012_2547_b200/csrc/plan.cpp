@@ -68,34 +68,6 @@ constexpr double K2_MAX_ENTROPY = -1.0;
 
 static inline int round16(int64_t x) { return (int)((x + 15) & ~(int64_t)15); }
 
-// Anchor choice: the window of `len` pattern bytes whose bytes are rarest.  Byte
-// rarity comes from the caller's text histogram when given, else from the
-// pattern's own byte counts (a proxy: patterns are drawn from the text).  For
-// a^(m-1)b in an 'a'-heavy text this picks the window holding 'b', keeping the
-// candidate rate near the true match rate.
-static int choose_anchor(const uint8_t* p, int64_t m, int len, const int64_t* hist) {
-  double w[256];
-  if (hist) {
-    double tot = 0;
-    for (int c = 0; c < 256; c++) tot += (double)hist[c];
-    for (int c = 0; c < 256; c++) w[c] = std::log(((double)hist[c] + 0.5) / (tot + 128.0));
-  } else {
-    int64_t cnt[256] = {0};
-    for (int64_t i = 0; i < m; i++) cnt[p[i]]++;
-    for (int c = 0; c < 256; c++) w[c] = std::log(((double)cnt[c] + 0.5) / ((double)m + 128.0));
-  }
-  int best = 0;
-  double best_s = 1e300;
-  for (int64_t a = 0; a + len <= m; a++) {
-    double s = 0;
-    for (int k = 0; k < len; k++) s += w[p[a + k]];
-    if (s < best_s - 1e-9) {
-      best_s = s;
-      best = (int)a;
-    }
-  }
-  return best;
-}
 
 // K3 sampled q-gram filter: every occurrence of p contains the
 // q-gram at exactly one text position x = S*i (S <= m - q + 1), at pattern offset
@@ -160,6 +132,45 @@ static bool build_sampled(const uint8_t* pat, int64_t m, PlanHost* ph) {
   return false;
 }
 
+// Filter-rate model: expected anchor hits per aligned text word, with byte
+// probabilities from the caller's text histogram or, as a proxy, the
+// pattern's own (smoothed) byte counts.
+static void byte_probs(const uint8_t* p, int64_t m, const int64_t* hist, double* pr) {
+  if (hist) {
+    double tot = 0;
+    for (int c = 0; c < 256; c++) tot += (double)hist[c];
+    for (int c = 0; c < 256; c++) pr[c] = ((double)hist[c] + 0.5) / (tot + 128.0);
+  } else {
+    double cnt[256] = {0};
+    for (int64_t i = 0; i < m; i++) cnt[p[i]] += 1;
+    for (int c = 0; c < 256; c++) pr[c] = (cnt[c] + 0.05) / ((double)m + 12.8);
+  }
+}
+static double gram_prob(const uint8_t* g, const double* pr) { return pr[g[0]] * pr[g[1]] * pr[g[2]] * pr[g[3]]; }
+
+// ALIGNED: the 7-byte window minimising sum_j P(p[a+j..a+j+4)), j = 0..3.
+static int best_aligned(const uint8_t* p, int64_t m, const double* pr, double* rate) {
+  int best = 0;
+  double br = 1e300;
+  for (int64_t a = 0; a + 7 <= m; a++) {
+    const double r = gram_prob(p + a, pr) + gram_prob(p + a + 1, pr) + gram_prob(p + a + 2, pr) + gram_prob(p + a + 3, pr);
+    if (r < br * (1 - 1e-12)) br = r, best = (int)a;
+  }
+  *rate = br;
+  return best;
+}
+// WIN4: one 4-byte window tested at all 4 byte phases of a word: 4 * P(gram).
+static int best_win4(const uint8_t* p, int64_t m, const double* pr, double* rate) {
+  int best = 0;
+  double br = 1e300;
+  for (int64_t a = 0; a + 4 <= m; a++) {
+    const double r = 4 * gram_prob(p + a, pr);
+    if (r < br * (1 - 1e-12)) br = r, best = (int)a;
+  }
+  *rate = br;
+  return best;
+}
+
 int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost* ph, std::string* err) {
   if (m < 1) {
     *err = "pattern must have length >= 1";
@@ -194,8 +205,9 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
     else if (m <= 64 && ph->entropy <= K2_MAX_ENTROPY)
       fam = MB_FAM_SHIFTOR;  // small alphabet: 4-byte anchors are unselective, shift-or needs no verify
     else
-      fam = MB_FAM_ALIGNED;
+      fam = MB_FAM_ALIGNED;  // may become SAMPLED or WIN4 below
   }
+  const bool auto_long = (opts == nullptr || opts->family == MB_FAM_AUTO) && fam == MB_FAM_ALIGNED;
   bool sampled_ok = false;
   if (fam == MB_FAM_AUTO || fam == MB_FAM_ALIGNED || fam == MB_FAM_SAMPLED) {
     PlanHost tmp;
@@ -209,6 +221,16 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       ph->dev.q = tmp.dev.q;
       ph->dev.B = tmp.dev.B;
     }
+  }
+  if (auto_long && fam == MB_FAM_ALIGNED) {
+    // ALIGNED tests 4 grams of one 7-byte window per word; WIN4 one gram at
+    // every byte phase.  When the rare bytes of a pattern fit only one gram
+    // (a^(m-1)b: 'aaab' vs three 'aaaa' grams) WIN4 is far more selective.
+    double pr[256], ra, rw;
+    byte_probs(pat, m, hist, pr);
+    best_aligned(pat, m, pr, &ra);
+    best_win4(pat, m, pr, &rw);
+    if (8 * rw < ra && !(m >= 16 && ph->period <= m / 2)) fam = MB_FAM_WIN4;
   }
   if (opts && opts->family == MB_FAM_SAMPLED && !sampled_ok) {
     *err = "sampled q-gram family does not apply to this pattern (m < 272, low entropy or periodic)";
@@ -241,7 +263,9 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       d.exact = 1;
       break;
     case MB_FAM_WIN4: {
-      int a = choose_anchor(pat, m, 4, hist);
+      double pr[256], rw;
+      byte_probs(pat, m, hist, pr);
+      int a = best_win4(pat, m, pr, &rw);
       ph->anchor = a;
       d.delta = a;
       d.G[0] = load_le32(pat + a);
@@ -249,7 +273,9 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       break;
     }
     case MB_FAM_ALIGNED: {
-      int a = choose_anchor(pat, m, 7, hist);
+      double pr[256], ra;
+      byte_probs(pat, m, hist, pr);
+      int a = best_aligned(pat, m, pr, &ra);
       ph->anchor = a;
       d.delta = a + 3;
       for (int j = 0; j < 4; j++) d.G[j] = load_le32(pat + a + j);

@@ -38,6 +38,7 @@ constexpr int SCAN_CHUNK = 4096;  // segment counts per offsets_kernel CTA
 constexpr int TICKET_OFFSETS = 7; // ticket slot of offsets_kernel (slots 0..6: family groups)
 constexpr int MAX_GROUPS = 7;
 constexpr int TICKET_MP0 = 8;     // MP chunk tickets use slots 8..14 (ticket array has 16)
+constexpr int TICKET_DENSE = 15;  // number of segments queued for expand_kernel
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 
 struct StageHdr {
@@ -74,7 +75,8 @@ struct ScanParams {
   uint16_t* counts;     // per segment (tile * NWARP + warp); <= SEG
   uint16_t* lists;      // per segment LIST_CAP tile-relative offsets
   uint32_t* bitmaps;    // per segment SEG_WORDS words (dense segments only)
-  int64_t* toff;        // per segment exclusive output offset
+  int64_t* toff;        // per segment exclusive output offset (queued segments only)
+  int64_t* seglist;     // segments queued for expand_kernel (count in ticket[TICKET_DENSE])
   uint64_t* state;      // look-back flags of offsets_kernel (per chunk)
   uint32_t epoch;
   int64_t* out;         // positions (may be null: count only)

@@ -124,9 +124,14 @@ def test_descriptor_substitution_seam():
 
 def test_plan_info_families():
     cases = {1: "swar", 3: "swar", 4: "win4", 6: "win4", 7: "aligned", 64: "aligned", 65: "aligned",
-             1024: "aligned", 8192: "aligned"}
+             271: "aligned", 1024: "sampled", 8192: "sampled"}
+    rng0 = np.random.default_rng(0)
     for m, fam in cases.items():
-        assert engine.Plan(b"\x05" * (m - 1) + b"\x07").info().family == fam
+        assert engine.Plan(rng0.integers(0, 256, m, dtype=np.uint8).tobytes()).info().family == fam, m
+    # rare byte confined to one gram (a^(m-1)b, b a^(m-1)): one-gram WIN4 anchor beats ALIGNED
+    for m in (16, 128, 1024, 8192):
+        assert engine.Plan(b"\x05" * (m - 1) + b"\x07").info().family == "win4", m
+        assert engine.Plan(b"\x07" + b"\x05" * (m - 1)).info().family == "win4", m
     assert engine.Plan(b"a" * 100).info().periodic
     assert not engine.Plan(b"a" * 99 + b"b").info().periodic
     with pytest.raises(ValueError):
@@ -135,7 +140,7 @@ def test_plan_info_families():
         engine.Plan(b"abc", family="aligned")
     # anchor choice keeps the rare byte of a^(m-1)b inside the anchor window
     info = engine.Plan(b"a" * 127 + b"b").info()
-    assert info.anchor <= 127 <= info.anchor + 6
+    assert info.anchor <= 127 <= info.anchor + 3
     rng = np.random.default_rng(1)
     long_random = rng.integers(0, 256, 1024, dtype=np.uint8).tobytes()
     assert engine.Plan(long_random).info().family == "sampled"
