@@ -190,13 +190,19 @@ __device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* p
 // Per-warp break bitmap of a segment: bit q of word i set iff
 // t[y] != t[y + per] for y = y0 + 32 i + q (y relative to the segment's first
 // start position).  nbw[i] = first break at or after word i (relative to y0).
+__device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {  // unaligned 4-byte smem read
+  const uintptr_t a = (uintptr_t)p;
+  const uint32_t* b = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  return __funnelshift_r(b[0], b[1], 8 * (uint32_t)(a & 3));
+}
+
 __device__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* brk, int32_t* nbw) {
   const int lane = threadIdx.x & 31;
-  for (int i = lane; i < nwords; i += 32) {
+  for (int i = lane; i < nwords; i += 32) {  // SWAR: 4 byte pairs per compare
     const uint8_t* q = Yseg + 32 * i;
     uint32_t bits = 0;
-#pragma unroll 8
-    for (int b = 0; b < 32; b++) bits |= (uint32_t)(q[b] != q[b + per]) << b;
+#pragma unroll
+    for (int b = 0; b < 32; b += 4) bits |= ((~zero_bytes4(lds32u(q + b) ^ lds32u(q + b + per))) & 0xFu) << b;
     brk[i] = bits;
   }
   __syncwarp();
@@ -366,33 +372,53 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
       // ---- verify (exact filters skip this)
       if (!pd.exact && __any_sync(0xffffffffu, (w0 | w1) != 0)) {
         const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
-        if (pd.periodic) warp_breaks(Y0 + c0, pd.per, (SEG + pd.L + 31) / 32, brk, nbw);
-        uint32_t ws[2] = {w0, w1};
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          uint32_t cw = ws[h], mw = 0;
-          while (cw) {
-            const int i = __ffs(cw) - 1;
-            cw &= cw - 1;
-            const int rel = c0 + 32 * (2 * lane + h) + i;
-            bool ok;
-            if (pd.periodic) {
-              ok = verify_direct(Y0 + rel, spat, pd.per);
-              if (ok) {
-                const int q = rel - c0;
-                const uint32_t x = brk[q >> 5] >> (q & 31);
-                const int nb = x ? q + __ffs(x) - 1 : nbw[(q >> 5) + 1];
-                ok = nb >= q + pd.L;
-              }
-            } else {
-              ok = verify_direct(Y0 + rel, spat, (int)pd.m);
+        if (pd.periodic) {
+          // s matches <=> t[s..s+per) = p[0..per) and no break t[y] != t[y+per] for
+          // y in [s, s+L).  A break y kills starts [y-L+1, y]: walk the few breaks
+          // that reach this lane's 64 starts, mask them out in bulk.
+          const int nwords = (SEG + pd.L + 31) / 32;
+          warp_breaks(Y0 + c0, pd.per, nwords, brk, nbw);
+          uint64_t cand = ((uint64_t)w1 << 32) | w0;
+          if (cand) {
+            auto nb = [&](int y) -> int {
+              if (y >= 32 * nwords) return 0x7fffffff;
+              const uint32_t x = brk[y >> 5] >> (y & 31);
+              return x ? y + __ffs(x) - 1 : nbw[(y >> 5) + 1];
+            };
+            const int q0 = 64 * lane, q1 = q0 + 63;
+            uint64_t killed = 0;
+            for (int y = nb(q0); y != 0x7fffffff && y - pd.L + 1 <= q1; y = nb(y + 1)) {
+              const int lo = max(q0, y - pd.L + 1) - q0, hi = min(q1, y) - q0;
+              if (lo <= hi) killed |= (hi - lo == 63) ? ~0ULL : (((1ULL << (hi - lo + 1)) - 1) << lo);
+              if (y >= q1) break;
             }
-            if (ok) mw |= 1u << i;
+            cand &= ~killed;
+            if (pd.per > 4) {  // the 4 anchor bytes do not cover a full period: check one block
+              uint64_t cc = cand;
+              while (cc) {
+                const int i = __ffsll((long long)cc) - 1;
+                cc &= cc - 1;
+                if (!verify_direct(Y0 + c0 + q0 + i, spat, pd.per)) cand &= ~(1ULL << i);
+              }
+            }
           }
-          ws[h] = mw;
+          w0 = (uint32_t)cand;
+          w1 = (uint32_t)(cand >> 32);
+        } else {
+          uint32_t ws[2] = {w0, w1};
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            uint32_t cw = ws[h], mw = 0;
+            while (cw) {
+              const int i = __ffs(cw) - 1;
+              cw &= cw - 1;
+              if (verify_direct(Y0 + c0 + 32 * (2 * lane + h) + i, spat, (int)pd.m)) mw |= 1u << i;
+            }
+            ws[h] = mw;
+          }
+          w0 = ws[0];
+          w1 = ws[1];
         }
-        w0 = ws[0];
-        w1 = ws[1];
       }
       // ---- count + compact store (segment g = tile * NWARP + warp)
       const uint32_t c2 = __popc(w0) + __popc(w1);
@@ -689,7 +715,6 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
 // staging buffer so every global store is a coalesced run.
 constexpr int EXP_WARPS = 4;
 __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
-  __shared__ int64_t stage[EXP_WARPS][1024];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nq = (int64_t)P.ticket[TICKET_DENSE];
   int cur_k = -1;
@@ -723,33 +748,40 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
         if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + v;
         continue;
       }
+      // dense: the 64 bitmap words (2 per lane), exclusive popcount prefix, then
+      // one word per step broadcast to the warp -- lane i writes bit i's
+      // position at its rank, so a full word is one coalesced 256-byte store
       const uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
       const int64_t segpos = pos0 + (g % NWARP) * SEG;
-      int64_t w_out = o;
-      for (int wb = 0; wb < SEG_WORDS; wb += 32) {
-        const uint32_t x = bmw[wb + lane];
-        const uint32_t pc = __popc(x);
-        uint32_t inc = pc;
+      const uint32_t xa = bmw[lane], xb = bmw[32 + lane];
+      const uint32_t pa = __popc(xa), pb = __popc(xb);
+      uint32_t ia = pa, ib = pb;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
-          if (lane >= d) inc += v;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t va = __shfl_up_sync(0xffffffffu, ia, d);
+        const uint32_t vb = __shfl_up_sync(0xffffffffu, ib, d);
+        if (lane >= d) ia += va, ib += vb;
+      }
+      const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31);
+      const uint32_t ea = ia - pa, eb = ta + ib - pb;
+      const uint32_t below = (1u << lane) - 1u;
+#pragma unroll 4
+      for (int w = 0; w < 32; w++) {
+        const uint32_t x = __shfl_sync(0xffffffffu, xa, w);
+        const uint32_t e = __shfl_sync(0xffffffffu, ea, w);
+        if ((x >> lane) & 1u) {
+          const int64_t idx = o + e + __popc(x & below);
+          if (idx < P.cap) P.out[idx] = segpos + 32 * w + lane;
         }
-        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-        if (total == 0) continue;
-        uint32_t j = inc - pc;
-        uint32_t xx = x;
-        const int64_t pb = segpos + 32 * (wb + lane);
-        while (xx) {
-          const int i = __ffs(xx) - 1;
-          xx &= xx - 1;
-          stage[warp][j++] = pb + i;
+      }
+#pragma unroll 4
+      for (int w = 0; w < 32; w++) {
+        const uint32_t x = __shfl_sync(0xffffffffu, xb, w);
+        const uint32_t e = __shfl_sync(0xffffffffu, eb, w);
+        if ((x >> lane) & 1u) {
+          const int64_t idx = o + e + __popc(x & below);
+          if (idx < P.cap) P.out[idx] = segpos + 32 * (32 + w) + lane;
         }
-        __syncwarp();
-        for (uint32_t q = lane; q < total; q += 32)
-          if (w_out + q < P.cap) P.out[w_out + q] = stage[warp][q];
-        __syncwarp();
-        w_out += total;
       }
     }
   }
