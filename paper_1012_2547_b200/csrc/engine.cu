@@ -404,6 +404,33 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
           }
           w0 = (uint32_t)cand;
           w1 = (uint32_t)(cand >> 32);
+        } else if (pd.m >= 64) {
+          // long windows: the whole warp verifies one candidate at a time,
+          // lane l comparing 4-byte words l, l+32, ... (smem text vs pattern)
+          const uint64_t mine = ((uint64_t)w1 << 32) | w0;
+          uint64_t keep = 0;
+          uint32_t active = __ballot_sync(0xffffffffu, mine != 0);
+          while (active) {
+            const int src = __ffs(active) - 1;
+            active &= active - 1;
+            uint64_t cm = ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(mine >> 32), src) << 32) |
+                          __shfl_sync(0xffffffffu, (uint32_t)mine, src);
+            while (cm) {
+              const int i = __ffsll((long long)cm) - 1;
+              cm &= cm - 1;
+              const uint8_t* tw = Y0 + c0 + 64 * src + i;
+              bool bad = false;
+              for (int k = 4 * lane; k < pd.m; k += 128) {
+                const uint32_t pw = *reinterpret_cast<const uint32_t*>(spat + k);
+                uint32_t diff = lds32u(tw + k) ^ pw;
+                if (pd.m - k < 4) diff &= (1u << (8 * (pd.m - k))) - 1u;
+                bad |= diff != 0;
+              }
+              if (!__any_sync(0xffffffffu, bad) && lane == src) keep |= 1ULL << i;
+            }
+          }
+          w0 = (uint32_t)keep;
+          w1 = (uint32_t)(keep >> 32);
         } else {
           uint32_t ws[2] = {w0, w1};
 #pragma unroll
