@@ -20,6 +20,25 @@
 
 namespace mb {
 
+// Bounds assertions for the debug build (make debug -> libmatchb200_dbg.so):
+// every shared-memory window a kernel reads is checked against its stage and
+// every global read against the text; a violation traps.  compute-sanitizer is
+// closed on this GPU pool, so this build stands in for memcheck
+// (tests/test_gpu_bounds.py).  Compiled out of the product library.
+#ifdef MB_BOUNDS_CHECK
+#define MB_CHECK(cond)                                                  \
+  do {                                                                  \
+    if (!(cond)) {                                                      \
+      printf("MB_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__); \
+      __trap();                                                         \
+    }                                                                   \
+  } while (0)
+#else
+#define MB_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -316,6 +335,10 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
     const int64_t B0 = hdr[s].tau * TILE;
     const uint8_t* spat = stages + s * P.stage_bytes;
     const uint8_t* S = spat + P.pat_cap + P.pre;  // S[c] = virtual text byte B0 + c
+    const uint8_t* const sbeg = spat + P.pat_cap;  // staged text window [sbeg, send)
+    const uint8_t* const send = spat + P.stage_bytes;
+    (void)sbeg, (void)send;
+    MB_CHECK(S + c0 + SEG + 4 <= send);
     const int64_t segb = B0 + c0;
     const bool interior = segb >= blo && segb + SEG - 1 <= bhi;
 
@@ -324,6 +347,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
     bool have;
     if constexpr (is_shiftor<Filt>::value) {
       // ---- K2: exact per-lane shift-or over positions [c0 + 64 lane, +64)
+      MB_CHECK(S + c0 + 64 * lane + 64 + pd.m + 3 <= send);
       shiftor_lane<Filt::kW>(S + c0 + 64 * lane, (int)pd.m, so_s, w0, w1);
       if (!interior) {
         const int64_t b = segb + 64 * lane;
@@ -377,6 +401,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
           // y in [s, s+L).  A break y kills starts [y-L+1, y]: walk the few breaks
           // that reach this lane's 64 starts, mask them out in bulk.
           const int nwords = (SEG + pd.L + 31) / 32;
+          MB_CHECK(Y0 + c0 >= sbeg && Y0 + c0 + 32 * nwords + pd.per + 8 <= send);
           warp_breaks(Y0 + c0, pd.per, nwords, brk, nbw);
           uint64_t cand = ((uint64_t)w1 << 32) | w0;
           if (cand) {
@@ -398,6 +423,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
               while (cc) {
                 const int i = __ffsll((long long)cc) - 1;
                 cc &= cc - 1;
+                MB_CHECK(Y0 + c0 + q0 + i >= sbeg && Y0 + c0 + q0 + i + pd.per <= send);
                 if (!verify_direct(Y0 + c0 + q0 + i, spat, pd.per)) cand &= ~(1ULL << i);
               }
             }
@@ -419,6 +445,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
               const int i = __ffsll((long long)cm) - 1;
               cm &= cm - 1;
               const uint8_t* tw = Y0 + c0 + 64 * src + i;
+              MB_CHECK(tw >= sbeg && tw + pd.m + 8 <= send);
               bool bad = false;
               for (int k = 4 * lane; k < pd.m; k += 128) {
                 const uint32_t pw = *reinterpret_cast<const uint32_t*>(spat + k);
@@ -439,6 +466,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
             while (cw) {
               const int i = __ffs(cw) - 1;
               cw &= cw - 1;
+              MB_CHECK(Y0 + c0 + 32 * (2 * lane + h) + i >= sbeg && Y0 + c0 + 32 * (2 * lane + h) + i + pd.m <= send);
               if (verify_direct(Y0 + c0 + 32 * (2 * lane + h) + i, spat, (int)pd.m)) mw |= 1u << i;
             }
             ws[h] = mw;
@@ -508,6 +536,7 @@ __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& 
     const int64_t bit = sv + pd.delta;  // = x - j + S - 1, inside [x, x + S)
     if (bit < ulo || bit >= uhi || bit < blo || bit > bhi) continue;
     const uint8_t* tp = P.text + sv;
+    MB_CHECK(sv >= P.off && sv + pd.m <= P.off + P.n);
     bool ok = true;
     for (int c = 0; c < pd.m && ok; c++) ok = __ldg(tp + c) == spat[c];
     if (ok) found[nf++] = (uint32_t)(bit - ulo);
@@ -568,6 +597,7 @@ __global__ void __launch_bounds__(NT) sampled_kernel(const ScanParams P) {
         const int64_t i = ib + r * 32 + lane;
         const int64_t x = S * i;
         if (i <= i1 && x + q <= tlimit) {
+          MB_CHECK(x >= 0 && x + 16 * (q == 32 ? 2 : 1) <= P.nv16 && (x & 15) == 0);
           g[r] = __ldcs(reinterpret_cast<const uint4*>(P.text + x));
           if (q == 32) g2[r] = __ldcs(reinterpret_cast<const uint4*>(P.text + x + 16));
         }
@@ -909,6 +939,7 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
           const int64_t m = pd->m;
           if (spos < 0 || spos + m > P.n) continue;
           const uint8_t* tp = S + (sv - B0);
+          MB_CHECK(tp >= stages + s * P.stage_bytes && tp + m <= stages + (s + 1) * P.stage_bytes);
           const uint8_t* pp = pd->bytes;
           bool ok = true;
           for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);

@@ -17,7 +17,9 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmatchb200.so")
+# MB_ENGINE_LIB selects another build of the same ABI (the bounds-checked
+# libmatchb200_dbg.so in tests/test_gpu_bounds.py); default: the product library.
+LIB_PATH = os.environ.get("MB_ENGINE_LIB") or os.path.join(_HERE, "libmatchb200.so")
 
 MB_OK, MB_EINVAL, MB_ENOMEM, MB_ECUDA, MB_EOVERFLOW = 0, 1, 2, 3, 4
 MB_MAX_M = 8192
