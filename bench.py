@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "text GB/s scanned (all matches emitted) vs m and σ; % of HBM roofline"
 CFG4_LENGTHS = (2, 8, 32, 128, 1024)
 PEAK_FALLBACK = 6650.0  # B200_PROFILING.md fallback, GB/s
+BACKEND = os.environ.get("MB_BENCH_BACKEND", "nccl")  # gloo only for multi-rank tests on one GPU
 
 
 def parse():
@@ -43,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=("cfg4", "cfg1", "cfg2", "cfg3", "cfg3b", "cfg5"), default="cfg4")
-    ap.add_argument("--n", type=int, default=0, help="text bytes per GPU (default: the config's size)")
+    ap.add_argument("--text-bytes", dest="n", type=int, default=0, help="text bytes per GPU (default: the config's size)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -63,12 +64,15 @@ def measured_peak():
         return PEAK_FALLBACK, "B200_PROFILING.md fallback"
 
 
-def ncu_traffic(workload):
+def ncu_traffic(workload, alg_bytes_per_launch):
+    """DRAM bytes per launch of the dominant kernel: the ncu-measured ratio of
+    traffic to algorithmic bytes (profiles/ncu_summary.json) at this launch size."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+            d = json.load(f).get(workload, {})
+        ratio = d["dram_bytes_per_launch"] / d["algorithmic_bytes_per_launch_min"]
+        return int(round(ratio * alg_bytes_per_launch))
     except Exception:
         return None
 
@@ -272,7 +276,7 @@ def run_ours(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     wl = build_workload(args, rank, world)
     n, halo, pats = wl["n"], wl["halo"], wl["patterns"]
@@ -295,8 +299,9 @@ def run_ours(args, rank, world, local_rank):
             if ev is not None:
                 ev[i][1].record(stream)
         if dist is not None:  # exchange: global output offsets from per-rank counts
-            allc = [torch.empty_like(cnt) for _ in range(world)]
-            dist.all_gather(allc, cnt)
+            src = cnt if BACKEND == "nccl" else cnt.cpu()
+            allc = [torch.empty_like(src) for _ in range(world)]
+            dist.all_gather(allc, src)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -323,7 +328,7 @@ def run_ours(args, rank, world, local_rank):
     clocks = clk.stop() if clk else None
     ms = t_start.elapsed_time(t_end) / args.steps
     if dist is not None:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        tt = torch.tensor([ms], device=dev if BACKEND == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     counts = cnt.cpu().tolist()
@@ -337,7 +342,6 @@ def run_ours(args, rank, world, local_rank):
     # they are reported per m with that traffic model instead.
     infos = [pl.info() for pl in plans]
     peak, peak_src = measured_peak()
-    traffic = ncu_traffic(args.workload)
     avg_ms = [statistics.mean(x) for x in per_launch]
     full = [i for i, inf in enumerate(infos) if inf.family != "sampled"]
     per_m = []
@@ -353,6 +357,7 @@ def run_ours(args, rank, world, local_rank):
                       **({"stride": inf.stride, "gram": inf.gram} if inf.family == "sampled" else {})})
     sel = full if full else list(range(K))
     achieved = sum(per_m[i]["alg_bytes"] for i in sel) / (sum(avg_ms[i] for i in sel) * 1e-3) / 1e9
+    traffic = ncu_traffic(args.workload, statistics.mean(per_m[i]["alg_bytes"] for i in sel))
 
     parity = None
     if not args.no_parity and rank == 0:
@@ -385,7 +390,7 @@ def run_ours(args, rank, world, local_rank):
             times.append(time.perf_counter() - t0)
         dt = statistics.median(times)
         if dist is not None:
-            tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+            tt = torch.tensor([dt], device=dev if BACKEND == "nccl" else "cpu", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
         e2e = {"value": round(world * K * n / dt / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(n + sum(map(len, pats))),
@@ -498,8 +503,11 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(local_rank % torch.cuda.device_count())
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:  # MB_BENCH_BACKEND=gloo: multi-rank plumbing test with ranks sharing GPUs
+            dist.init_process_group("gloo")
     try:
         if args.workload in ("cfg2", "cfg3b"):
             run_batched_sweep(args, rank, world, local_rank)

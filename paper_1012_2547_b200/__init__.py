@@ -19,6 +19,18 @@ from .core import (
     brute_force_search,
     verify_equal,
 )
+from .harness import (
+    ALLOWED_SIGMAS,
+    DEFAULT_LENGTHS,
+    BenchConfig,
+    Measurement,
+    generate_rand_text,
+    run_benchmark,
+    sample_patterns,
+    sample_positions,
+    standard_texts,
+    state_word_count,
+)
 from .registry import (
     B200,
     DEFAULT_SELECTION_MAP,

@@ -54,3 +54,13 @@ def test_bench_rows_reference_format(cuda, tmp_path):
     cells = {(r[3], int(r[4])) for r in rows[1:]}
     assert cells == {("B200", 4), ("B200", 32), ("HOR", 4), ("HOR", 32), ("SSEF", 32)}  # SSEF m>=32
     assert all(float(r[5]) > 0 and r[8] == "time" and int(r[1]) == 4 for r in rows[1:])
+
+
+def test_run_benchmark_mirror(cuda):
+    import paper_1012_2547_b200 as mb
+
+    text = mb.generate_rand_text(4, 1 << 16, seed=3)
+    cfg = mb.BenchConfig(lengths=(4, 32), patterns_per_length=2)
+    ms = mb.run_benchmark(cfg, [text], [mb.get_algorithm("B200"), mb.get_algorithm("SSEF")])
+    assert {(x.algorithm, x.m) for x in ms} == {("B200", 4), ("B200", 32), ("SSEF", 32)}
+    assert all(x.metric == "time" and x.mean_value > 0 and x.runs == 2 and x.sigma == 4 for x in ms)

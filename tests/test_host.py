@@ -216,3 +216,24 @@ def test_sharded_search_gloo(world):
             assert off == len(merged)
             merged += local
         assert merged == want
+
+
+def test_harness_mirror_matches_reference_streams():
+    import hashlib
+    import json
+
+    from paper_1012_2547_b200 import harness
+    from paper_1012_2547_b200.inputs import ROOT_SEED, derive_seed
+
+    fx = json.load(open(os.path.join(ROOT, "tests", "golden", "configs.json")))
+    cfg1 = harness.generate_rand_text(4, 1 << 20, derive_seed(ROOT_SEED, "cfg1", "text"))
+    assert hashlib.sha1(cfg1.data).hexdigest()[:16] == fx["cfg1"]["text"]
+    (p,) = harness.sample_patterns(cfg1, 8, 1, derive_seed(ROOT_SEED, "cfg1", "pat"))
+    assert p.data.hex() == fx["cfg1"]["pattern"]
+    assert harness.state_word_count(64) == 1 and harness.state_word_count(65) == 2
+    with pytest.raises(ValueError):
+        harness.generate_rand_text(3, 10, 1)
+    with pytest.raises(ValueError):
+        harness.BenchConfig(lengths=(4, 2))
+    with pytest.raises(ValueError):
+        harness.run_benchmark(harness.BenchConfig(metric="reads"), [cfg1])
