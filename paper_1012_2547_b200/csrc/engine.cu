@@ -519,6 +519,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
 constexpr int SMP_SEGS = 64;     // segments per warp unit (= 8 tiles)
 constexpr int SMP_LIST = 1024;   // per-warp match capacity per unit (bound: 131072/per + 2 < 1024)
 constexpr int SMP_ILP = 4;       // samples per lane per batch
+constexpr int SMP_WARPS = 8;     // warps per sampled_kernel CTA (independent of the scan tiling)
+constexpr int SMP_NT = SMP_WARPS * 32;
 __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& pd, const uint32_t* bloom,
                                              const uint16_t* bstart, const uint16_t* bent, const uint8_t* spat,
                                              const uint32_t* w, int64_t x, int64_t ulo, int64_t uhi, int64_t blo,
@@ -544,18 +546,18 @@ __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& 
   return nf;
 }
 
-__global__ void __launch_bounds__(NT) sampled_kernel(const ScanParams P) {
+__global__ void __launch_bounds__(SMP_NT) sampled_kernel(const ScanParams P) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* bloom = reinterpret_cast<uint32_t*>(smem);                 // 2048 words
   uint16_t* bstart = reinterpret_cast<uint16_t*>(smem + 8192);         // <= 1025
   uint16_t* bent = reinterpret_cast<uint16_t*>(smem + 8192 + 2064);    // <= 4096
-  uint32_t* lists = reinterpret_cast<uint32_t*>(smem + 8192 + 2064 + 8192);  // [NWARP][SMP_LIST]
-  int64_t* s_ticket = reinterpret_cast<int64_t*>(lists + NWARP * SMP_LIST);
+  uint32_t* lists = reinterpret_cast<uint32_t*>(smem + 8192 + 2064 + 8192);  // [SMP_WARPS][SMP_LIST]
+  int64_t* s_ticket = reinterpret_cast<int64_t*>(lists + SMP_WARPS * SMP_LIST);
   uint8_t* spat = reinterpret_cast<uint8_t*>(s_ticket + 2);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t segs = P.ntiles * NWARP;                                   // segments per pattern
   const int64_t wunits = (segs + SMP_SEGS - 1) / SMP_SEGS;                 // warp units per pattern
-  const int64_t units = (wunits + NWARP - 1) / NWARP;                      // CTA units per pattern
+  const int64_t units = (wunits + SMP_WARPS - 1) / SMP_WARPS;              // CTA units per pattern
   const int64_t total = units * P.group_k;
   int cur_k = -1;
   PatDev pd;
@@ -571,14 +573,14 @@ __global__ void __launch_bounds__(NT) sampled_kernel(const ScanParams P) {
     if (k != cur_k) {  // load this pattern's tables (uniform across the CTA)
       pd = P.pats[k];
       const int nb = (1 << pd.B) + 1;
-      for (int i = tid; i < 2048; i += NT) bloom[i] = pd.bloom[i];
-      for (int i = tid; i < nb; i += NT) bstart[i] = pd.bstart[i];
-      for (int i = tid; i < pd.S; i += NT) bent[i] = pd.bent[i];
-      for (int i = tid; i < pd.m; i += NT) spat[i] = pd.bytes[i];
+      for (int i = tid; i < 2048; i += SMP_NT) bloom[i] = pd.bloom[i];
+      for (int i = tid; i < nb; i += SMP_NT) bstart[i] = pd.bstart[i];
+      for (int i = tid; i < pd.S; i += SMP_NT) bent[i] = pd.bent[i];
+      for (int i = tid; i < pd.m; i += SMP_NT) spat[i] = pd.bytes[i];
       cur_k = k;
       __syncthreads();
     }
-    const int64_t wu = u * NWARP + warp;
+    const int64_t wu = u * SMP_WARPS + warp;
     if (wu >= wunits) continue;
     const int64_t seg0 = wu * SMP_SEGS;
     const int nsegs = (int)(segs - seg0 < SMP_SEGS ? segs - seg0 : SMP_SEGS);
@@ -1244,7 +1246,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
   P.stage_bytes = (P.pat_cap + pre + TILE + post + 127) & ~127;
   P.brk_words = any_periodic ? ((((SEG + maxL + 31) / 32) + 1 + 3) & ~3) : 0;
   if constexpr (std::is_same<F, SampledTag>::value) {
-    const size_t smem_s = 8192 + 2064 + 8192 + NWARP * SMP_LIST * 4 + 16 + P.pat_cap + 16;
+    const size_t smem_s = 8192 + 2064 + 8192 + SMP_WARPS * SMP_LIST * 4 + 16 + P.pat_cap + 16;
     static std::mutex mu_s;
     static bool attr_s = false;
     static size_t occ_smem_s = 0;
@@ -1257,16 +1259,16 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
         attr_s = true;
       }
       if (occ_smem_s != smem_s) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, sampled_kernel, NT, smem_s));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, sampled_kernel, SMP_NT, smem_s));
         occ_smem_s = smem_s;
       }
       per_sm_s = occ_s;
     }
     if (per_sm_s < 1) return fail(MB_ECUDA, "sampled kernel does not fit on an SM");
     const int64_t wunits = (P.ntiles * NWARP + SMP_SEGS - 1) / SMP_SEGS;
-    const int64_t units = ((wunits + NWARP - 1) / NWARP) * gk;
+    const int64_t units = ((wunits + SMP_WARPS - 1) / SMP_WARPS) * gk;
     const int64_t grid_s = std::min<int64_t>(units, (int64_t)c->nsm * per_sm_s);
-    sampled_kernel<<<(int)grid_s, NT, smem_s, st>>>(P);
+    sampled_kernel<<<(int)grid_s, SMP_NT, smem_s, st>>>(P);
   } else {
     const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
                         (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * 256 * 8 : 0);

@@ -27,12 +27,18 @@
 
 namespace mb {
 
-constexpr int TILE = 16384;       // bitmap positions per tile (one TMA stage)
-constexpr int NWARP = 8;          // consumer warps; warp NWARP is the TMA producer
+#ifndef MB_NWARP
+#define MB_NWARP 16
+#endif
+#ifndef MB_STAGES
+#define MB_STAGES 3
+#endif
+constexpr int NWARP = MB_NWARP;   // consumer warps; warp NWARP is the TMA producer
+constexpr int TILE = NWARP * 2048; // bitmap positions per tile (one TMA stage): 2 KiB per consumer warp
 constexpr int NT = NWARP * 32;    // consumer threads
 constexpr int SEG = TILE / NWARP; // positions per consumer-warp segment
 constexpr int SEG_WORDS = SEG / 32;
-constexpr int STAGES = 4;         // TMA ring depth
+constexpr int STAGES = MB_STAGES;  // TMA ring depth
 constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offsets
 constexpr int SCAN_CHUNK = 4096;  // segment counts per offsets_kernel CTA
 constexpr int TICKET_OFFSETS = 7; // ticket slot of offsets_kernel (slots 0..6: family groups)
@@ -52,7 +58,7 @@ struct StageHdr {
 constexpr int SM_HDR = 0;
 constexpr int SM_FULL = SM_HDR + 32 * STAGES;
 constexpr int SM_EMPTY = SM_FULL + 8 * STAGES;
-constexpr int SM_STAGES = 256;  // stage s: [pattern pat_cap][text pre + TILE + post]
+constexpr int SM_STAGES = (SM_EMPTY + 8 * STAGES + 127) & ~127;  // stage s: [pattern pat_cap][text pre + TILE + post]
 
 struct ScanParams {
   const uint8_t* text;  // 16-byte aligned base (text pointer rounded down)
