@@ -518,8 +518,14 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
 // offsets/expand are shared.
 constexpr int SMP_SEGS = 64;     // segments per warp unit (= 8 tiles)
 constexpr int SMP_LIST = 1024;   // per-warp match capacity per unit (bound: 131072/per + 2 < 1024)
-constexpr int SMP_ILP = 4;       // samples per lane per batch
-constexpr int SMP_WARPS = 8;     // warps per sampled_kernel CTA (independent of the scan tiling)
+#ifndef MB_SMP_ILP
+#define MB_SMP_ILP 4
+#endif
+#ifndef MB_SMP_WARPS
+#define MB_SMP_WARPS 16
+#endif
+constexpr int SMP_ILP = MB_SMP_ILP;     // samples per lane per batch
+constexpr int SMP_WARPS = MB_SMP_WARPS; // warps per sampled_kernel CTA (independent of the scan tiling)
 constexpr int SMP_NT = SMP_WARPS * 32;
 __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& pd, const uint32_t* bloom,
                                              const uint16_t* bstart, const uint16_t* bent, const uint8_t* spat,
@@ -547,7 +553,7 @@ __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& 
 }
 
 __global__ void __launch_bounds__(SMP_NT) sampled_kernel(const ScanParams P) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* bloom = reinterpret_cast<uint32_t*>(smem);                 // 2048 words
   uint16_t* bstart = reinterpret_cast<uint16_t*>(smem + 8192);         // <= 1025
   uint16_t* bent = reinterpret_cast<uint16_t*>(smem + 8192 + 2064);    // <= 4096
@@ -674,14 +680,22 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   const int64_t ch = s_chunk;
   const int64_t nseg = P.total_tiles * NWARP;
   const int64_t base = ch * SCAN_CHUNK;
-  constexpr int PER = SCAN_CHUNK / NT;  // 16 counts per thread
+  constexpr int PER = SCAN_CHUNK / NT;  // 32 counts per thread, read as 16-byte vectors
+  static_assert(PER % 8 == 0, "vector loads of 8 uint16 counts");
   uint32_t v[PER];
   int64_t tsum = 0;
+  const uint4* cv = reinterpret_cast<const uint4*>(P.counts + base + (int64_t)tid * PER);
 #pragma unroll
-  for (int q = 0; q < PER; q++) {
-    const int64_t t = base + (int64_t)tid * PER + q;
-    v[q] = t < nseg ? (uint32_t)P.counts[t] : 0u;
-    tsum += v[q];
+  for (int q8 = 0; q8 < PER / 8; q8++) {
+    const uint4 x = cv[q8];  // counts are allocated to a whole number of chunks
+    const uint32_t wds[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int h = 0; h < 8; h++) {
+      const int q = 8 * q8 + h;
+      const int64_t t = base + (int64_t)tid * PER + q;
+      v[q] = t < nseg ? ((wds[h >> 1] >> (16 * (h & 1))) & 0xFFFFu) : 0u;
+      tsum += v[q];
+    }
   }
   int64_t inc = tsum;
 #pragma unroll
@@ -1397,7 +1411,8 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   const int64_t T = P.total_tiles * NWARP;  // segments
   const int64_t nchunks = (T + SCAN_CHUNK - 1) / SCAN_CHUNK;
   int rc;
-  if ((rc = grow(&c->counts, &c->counts_cap, T + 2, "counts"))) return rc;
+  // whole chunks (offsets_kernel reads 16-byte vectors) + 2 slots for the MP overflow flag
+  if ((rc = grow(&c->counts, &c->counts_cap, nchunks * SCAN_CHUNK + 8, "counts"))) return rc;
   if ((rc = grow(&c->lists, &c->lists_cap, T * LIST_CAP, "lists"))) return rc;
   if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * SEG_WORDS, "bitmaps"))) return rc;
   if ((rc = grow(&c->toff, &c->toff_cap, T, "tile offsets"))) return rc;
