@@ -242,3 +242,33 @@ def test_mp_overflow_falls_back(cuda):
     res = mb.search_many(pats, t)
     for p, r in zip(pats, res):
         assert r == oracle.search(p, t).tolist()
+
+
+def test_compiled_searcher_shared_across_threads(cuda):
+    """tests/test_registry.py:152-162 analog: one compiled run(hay) used from 4 threads."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(99)
+    t = rand_bytes(rng, 4, 20000)
+    p = t[1234:1246]
+    expected = oracle.search(p, t).tolist()
+    for algo_id in ("HOR", "EBOM", "SBNDM", "HASH5", "B200"):
+        run = mb.get_algorithm(algo_id).compile(p)
+        with ThreadPoolExecutor(max_workers=4) as pool:
+            results = list(pool.map(run, [t] * 16))
+        assert all(r == expected for r in results), algo_id
+
+
+def test_streams_and_device_tensor_inputs(cuda):
+    rng = np.random.default_rng(7)
+    t = rand_bytes(rng, 256, 3 * TILE)
+    d = torch.from_numpy(np.frombuffer(t, dtype=np.uint8).copy()).cuda()
+    p = t[500:540]
+    plan = engine.Plan(p)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        got = engine.find(plan, d, stream=s)
+    s.synchronize()
+    assert got.cpu().tolist() == oracle.search(p, t).tolist()
+    run = mb.compile_tensor(p)
+    assert run(d).cpu().tolist() == oracle.search(p, t).tolist()
