@@ -1,0 +1,235 @@
+// device_common.cuh -- PTX helpers (TMA bulk copy, mbarrier), SWAR primitives, the K1/K2 filters, verification and break-run helpers, MB_CHECK bounds assertions
+// (part of libmatchb200; included by engine.cu)
+#pragma once
+
+namespace mb {
+
+
+// Bounds assertions for the debug build (make debug -> libmatchb200_dbg.so):
+// every shared-memory window a kernel reads is checked against its stage and
+// every global read against the text; a violation traps.  compute-sanitizer is
+// closed on this GPU pool, so this build stands in for memcheck
+// (tests/test_gpu_bounds.py).  Compiled out of the product library.
+#ifdef MB_BOUNDS_CHECK
+#define MB_CHECK(cond)                                                  \
+  do {                                                                  \
+    if (!(cond)) {                                                      \
+      printf("MB_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__); \
+      __trap();                                                         \
+    }                                                                   \
+  } while (0)
+#else
+#define MB_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// TMA 1D bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// look-back flag word: [epoch:24][status:2][value:38]
+constexpr uint64_t ST_AGG = 1, ST_INCL = 2;
+__device__ __forceinline__ uint64_t pack_state(uint32_t epoch, uint64_t st, uint64_t val) {
+  return ((uint64_t)epoch << 40) | (st << 38) | (val & ((1ULL << 38) - 1));
+}
+
+// ----------------------------------------------------------- SWAR primitives
+// exact per-byte zero flags (0x80 in each zero byte) -> 4-bit mask
+__device__ __forceinline__ uint32_t zero_bytes4(uint32_t x) {
+  uint32_t y = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);
+  return ((y >> 7) * 0x01020408u) >> 24 & 0xFu;
+}
+__device__ __forceinline__ uint32_t shr8(uint32_t lo, uint32_t hi, int k) {
+  return __funnelshift_r(lo, hi, 8 * k);
+}
+
+// -------------------------------------------------------------- filters
+// Each filter looks at the 16 staged bytes of one lane (w[0..3]) plus the
+// next word (w[4]) and returns the candidate mask over the lane's 16 bitmap
+// positions: a cheap existence test first, the exact bit set only on a hit.
+
+// K1 / m <= 3: byte d of x_k is zero iff t[v..v+m) == p (v = 4k + d).
+template <int M>
+struct FiltSWAR {
+  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
+    uint32_t x[4], acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      uint32_t v = w[k] ^ P.G[0];
+      if (M >= 2) v |= shr8(w[k], w[k + 1], 1) ^ P.G[1];
+      if (M >= 3) v |= shr8(w[k], w[k + 1], 2) ^ P.G[2];
+      x[k] = v;
+      acc |= (v - 0x01010101u) & ~v;
+    }
+    if (!(acc & 0x80808080u)) return 0;
+    uint32_t mk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) mk |= zero_bytes4(x[k]) << (4 * k);
+    return mk;
+  }
+};
+
+// K1 / 4 <= m <= 6: 32-bit window at every byte offset vs the anchor word.
+struct FiltWIN4 {
+  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
+    const uint32_t g = P.G[0];
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      hit |= (w[k] == g) | (shr8(w[k], w[k + 1], 1) == g) | (shr8(w[k], w[k + 1], 2) == g) |
+             (shr8(w[k], w[k + 1], 3) == g);
+    }
+    if (!hit) return 0;
+    uint32_t mk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+      for (int d = 0; d < 4; d++)
+        if (shr8(w[k], w[k + 1], d) == g) mk |= 1u << (4 * k + d);
+    return mk;
+  }
+};
+
+// K1/K3 / m >= 7: every occurrence contains one 4-aligned text word inside its
+// 7-byte anchor window [a, a+7); that word equals p[a+j .. a+j+4) for exactly
+// one j in 0..3.  Word k matching G_j marks bitmap position 4k + 3 - j.
+struct FiltALIGNED {
+  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
+    if (!hit) return 0;
+    uint32_t mk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (w[k] == P.G[j]) mk |= 1u << (4 * k + 3 - j);
+    return mk;
+  }
+};
+
+// K2 / 7 <= m <= 64, small alphabets (bitparallel.py:41-63 compile_so): per-lane
+// bit-parallel Shift-Or over a 64-position run of the segment (+ m-1 bytes of
+// look-ahead).  Exact, no verification.  W = 32 or 64 bits of state.
+template <int W>
+struct FiltSO {
+  static constexpr bool kShiftOr = true;
+  static constexpr int kW = W;
+};
+template <class F, class = void>
+struct is_shiftor : std::false_type {};
+template <class F>
+struct is_shiftor<F, std::void_t<decltype(F::kShiftOr)>> : std::true_type {};
+
+template <int W>
+__device__ __forceinline__ void shiftor_lane(const uint8_t* q, int m, const uint64_t* masks, uint32_t& w0,
+                                             uint32_t& w1) {
+  using T = typename std::conditional<W == 32, uint32_t, uint64_t>::type;
+  T D = ~T(0);
+  uint64_t acc = 0;  // shift register of match bits; after 64 + m - 1 bytes holds positions 0..63
+  const int total = 64 + m - 1;
+  const int hb = m - 1;
+  int y = 0;
+  for (; y + 4 <= total; y += 4) {
+    const uint32_t word = *reinterpret_cast<const uint32_t*>(q + y);
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      D = (D << 1) | (T)masks[(word >> (8 * b)) & 0xFFu];
+      acc = (acc >> 1) | ((uint64_t)((~D >> hb) & 1u) << 63);
+    }
+  }
+  for (; y < total; y++) {
+    D = (D << 1) | (T)masks[q[y]];
+    acc = (acc >> 1) | ((uint64_t)((~D >> hb) & 1u) << 63);
+  }
+  w0 = (uint32_t)acc;
+  w1 = (uint32_t)(acc >> 32);
+}
+
+// ------------------------------------------------------------ verification
+// Direct window compare in shared memory (core.py:131-136 match_at).
+__device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* pat, int m) {
+  for (int k = 0; k < m; k++)
+    if (s[k] != pat[k]) return false;
+  return true;
+}
+
+// Per-warp break bitmap of a segment: bit q of word i set iff
+// t[y] != t[y + per] for y = y0 + 32 i + q (y relative to the segment's first
+// start position).  nbw[i] = first break at or after word i (relative to y0).
+__device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {  // unaligned 4-byte smem read
+  const uintptr_t a = (uintptr_t)p;
+  const uint32_t* b = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  return __funnelshift_r(b[0], b[1], 8 * (uint32_t)(a & 3));
+}
+
+__device__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* brk, int32_t* nbw) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < nwords; i += 32) {  // SWAR: 4 byte pairs per compare
+    const uint8_t* q = Yseg + 32 * i;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int b = 0; b < 32; b += 4) bits |= ((~zero_bytes4(lds32u(q + b) ^ lds32u(q + b + per))) & 0xFu) << b;
+    brk[i] = bits;
+  }
+  __syncwarp();
+  const int seg = (nwords + 31) / 32;
+  const int lo = lane * seg, hi = min(nwords, lo + seg);
+  int first = 0x7fffffff;
+  for (int i = hi - 1; i >= lo; i--)
+    if (brk[i]) first = 32 * i + __ffs(brk[i]) - 1;
+  int suf = first;  // inclusive suffix-min over lanes
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int o = __shfl_down_sync(0xffffffffu, suf, d);
+    if (lane + d < 32) suf = min(suf, o);
+  }
+  int cur = __shfl_down_sync(0xffffffffu, suf, 1);
+  if (lane == 31) cur = 0x7fffffff;
+  for (int i = hi - 1; i >= lo; i--) {
+    if (brk[i]) cur = 32 * i + __ffs(brk[i]) - 1;
+    nbw[i] = cur;
+  }
+  if (lane == 0) nbw[nwords] = 0x7fffffff;
+  __syncwarp();
+}
+
+
+}  // namespace mb

@@ -18,982 +18,15 @@
 #include "plan.h"
 #include "scan.h"
 
-namespace mb {
+#include "device_common.cuh"
+#include "kernel_scan.cuh"
+#include "kernel_sampled.cuh"
+#include "kernel_output.cuh"
+#include "kernel_mp.cuh"
 
-// Bounds assertions for the debug build (make debug -> libmatchb200_dbg.so):
-// every shared-memory window a kernel reads is checked against its stage and
-// every global read against the text; a violation traps.  compute-sanitizer is
-// closed on this GPU pool, so this build stands in for memcheck
-// (tests/test_gpu_bounds.py).  Compiled out of the product library.
-#ifdef MB_BOUNDS_CHECK
-#define MB_CHECK(cond)                                                  \
-  do {                                                                  \
-    if (!(cond)) {                                                      \
-      printf("MB_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__); \
-      __trap();                                                         \
-    }                                                                   \
-  } while (0)
-#else
-#define MB_CHECK(cond) \
-  do {                 \
-  } while (0)
-#endif
-
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-// TMA 1D bulk copy global -> shared, completion counted on the mbarrier.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(
-          smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// look-back flag word: [epoch:24][status:2][value:38]
-constexpr uint64_t ST_AGG = 1, ST_INCL = 2;
-__device__ __forceinline__ uint64_t pack_state(uint32_t epoch, uint64_t st, uint64_t val) {
-  return ((uint64_t)epoch << 40) | (st << 38) | (val & ((1ULL << 38) - 1));
-}
-
-// ----------------------------------------------------------- SWAR primitives
-// exact per-byte zero flags (0x80 in each zero byte) -> 4-bit mask
-__device__ __forceinline__ uint32_t zero_bytes4(uint32_t x) {
-  uint32_t y = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);
-  return ((y >> 7) * 0x01020408u) >> 24 & 0xFu;
-}
-__device__ __forceinline__ uint32_t shr8(uint32_t lo, uint32_t hi, int k) {
-  return __funnelshift_r(lo, hi, 8 * k);
-}
-
-// -------------------------------------------------------------- filters
-// Each filter looks at the 16 staged bytes of one lane (w[0..3]) plus the
-// next word (w[4]) and returns the candidate mask over the lane's 16 bitmap
-// positions: a cheap existence test first, the exact bit set only on a hit.
-
-// K1 / m <= 3: byte d of x_k is zero iff t[v..v+m) == p (v = 4k + d).
-template <int M>
-struct FiltSWAR {
-  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
-    uint32_t x[4], acc = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      uint32_t v = w[k] ^ P.G[0];
-      if (M >= 2) v |= shr8(w[k], w[k + 1], 1) ^ P.G[1];
-      if (M >= 3) v |= shr8(w[k], w[k + 1], 2) ^ P.G[2];
-      x[k] = v;
-      acc |= (v - 0x01010101u) & ~v;
-    }
-    if (!(acc & 0x80808080u)) return 0;
-    uint32_t mk = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) mk |= zero_bytes4(x[k]) << (4 * k);
-    return mk;
-  }
-};
-
-// K1 / 4 <= m <= 6: 32-bit window at every byte offset vs the anchor word.
-struct FiltWIN4 {
-  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
-    const uint32_t g = P.G[0];
-    bool hit = false;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      hit |= (w[k] == g) | (shr8(w[k], w[k + 1], 1) == g) | (shr8(w[k], w[k + 1], 2) == g) |
-             (shr8(w[k], w[k + 1], 3) == g);
-    }
-    if (!hit) return 0;
-    uint32_t mk = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++)
-#pragma unroll
-      for (int d = 0; d < 4; d++)
-        if (shr8(w[k], w[k + 1], d) == g) mk |= 1u << (4 * k + d);
-    return mk;
-  }
-};
-
-// K1/K3 / m >= 7: every occurrence contains one 4-aligned text word inside its
-// 7-byte anchor window [a, a+7); that word equals p[a+j .. a+j+4) for exactly
-// one j in 0..3.  Word k matching G_j marks bitmap position 4k + 3 - j.
-struct FiltALIGNED {
-  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
-    bool hit = false;
-#pragma unroll
-    for (int k = 0; k < 4; k++)
-      hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
-    if (!hit) return 0;
-    uint32_t mk = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++)
-#pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (w[k] == P.G[j]) mk |= 1u << (4 * k + 3 - j);
-    return mk;
-  }
-};
-
-// K2 / 7 <= m <= 64, small alphabets (bitparallel.py:41-63 compile_so): per-lane
-// bit-parallel Shift-Or over a 64-position run of the segment (+ m-1 bytes of
-// look-ahead).  Exact, no verification.  W = 32 or 64 bits of state.
-template <int W>
-struct FiltSO {
-  static constexpr bool kShiftOr = true;
-  static constexpr int kW = W;
-};
-template <class F, class = void>
-struct is_shiftor : std::false_type {};
-template <class F>
-struct is_shiftor<F, std::void_t<decltype(F::kShiftOr)>> : std::true_type {};
-
-template <int W>
-__device__ __forceinline__ void shiftor_lane(const uint8_t* q, int m, const uint64_t* masks, uint32_t& w0,
-                                             uint32_t& w1) {
-  using T = typename std::conditional<W == 32, uint32_t, uint64_t>::type;
-  T D = ~T(0);
-  uint64_t acc = 0;  // shift register of match bits; after 64 + m - 1 bytes holds positions 0..63
-  const int total = 64 + m - 1;
-  const int hb = m - 1;
-  int y = 0;
-  for (; y + 4 <= total; y += 4) {
-    const uint32_t word = *reinterpret_cast<const uint32_t*>(q + y);
-#pragma unroll
-    for (int b = 0; b < 4; b++) {
-      D = (D << 1) | (T)masks[(word >> (8 * b)) & 0xFFu];
-      acc = (acc >> 1) | ((uint64_t)((~D >> hb) & 1u) << 63);
-    }
-  }
-  for (; y < total; y++) {
-    D = (D << 1) | (T)masks[q[y]];
-    acc = (acc >> 1) | ((uint64_t)((~D >> hb) & 1u) << 63);
-  }
-  w0 = (uint32_t)acc;
-  w1 = (uint32_t)(acc >> 32);
-}
-
-// ------------------------------------------------------------ verification
-// Direct window compare in shared memory (core.py:131-136 match_at).
-__device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* pat, int m) {
-  for (int k = 0; k < m; k++)
-    if (s[k] != pat[k]) return false;
-  return true;
-}
-
-// Per-warp break bitmap of a segment: bit q of word i set iff
-// t[y] != t[y + per] for y = y0 + 32 i + q (y relative to the segment's first
-// start position).  nbw[i] = first break at or after word i (relative to y0).
-__device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {  // unaligned 4-byte smem read
-  const uintptr_t a = (uintptr_t)p;
-  const uint32_t* b = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
-  return __funnelshift_r(b[0], b[1], 8 * (uint32_t)(a & 3));
-}
-
-__device__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* brk, int32_t* nbw) {
-  const int lane = threadIdx.x & 31;
-  for (int i = lane; i < nwords; i += 32) {  // SWAR: 4 byte pairs per compare
-    const uint8_t* q = Yseg + 32 * i;
-    uint32_t bits = 0;
-#pragma unroll
-    for (int b = 0; b < 32; b += 4) bits |= ((~zero_bytes4(lds32u(q + b) ^ lds32u(q + b + per))) & 0xFu) << b;
-    brk[i] = bits;
-  }
-  __syncwarp();
-  const int seg = (nwords + 31) / 32;
-  const int lo = lane * seg, hi = min(nwords, lo + seg);
-  int first = 0x7fffffff;
-  for (int i = hi - 1; i >= lo; i--)
-    if (brk[i]) first = 32 * i + __ffs(brk[i]) - 1;
-  int suf = first;  // inclusive suffix-min over lanes
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    int o = __shfl_down_sync(0xffffffffu, suf, d);
-    if (lane + d < 32) suf = min(suf, o);
-  }
-  int cur = __shfl_down_sync(0xffffffffu, suf, 1);
-  if (lane == 31) cur = 0x7fffffff;
-  for (int i = hi - 1; i >= lo; i--) {
-    if (brk[i]) cur = 32 * i + __ffs(brk[i]) - 1;
-    nbw[i] = cur;
-  }
-  if (lane == 0) nbw[nwords] = 0x7fffffff;
-  __syncwarp();
-}
-
-// ---------------------------------------------------------------- kernel 1: scan
-// Warp-specialised: warp NWARP is the TMA producer (ticket -> bulk copies of
-// the tile+halo and of the pattern into a free stage), warps 0..NWARP-1 are
-// consumers that each own one SEG-position segment of every tile.  Stages are
-// handed over through full/empty mbarriers; there is no block-wide barrier in
-// the loop, so warps drift independently within the ring.
-template <class Filt>
-__global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
-  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
-  uint8_t* stages = smem + SM_STAGES;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (P.run_if && *P.run_if == 0u) return;  // conditional fallback launch (MP did not overflow)
-  uint32_t* bm = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes) + warp * SEG_WORDS;
-  uint32_t* brk = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4) +
-                  warp * 2 * (P.brk_words + 4);
-  int32_t* nbw = reinterpret_cast<int32_t*>(brk + P.brk_words + 4);
-  uint64_t* so_s = reinterpret_cast<uint64_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
-                                               NWARP * 2 * (P.brk_words + 4) * 4) +
-                   warp * 256;  // K2 only: per-warp shift-or masks
-
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWARP);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == NWARP) {  // ---------------- producer
-    if (lane == 0) {
-      for (int it = 0;; it++) {
-        const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
-        const unsigned long long tk = atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
-        if ((int64_t)tk >= P.group_tiles) {
-          hdr[s].tk = -1;
-          mbar_arrive(&full[s]);
-          break;
-        }
-        const int kg = (int)((int64_t)tk / P.ntiles);
-        const int k = P.plist ? P.plist[kg] : kg;  // this launch's family group -> batch index
-        const int64_t tau = (int64_t)tk - (int64_t)kg * P.ntiles;
-        hdr[s].tk = (int64_t)k * P.ntiles + tau;   // global tile id (segment index base)
-        hdr[s].k = k;
-        hdr[s].tau = tau;
-        const int64_t start = tau * TILE - P.pre;
-        const int64_t end = tau * TILE + TILE + P.post;
-        const int64_t cs = start < 0 ? 0 : start;
-        const int64_t ce = end > P.nv16 ? P.nv16 : end;
-        const uint32_t tb = ce > cs ? (uint32_t)(ce - cs) : 0u;
-        const PatDev* pd = P.pats + k;
-        const uint32_t pb = (uint32_t)((pd->m + 15) & ~15LL);
-        uint8_t* st = stages + s * P.stage_bytes;
-        mbar_expect_tx(&full[s], tb + pb);
-        bulk_g2s(st, pd->bytes, pb, &full[s]);
-        if (tb) bulk_g2s(st + P.pat_cap + (cs - start), P.text + cs, tb, &full[s]);
-      }
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------ consumers
-  const int c0 = warp * SEG;  // this warp's segment of every tile
-  int cur_k = -1;
-  PatDev pd;
-  int64_t blo = 0, bhi = -1;
-  for (int it = 0;; it++) {
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
-    const int64_t tk = hdr[s].tk;
-    if (tk < 0) break;
-    const int k = hdr[s].k;
-    if (k != cur_k) {  // per-pattern parameters stay in registers across tiles
-      pd = P.pats[k];
-      blo = P.off + pd.delta;               // valid bits: s = b - delta - off in [0, n-m]
-      bhi = P.off + pd.delta + P.n - pd.m;  // inclusive (may be < blo)
-      cur_k = k;
-      if constexpr (is_shiftor<Filt>::value) {  // this warp's copy of the 256 shift-or masks
-        for (int i = lane; i < 256; i += 32) so_s[i] = pd.so_masks[i];
-        __syncwarp();
-      }
-    }
-    const int64_t B0 = hdr[s].tau * TILE;
-    const uint8_t* spat = stages + s * P.stage_bytes;
-    const uint8_t* S = spat + P.pat_cap + P.pre;  // S[c] = virtual text byte B0 + c
-    const uint8_t* const sbeg = spat + P.pat_cap;  // staged text window [sbeg, send)
-    const uint8_t* const send = spat + P.stage_bytes;
-    (void)sbeg, (void)send;
-    MB_CHECK(S + c0 + SEG + 4 <= send);
-    const int64_t segb = B0 + c0;
-    const bool interior = segb >= blo && segb + SEG - 1 <= bhi;
-
-    // this lane's 64 positions of the segment: linear bitmap words 2*lane, 2*lane+1
-    uint32_t w0 = 0, w1 = 0;
-    bool have;
-    if constexpr (is_shiftor<Filt>::value) {
-      // ---- K2: exact per-lane shift-or over positions [c0 + 64 lane, +64)
-      MB_CHECK(S + c0 + 64 * lane + 64 + pd.m + 3 <= send);
-      shiftor_lane<Filt::kW>(S + c0 + 64 * lane, (int)pd.m, so_s, w0, w1);
-      if (!interior) {
-        const int64_t b = segb + 64 * lane;
-        uint64_t vm = 0;
-        for (int i = 0; i < 64; i++)
-          if (b + i >= blo && b + i <= bhi) vm |= 1ULL << i;
-        w0 &= (uint32_t)vm;
-        w1 &= (uint32_t)(vm >> 32);
-      }
-      have = __any_sync(0xffffffffu, (w0 | w1) != 0);
-    } else {
-      // ---- filter (fast path): 4 rounds of 512 positions, 16 per lane, masks kept in registers
-      uint32_t mk[SEG / 512];
-      bool anyc = false;
-#pragma unroll
-      for (int r = 0; r < SEG / 512; r++) {
-        const int c = c0 + r * 512 + lane * 16;
-        const uint4 X = *reinterpret_cast<const uint4*>(S + c);
-        const uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
-        mk[r] = Filt::run(w, pd);
-        anyc |= (mk[r] != 0);
-      }
-      have = __any_sync(0xffffffffu, anyc);
-      if (have) {
-        // ---- slow path: validity mask at text edges, linear segment bitmap
-#pragma unroll
-        for (int r = 0; r < SEG / 512; r++) {
-          uint32_t m = mk[r];
-          if (!interior) {
-            const int64_t b = segb + r * 512 + lane * 16;
-            uint32_t vm = 0;
-            for (int i = 0; i < 16; i++)
-              if (b + i >= blo && b + i <= bhi) vm |= 1u << i;
-            m &= vm;
-          }
-          const uint32_t other = __shfl_down_sync(0xffffffffu, m, 1);
-          if (!(lane & 1)) bm[r * 16 + (lane >> 1)] = m | (other << 16);
-        }
-        __syncwarp();
-        w0 = bm[2 * lane];
-        w1 = bm[2 * lane + 1];
-      }
-    }
-    uint32_t cnt = 0;
-    if (have) {
-      // ---- verify (exact filters skip this)
-      if (!pd.exact && __any_sync(0xffffffffu, (w0 | w1) != 0)) {
-        const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
-        if (pd.periodic) {
-          // s matches <=> t[s..s+per) = p[0..per) and no break t[y] != t[y+per] for
-          // y in [s, s+L).  A break y kills starts [y-L+1, y]: walk the few breaks
-          // that reach this lane's 64 starts, mask them out in bulk.
-          const int nwords = (SEG + pd.L + 31) / 32;
-          MB_CHECK(Y0 + c0 >= sbeg && Y0 + c0 + 32 * nwords + pd.per + 8 <= send);
-          warp_breaks(Y0 + c0, pd.per, nwords, brk, nbw);
-          uint64_t cand = ((uint64_t)w1 << 32) | w0;
-          if (cand) {
-            auto nb = [&](int y) -> int {
-              if (y >= 32 * nwords) return 0x7fffffff;
-              const uint32_t x = brk[y >> 5] >> (y & 31);
-              return x ? y + __ffs(x) - 1 : nbw[(y >> 5) + 1];
-            };
-            const int q0 = 64 * lane, q1 = q0 + 63;
-            uint64_t killed = 0;
-            for (int y = nb(q0); y != 0x7fffffff && y - pd.L + 1 <= q1; y = nb(y + 1)) {
-              const int lo = max(q0, y - pd.L + 1) - q0, hi = min(q1, y) - q0;
-              if (lo <= hi) killed |= (hi - lo == 63) ? ~0ULL : (((1ULL << (hi - lo + 1)) - 1) << lo);
-              if (y >= q1) break;
-            }
-            cand &= ~killed;
-            if (pd.per > 4) {  // the 4 anchor bytes do not cover a full period: check one block
-              uint64_t cc = cand;
-              while (cc) {
-                const int i = __ffsll((long long)cc) - 1;
-                cc &= cc - 1;
-                MB_CHECK(Y0 + c0 + q0 + i >= sbeg && Y0 + c0 + q0 + i + pd.per <= send);
-                if (!verify_direct(Y0 + c0 + q0 + i, spat, pd.per)) cand &= ~(1ULL << i);
-              }
-            }
-          }
-          w0 = (uint32_t)cand;
-          w1 = (uint32_t)(cand >> 32);
-        } else if (pd.m >= 64) {
-          // long windows: the whole warp verifies one candidate at a time,
-          // lane l comparing 4-byte words l, l+32, ... (smem text vs pattern)
-          const uint64_t mine = ((uint64_t)w1 << 32) | w0;
-          uint64_t keep = 0;
-          uint32_t active = __ballot_sync(0xffffffffu, mine != 0);
-          while (active) {
-            const int src = __ffs(active) - 1;
-            active &= active - 1;
-            uint64_t cm = ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(mine >> 32), src) << 32) |
-                          __shfl_sync(0xffffffffu, (uint32_t)mine, src);
-            while (cm) {
-              const int i = __ffsll((long long)cm) - 1;
-              cm &= cm - 1;
-              const uint8_t* tw = Y0 + c0 + 64 * src + i;
-              MB_CHECK(tw >= sbeg && tw + pd.m + 8 <= send);
-              bool bad = false;
-              for (int k = 4 * lane; k < pd.m; k += 128) {
-                const uint32_t pw = *reinterpret_cast<const uint32_t*>(spat + k);
-                uint32_t diff = lds32u(tw + k) ^ pw;
-                if (pd.m - k < 4) diff &= (1u << (8 * (pd.m - k))) - 1u;
-                bad |= diff != 0;
-              }
-              if (!__any_sync(0xffffffffu, bad) && lane == src) keep |= 1ULL << i;
-            }
-          }
-          w0 = (uint32_t)keep;
-          w1 = (uint32_t)(keep >> 32);
-        } else {
-          uint32_t ws[2] = {w0, w1};
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            uint32_t cw = ws[h], mw = 0;
-            while (cw) {
-              const int i = __ffs(cw) - 1;
-              cw &= cw - 1;
-              MB_CHECK(Y0 + c0 + 32 * (2 * lane + h) + i >= sbeg && Y0 + c0 + 32 * (2 * lane + h) + i + pd.m <= send);
-              if (verify_direct(Y0 + c0 + 32 * (2 * lane + h) + i, spat, (int)pd.m)) mw |= 1u << i;
-            }
-            ws[h] = mw;
-          }
-          w0 = ws[0];
-          w1 = ws[1];
-        }
-      }
-      // ---- count + compact store (segment g = tile * NWARP + warp)
-      const uint32_t c2 = __popc(w0) + __popc(w1);
-      uint32_t inc = c2;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-      }
-      cnt = __shfl_sync(0xffffffffu, inc, 31);
-      const int64_t g = tk * NWARP + warp;
-      if (cnt <= LIST_CAP) {
-        uint32_t j = inc - c2;
-        uint16_t* L = P.lists + g * LIST_CAP;
-        uint64_t bits = ((uint64_t)w1 << 32) | w0;
-        while (bits) {
-          const int i = __ffsll((long long)bits) - 1;
-          bits &= bits - 1;
-          L[j++] = (uint16_t)(c0 + 64 * lane + i);
-        }
-      } else {
-        reinterpret_cast<uint2*>(P.bitmaps + g * SEG_WORDS)[lane] = make_uint2(w0, w1);
-      }
-      __syncwarp();
-    }
-    if (lane == 0) {
-      P.counts[tk * NWARP + warp] = (uint16_t)cnt;
-      mbar_arrive(&empty[s]);
-    }
-  }
-}
-
-// ------------------------------------------------ kernel 1b: sampled q-gram scan (K3)
-// For long, non-periodic patterns: only the q-gram at every
-// S-th text position is read (one 128-byte DRAM line per sample instead of S
-// bytes); a bloom filter + bucketed offset lists in smem map a gram to the
-// pattern offsets j where it occurs, each giving a candidate start s = x - j
-// that is verified against the text in global memory.  A warp owns SMP_SEGS
-// consecutive segments (8 tiles) and reads every sample whose bit range
-// [S*i, S*i + S) meets them, 4 independent 16-byte loads per lane in flight.
-// Output (segment counts, uint16 tile-relative lists) is the scan kernel's, so
-// offsets/expand are shared.
-constexpr int SMP_SEGS = 64;     // segments per warp unit (= 8 tiles)
-constexpr int SMP_LIST = 1024;   // per-warp match capacity per unit (bound: 131072/per + 2 < 1024)
-#ifndef MB_SMP_ILP
-#define MB_SMP_ILP 4
-#endif
-#ifndef MB_SMP_WARPS
-#define MB_SMP_WARPS 16
-#endif
-constexpr int SMP_ILP = MB_SMP_ILP;     // samples per lane per batch
-constexpr int SMP_WARPS = MB_SMP_WARPS; // warps per sampled_kernel CTA (independent of the scan tiling)
-constexpr int SMP_NT = SMP_WARPS * 32;
-__device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& pd, const uint32_t* bloom,
-                                             const uint16_t* bstart, const uint16_t* bent, const uint8_t* spat,
-                                             const uint32_t* w, int64_t x, int64_t ulo, int64_t uhi, int64_t blo,
-                                             int64_t bhi, uint32_t* found) {
-  const uint32_t h = gram_mix(w, pd.q >> 2);
-  if (!((bloom[h >> 21] >> ((h >> 16) & 31)) & 1u)) return 0;
-  int nf = 0;
-  const uint32_t bk = h >> (32 - pd.B);
-  for (int e = bstart[bk]; e < bstart[bk + 1] && nf < 4; e++) {
-    const int j = bent[e];
-    bool eq = true;
-    for (int c = 0; c < pd.q && eq; c++) eq = spat[j + c] == (uint8_t)(w[c >> 2] >> (8 * (c & 3)));
-    if (!eq) continue;
-    const int64_t sv = x - j;           // virtual start
-    const int64_t bit = sv + pd.delta;  // = x - j + S - 1, inside [x, x + S)
-    if (bit < ulo || bit >= uhi || bit < blo || bit > bhi) continue;
-    const uint8_t* tp = P.text + sv;
-    MB_CHECK(sv >= P.off && sv + pd.m <= P.off + P.n);
-    bool ok = true;
-    for (int c = 0; c < pd.m && ok; c++) ok = __ldg(tp + c) == spat[c];
-    if (ok) found[nf++] = (uint32_t)(bit - ulo);
-  }
-  return nf;
-}
-
-__global__ void __launch_bounds__(SMP_NT) sampled_kernel(const ScanParams P) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* bloom = reinterpret_cast<uint32_t*>(smem);                 // 2048 words
-  uint16_t* bstart = reinterpret_cast<uint16_t*>(smem + 8192);         // <= 1025
-  uint16_t* bent = reinterpret_cast<uint16_t*>(smem + 8192 + 2064);    // <= 4096
-  uint32_t* lists = reinterpret_cast<uint32_t*>(smem + 8192 + 2064 + 8192);  // [SMP_WARPS][SMP_LIST]
-  int64_t* s_ticket = reinterpret_cast<int64_t*>(lists + SMP_WARPS * SMP_LIST);
-  uint8_t* spat = reinterpret_cast<uint8_t*>(s_ticket + 2);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t segs = P.ntiles * NWARP;                                   // segments per pattern
-  const int64_t wunits = (segs + SMP_SEGS - 1) / SMP_SEGS;                 // warp units per pattern
-  const int64_t units = (wunits + SMP_WARPS - 1) / SMP_WARPS;              // CTA units per pattern
-  const int64_t total = units * P.group_k;
-  int cur_k = -1;
-  PatDev pd;
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_ticket[0] = (int64_t)atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
-    __syncthreads();
-    const int64_t t = s_ticket[0];
-    if (t >= total) break;
-    const int kg = (int)(t / units);
-    const int k = P.plist ? P.plist[kg] : kg;  // family group -> batch index
-    const int64_t u = t - (int64_t)kg * units;
-    if (k != cur_k) {  // load this pattern's tables (uniform across the CTA)
-      pd = P.pats[k];
-      const int nb = (1 << pd.B) + 1;
-      for (int i = tid; i < 2048; i += SMP_NT) bloom[i] = pd.bloom[i];
-      for (int i = tid; i < nb; i += SMP_NT) bstart[i] = pd.bstart[i];
-      for (int i = tid; i < pd.S; i += SMP_NT) bent[i] = pd.bent[i];
-      for (int i = tid; i < pd.m; i += SMP_NT) spat[i] = pd.bytes[i];
-      cur_k = k;
-      __syncthreads();
-    }
-    const int64_t wu = u * SMP_WARPS + warp;
-    if (wu >= wunits) continue;
-    const int64_t seg0 = wu * SMP_SEGS;
-    const int nsegs = (int)(segs - seg0 < SMP_SEGS ? segs - seg0 : SMP_SEGS);
-    const int64_t ulo = seg0 * SEG, uhi = ulo + (int64_t)nsegs * SEG;  // bits of this unit
-    const int64_t blo = P.off + pd.delta, bhi = P.off + pd.delta + P.n - pd.m;
-    const int64_t S = pd.S;
-    const int q = pd.q;
-    const int64_t tlimit = P.off + P.n;  // virtual end of the text
-    const int64_t i0 = ulo / S, i1 = (uhi - 1) / S;
-    uint32_t* wl = lists + warp * SMP_LIST;
-    uint32_t nmatch = 0;
-    for (int64_t ib = i0; ib <= i1; ib += 32 * SMP_ILP) {
-      uint4 g[SMP_ILP], g2[SMP_ILP];
-#pragma unroll
-      for (int r = 0; r < SMP_ILP; r++) {  // issue every load of the batch first
-        const int64_t i = ib + r * 32 + lane;
-        const int64_t x = S * i;
-        if (i <= i1 && x + q <= tlimit) {
-          MB_CHECK(x >= 0 && x + 16 * (q == 32 ? 2 : 1) <= P.nv16 && (x & 15) == 0);
-          g[r] = __ldcs(reinterpret_cast<const uint4*>(P.text + x));
-          if (q == 32) g2[r] = __ldcs(reinterpret_cast<const uint4*>(P.text + x + 16));
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < SMP_ILP; r++) {
-        const int64_t i = ib + r * 32 + lane;
-        const int64_t x = S * i;
-        uint32_t found[4];
-        int nf = 0;
-        if (i <= i1 && x + q <= tlimit) {
-          const uint32_t w[8] = {g[r].x, g[r].y, g[r].z, g[r].w, g2[r].x, g2[r].y, g2[r].z, g2[r].w};
-          nf = sampled_probe(P, pd, bloom, bstart, bent, spat, w, x, ulo, uhi, blo, bhi, found);
-        }
-        // ascending: lanes own disjoint increasing bit ranges; bucket entries are in ascending start order
-        const uint32_t any = __ballot_sync(0xffffffffu, nf != 0);
-        if (any) {
-          uint32_t inc = nf;
-#pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += o;
-          }
-          const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-          const uint32_t pos = nmatch + inc - nf;
-          for (int f = 0; f < nf; f++)
-            if (pos + f < SMP_LIST) wl[pos + f] = found[f];
-          nmatch += tot;
-        }
-      }
-    }
-    if (nmatch > SMP_LIST) __trap();  // impossible for the plans that choose K3 (see plan.cpp)
-    __syncwarp();
-    // per-segment counts and uint16 tile-relative lists, as scan_kernel writes them
-    for (int sl = lane; sl < nsegs; sl += 32) {
-      const uint32_t lo = sl * SEG, hi = lo + SEG;
-      uint32_t c = 0, first = 0;
-      for (uint32_t e = 0; e < nmatch; e++) {
-        const uint32_t v = wl[e];
-        if (v < lo) first = e + 1;
-        else if (v < hi) c++;
-      }
-      const int64_t g = (int64_t)k * segs + seg0 + sl;
-      P.counts[g] = (uint16_t)c;
-      const uint32_t tile_rel = (uint32_t)(((seg0 + sl) % NWARP) * SEG);  // segment start within its tile
-      if (c <= LIST_CAP) {
-        for (uint32_t e = 0; e < c; e++) P.lists[g * LIST_CAP + e] = (uint16_t)(wl[first + e] - lo + tile_rel);
-      } else {
-        uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
-        for (int q2 = 0; q2 < SEG_WORDS; q2++) bmw[q2] = 0;
-        for (uint32_t e = 0; e < c; e++) {
-          const uint32_t r = wl[first + e] - lo;
-          bmw[r >> 5] |= 1u << (r & 31);
-        }
-      }
-    }
-  }
-}
-
-// ------------------------------------------------ kernel 2: segment offsets (scan)
-// Exclusive scan of per-segment counts in SCAN_CHUNK pieces; chunk order =
-// ticket order taken at CTA start (no prefetch), so each chunk only waits on
-// chunks already running -- the decoupled look-back never stalls on a queued
-// predecessor.
-__global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
-  __shared__ int64_t wsum[NWARP];
-  __shared__ int64_t s_excl;
-  __shared__ int64_t s_chunk;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_chunk = (int64_t)atomicAdd(&P.ticket[TICKET_OFFSETS], 1ULL);
-  __syncthreads();
-  const int64_t ch = s_chunk;
-  const int64_t nseg = P.total_tiles * NWARP;
-  const int64_t base = ch * SCAN_CHUNK;
-  constexpr int PER = SCAN_CHUNK / NT;  // 32 counts per thread, read as 16-byte vectors
-  static_assert(PER % 8 == 0, "vector loads of 8 uint16 counts");
-  uint32_t v[PER];
-  int64_t tsum = 0;
-  const uint4* cv = reinterpret_cast<const uint4*>(P.counts + base + (int64_t)tid * PER);
-#pragma unroll
-  for (int q8 = 0; q8 < PER / 8; q8++) {
-    const uint4 x = cv[q8];  // counts are allocated to a whole number of chunks
-    const uint32_t wds[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-    for (int h = 0; h < 8; h++) {
-      const int q = 8 * q8 + h;
-      const int64_t t = base + (int64_t)tid * PER + q;
-      v[q] = t < nseg ? ((wds[h >> 1] >> (16 * (h & 1))) & 0xFFFFu) : 0u;
-      tsum += v[q];
-    }
-  }
-  int64_t inc = tsum;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int64_t o = __shfl_up_sync(0xffffffffu, inc, d);
-    if (lane >= d) inc += o;
-  }
-  if (lane == 31) wsum[warp] = inc;
-  __syncthreads();
-  int64_t chunk_total = 0, wbefore = 0;
-  for (int q = 0; q < NWARP; q++) {
-    chunk_total += wsum[q];
-    wbefore += q < warp ? wsum[q] : 0;
-  }
-  if (warp == 0) {
-    int64_t excl = 0;
-    if (ch == 0) {
-      if (lane == 0) st_relaxed(&P.state[0], pack_state(P.epoch, ST_INCL, (uint64_t)chunk_total));
-    } else {
-      if (lane == 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_AGG, (uint64_t)chunk_total));
-      int64_t j = ch - 1;
-      while (true) {
-        const int64_t idx = j - lane;
-        uint64_t sv;
-        if (idx < 0) {
-          sv = pack_state(P.epoch, ST_INCL, 0);
-        } else {
-          while (true) {
-            sv = ld_relaxed(&P.state[idx]);
-            if ((uint32_t)(sv >> 40) == P.epoch && ((sv >> 38) & 3)) break;
-            __nanosleep(20);
-          }
-        }
-        const uint64_t st = (sv >> 38) & 3;
-        const int64_t val = (int64_t)(sv & ((1ULL << 38) - 1));
-        const uint32_t incl = __ballot_sync(0xffffffffu, st == ST_INCL);
-        int64_t contrib = val;
-        if (incl) contrib = lane <= __ffs(incl) - 1 ? val : 0;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
-        excl += contrib;
-        if (incl) break;
-        j -= 32;
-      }
-      if (lane == 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_INCL, (uint64_t)(excl + chunk_total)));
-    }
-    if (lane == 0) s_excl = excl + (P.out_base ? *P.out_base : 0);
-  }
-  __syncthreads();
-  int64_t run = s_excl + wbefore + inc - tsum;
-  const int64_t seg_per_pat = P.ntiles * NWARP;
-  // Sorted sparse segments (<= LIST_CAP uint16 offsets) are expanded right here,
-  // their offsets never leave registers; dense or unsorted (MP) segments are
-  // queued for expand_kernel with their offset.
-  const bool fuse = P.out && !P.unsorted_lists;
-  int cur_k = -1;
-  int64_t shift = 0;
-#pragma unroll
-  for (int q = 0; q < PER; q++) {
-    const int64_t t = base + (int64_t)tid * PER + q;
-    if (t < nseg) {
-      if (v[q] && P.out) {
-        if (fuse && v[q] <= (uint32_t)LIST_CAP) {
-          const int64_t tile = t / NWARP;
-          const int k = (int)(tile / P.ntiles);
-          if (k != cur_k) {
-            shift = P.pats[k].delta + P.off;
-            cur_k = k;
-          }
-          const int64_t pos0 = (tile % P.ntiles) * TILE - shift;
-          const uint16_t* L = P.lists + t * LIST_CAP;
-          for (uint32_t e = 0; e < v[q]; e++)
-            if (run + e < P.cap) P.out[run + e] = pos0 + L[e];
-        } else {
-          P.toff[t] = run;
-          const unsigned long long slot = atomicAdd(&P.ticket[TICKET_DENSE], 1ULL);
-          P.seglist[slot] = t;
-        }
-      }
-      if (t % seg_per_pat == seg_per_pat - 1) P.offsets_plus1[t / seg_per_pat] = run + v[q];
-    }
-    run += v[q];
-  }
-}
-
-// ------------------------------------------------ kernel 3: expansion
-// The segments offsets_kernel queued (dense, or MP's unsorted lists), a warp
-// per segment: unsorted lists get a 32-lane bitonic sort, dense segments
-// expand their 64-word bitmap 32 words at a time through a per-warp smem
-// staging buffer so every global store is a coalesced run.
-constexpr int EXP_WARPS = 4;
-__global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nq = (int64_t)P.ticket[TICKET_DENSE];
-  int cur_k = -1;
-  int64_t shift = 0;
-  for (int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp; qi < nq; qi += (int64_t)gridDim.x * EXP_WARPS) {
-    {
-      const int64_t g = P.seglist[qi];
-      const uint32_t c = P.counts[g];
-      const int64_t tile = g / NWARP;
-      const int k = (int)(tile / P.ntiles);
-      if (k != cur_k) {
-        shift = P.pats[k].delta + P.off;
-        cur_k = k;
-      }
-      const int64_t pos0 = (tile % P.ntiles) * TILE - shift;  // tile-relative offsets below
-      const int64_t o = P.toff[g];
-      if (o >= P.cap) continue;
-      if (c <= LIST_CAP) {
-        uint32_t v = lane < (int)c ? (uint32_t)P.lists[g * LIST_CAP + lane] : 0xFFFFFFFFu;
-        if (P.unsorted_lists) {  // MP fills list slots atomically: warp bitonic sort of <= 32 offsets
-#pragma unroll
-          for (int kk = 2; kk <= 32; kk <<= 1)
-#pragma unroll
-            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-              const uint32_t o2 = __shfl_xor_sync(0xffffffffu, v, jj);
-              const bool up = ((lane & kk) == 0);
-              const bool lower = ((lane & jj) == 0);
-              v = (lower == up) ? min(v, o2) : max(v, o2);
-            }
-        }
-        if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + v;
-        continue;
-      }
-      // dense: the 64 bitmap words (2 per lane), exclusive popcount prefix, then
-      // one word per step broadcast to the warp -- lane i writes bit i's
-      // position at its rank, so a full word is one coalesced 256-byte store
-      const uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
-      const int64_t segpos = pos0 + (g % NWARP) * SEG;
-      const uint32_t xa = bmw[lane], xb = bmw[32 + lane];
-      const uint32_t pa = __popc(xa), pb = __popc(xb);
-      uint32_t ia = pa, ib = pb;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t va = __shfl_up_sync(0xffffffffu, ia, d);
-        const uint32_t vb = __shfl_up_sync(0xffffffffu, ib, d);
-        if (lane >= d) ia += va, ib += vb;
-      }
-      const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31);
-      const uint32_t ea = ia - pa, eb = ta + ib - pb;
-      const uint32_t below = (1u << lane) - 1u;
-#pragma unroll 4
-      for (int w = 0; w < 32; w++) {
-        const uint32_t x = __shfl_sync(0xffffffffu, xa, w);
-        const uint32_t e = __shfl_sync(0xffffffffu, ea, w);
-        if ((x >> lane) & 1u) {
-          const int64_t idx = o + e + __popc(x & below);
-          if (idx < P.cap) P.out[idx] = segpos + 32 * w + lane;
-        }
-      }
-#pragma unroll 4
-      for (int w = 0; w < 32; w++) {
-        const uint32_t x = __shfl_sync(0xffffffffu, xb, w);
-        const uint32_t e = __shfl_sync(0xffffffffu, eb, w);
-        if ((x >> lane) & 1u) {
-          const int64_t idx = o + e + __popc(x & below);
-          if (idx < P.cap) P.out[idx] = segpos + 32 * (32 + w) + lane;
-        }
-      }
-    }
-  }
-}
-
-// ------------------------------------------------ kernel 1c: batched multi-pattern pass (K5 "MP")
-// One TMA pass over the text serves a whole batch of anchor-filter (K1
-// ALIGNED) patterns: each 4-aligned text word X is hashed once; a bloom bit
-// test in smem rejects almost every word, and a hit walks the bucket of
-// {gram, pattern, anchor+j} entries.  A verified occurrence (k, s) maps to the
-// same bitmap bit b = s + off + a_k + 3 as the single-pattern ALIGNED plan, so
-// it lands in the consumer's own segment of pattern k's segment layout: one
-// 16-bit atomic count and an (unordered) list slot; offsets/expand are shared
-// (expand sorts MP lists).  Segments above LIST_CAP set `overflow` and the
-// host re-runs the batch through the per-pattern path.
-__global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
-  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
-  uint8_t* stages = smem + SM_STAGES;
-  uint32_t* bloom = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes);
-  uint32_t* bstart = bloom + 2048;
-  uint2* ents = reinterpret_cast<uint2*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < 2048; i += NT + 32) bloom[i] = P.bloom[i];
-  for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
-  for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents[i];
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWARP);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == NWARP) {  // ---------------- producer: text tiles only
-    if (lane == 0) {
-      for (int it = 0;; it++) {
-        const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
-        const unsigned long long tk = atomicAdd(P.ticket, 1ULL);
-        if ((int64_t)tk >= P.ntiles_text) {
-          hdr[s].tk = -1;
-          mbar_arrive(&full[s]);
-          break;
-        }
-        hdr[s].tk = (int64_t)tk;
-        hdr[s].tau = (int64_t)tk;
-        const int64_t start = (int64_t)tk * TILE - P.pre;
-        const int64_t end = (int64_t)tk * TILE + TILE + P.post;
-        const int64_t cs = start < 0 ? 0 : start;
-        const int64_t ce = end > P.nv16 ? P.nv16 : end;
-        const uint32_t tb = ce > cs ? (uint32_t)(ce - cs) : 0u;
-        uint8_t* st = stages + s * P.stage_bytes;
-        mbar_expect_tx(&full[s], tb);
-        if (tb) bulk_g2s(st + (cs - start), P.text + cs, tb, &full[s]);
-      }
-    }
-    return;
-  }
-
-  const int c0 = warp * SEG;
-  for (int it = 0;; it++) {
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
-    const int64_t tau = hdr[s].tk;
-    if (tau < 0) break;
-    const int64_t B0 = tau * TILE;
-    const uint8_t* S = stages + s * P.stage_bytes + P.pre;  // S[c] = virtual byte B0 + c
-#pragma unroll 1
-    for (int r = 0; r < SEG / 512; r++) {
-      const int c = c0 + r * 512 + lane * 16;
-      const uint4 X4 = *reinterpret_cast<const uint4*>(S + c);
-      const uint32_t w[4] = {X4.x, X4.y, X4.z, X4.w};
-      uint32_t hits = 0;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const uint32_t h = w[q] * 0x9E3779B1u;
-        hits |= ((bloom[h >> 21] >> ((h >> 16) & 31)) & 1u) << q;
-      }
-      while (hits) {  // rare: bucket walk + verification
-        const int q = __ffs(hits) - 1;
-        hits &= hits - 1;
-        const uint32_t X = w[q];
-        const uint32_t h = X * 0x9E3779B1u;
-        const uint32_t bk = h >> (32 - P.B);
-        const int64_t x = B0 + c + 4 * q;  // virtual position of the word
-        for (uint32_t e = bstart[bk]; e < bstart[bk + 1]; e++) {
-          const uint2 en = ents[e];
-          if (en.x != X) continue;
-          const int kl = (int)(en.y >> 16);  // pattern within this chunk
-          const int aj = (int)(en.y & 0xFFFFu);
-          const int64_t sv = x - aj;  // virtual start
-          const int64_t spos = sv - P.off;
-          const PatDev* pd = P.pats + P.kbase + kl;
-          const int64_t m = pd->m;
-          if (spos < 0 || spos + m > P.n) continue;
-          const uint8_t* tp = S + (sv - B0);
-          MB_CHECK(tp >= stages + s * P.stage_bytes && tp + m <= stages + (s + 1) * P.stage_bytes);
-          const uint8_t* pp = pd->bytes;
-          bool ok = true;
-          for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);
-          if (!ok) continue;
-          // same bit as the single-pattern ALIGNED plan: b = sv + a + 3 -> this lane's chunk
-          const int64_t b = sv + pd->delta;
-          const int64_t g = ((int64_t)(P.kbase + kl) * P.ntiles + tau) * NWARP + warp;
-          unsigned int* wptr = reinterpret_cast<unsigned int*>(P.counts) + (g >> 1);
-          const unsigned int sh = 16u * (unsigned)(g & 1);
-          const unsigned int old = (atomicAdd(wptr, 1u << sh) >> sh) & 0xFFFFu;
-          if (old < (unsigned)LIST_CAP)
-            P.lists[g * LIST_CAP + old] = (uint16_t)(b - B0);
-          else
-            atomicExch(P.overflow, 1u);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
-
-// K0: byte histogram (Text.alphabet_size, core.py:42-44)
-__global__ void hist_kernel(const uint8_t* t, int64_t n, unsigned long long* hist) {
-  __shared__ unsigned int h[256];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(&h[t[i]], 1u);
-  __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += blockDim.x)
-    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
-}
-
-}  // namespace mb
+using namespace mb;
 
 // ===================================================================== C ABI
-using namespace mb;
 
 static thread_local std::string g_err;
 static std::atomic<int64_t> g_launches{0};

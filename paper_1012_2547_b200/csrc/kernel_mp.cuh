@@ -1,0 +1,138 @@
+// kernel_mp.cuh -- mp_scan_kernel: K5 batched multi-pattern single pass; hist_kernel: K0 byte histogram
+// (part of libmatchb200; included by engine.cu)
+#pragma once
+
+namespace mb {
+
+// ------------------------------------------------ kernel 1c: batched multi-pattern pass (K5 "MP")
+// One TMA pass over the text serves a whole batch of anchor-filter (K1
+// ALIGNED) patterns: each 4-aligned text word X is hashed once; a bloom bit
+// test in smem rejects almost every word, and a hit walks the bucket of
+// {gram, pattern, anchor+j} entries.  A verified occurrence (k, s) maps to the
+// same bitmap bit b = s + off + a_k + 3 as the single-pattern ALIGNED plan, so
+// it lands in the consumer's own segment of pattern k's segment layout: one
+// 16-bit atomic count and an (unordered) list slot; offsets/expand are shared
+// (expand sorts MP lists).  Segments above LIST_CAP set `overflow` and the
+// host re-runs the batch through the per-pattern path.
+__global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
+  uint8_t* stages = smem + SM_STAGES;
+  uint32_t* bloom = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes);
+  uint32_t* bstart = bloom + 2048;
+  uint2* ents = reinterpret_cast<uint2*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 2048; i += NT + 32) bloom[i] = P.bloom[i];
+  for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
+  for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents[i];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NWARP) {  // ---------------- producer: text tiles only
+    if (lane == 0) {
+      for (int it = 0;; it++) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
+        const unsigned long long tk = atomicAdd(P.ticket, 1ULL);
+        if ((int64_t)tk >= P.ntiles_text) {
+          hdr[s].tk = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        hdr[s].tk = (int64_t)tk;
+        hdr[s].tau = (int64_t)tk;
+        const int64_t start = (int64_t)tk * TILE - P.pre;
+        const int64_t end = (int64_t)tk * TILE + TILE + P.post;
+        const int64_t cs = start < 0 ? 0 : start;
+        const int64_t ce = end > P.nv16 ? P.nv16 : end;
+        const uint32_t tb = ce > cs ? (uint32_t)(ce - cs) : 0u;
+        uint8_t* st = stages + s * P.stage_bytes;
+        mbar_expect_tx(&full[s], tb);
+        if (tb) bulk_g2s(st + (cs - start), P.text + cs, tb, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int c0 = warp * SEG;
+  for (int it = 0;; it++) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+    const int64_t tau = hdr[s].tk;
+    if (tau < 0) break;
+    const int64_t B0 = tau * TILE;
+    const uint8_t* S = stages + s * P.stage_bytes + P.pre;  // S[c] = virtual byte B0 + c
+#pragma unroll 1
+    for (int r = 0; r < SEG / 512; r++) {
+      const int c = c0 + r * 512 + lane * 16;
+      const uint4 X4 = *reinterpret_cast<const uint4*>(S + c);
+      const uint32_t w[4] = {X4.x, X4.y, X4.z, X4.w};
+      uint32_t hits = 0;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint32_t h = w[q] * 0x9E3779B1u;
+        hits |= ((bloom[h >> 21] >> ((h >> 16) & 31)) & 1u) << q;
+      }
+      while (hits) {  // rare: bucket walk + verification
+        const int q = __ffs(hits) - 1;
+        hits &= hits - 1;
+        const uint32_t X = w[q];
+        const uint32_t h = X * 0x9E3779B1u;
+        const uint32_t bk = h >> (32 - P.B);
+        const int64_t x = B0 + c + 4 * q;  // virtual position of the word
+        for (uint32_t e = bstart[bk]; e < bstart[bk + 1]; e++) {
+          const uint2 en = ents[e];
+          if (en.x != X) continue;
+          const int kl = (int)(en.y >> 16);  // pattern within this chunk
+          const int aj = (int)(en.y & 0xFFFFu);
+          const int64_t sv = x - aj;  // virtual start
+          const int64_t spos = sv - P.off;
+          const PatDev* pd = P.pats + P.kbase + kl;
+          const int64_t m = pd->m;
+          if (spos < 0 || spos + m > P.n) continue;
+          const uint8_t* tp = S + (sv - B0);
+          MB_CHECK(tp >= stages + s * P.stage_bytes && tp + m <= stages + (s + 1) * P.stage_bytes);
+          const uint8_t* pp = pd->bytes;
+          bool ok = true;
+          for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);
+          if (!ok) continue;
+          // same bit as the single-pattern ALIGNED plan: b = sv + a + 3 -> this lane's chunk
+          const int64_t b = sv + pd->delta;
+          const int64_t g = ((int64_t)(P.kbase + kl) * P.ntiles + tau) * NWARP + warp;
+          unsigned int* wptr = reinterpret_cast<unsigned int*>(P.counts) + (g >> 1);
+          const unsigned int sh = 16u * (unsigned)(g & 1);
+          const unsigned int old = (atomicAdd(wptr, 1u << sh) >> sh) & 0xFFFFu;
+          if (old < (unsigned)LIST_CAP)
+            P.lists[g * LIST_CAP + old] = (uint16_t)(b - B0);
+          else
+            atomicExch(P.overflow, 1u);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+// K0: byte histogram (Text.alphabet_size, core.py:42-44)
+__global__ void hist_kernel(const uint8_t* t, int64_t n, unsigned long long* hist) {
+  __shared__ unsigned int h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(&h[t[i]], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+
+
+}  // namespace mb

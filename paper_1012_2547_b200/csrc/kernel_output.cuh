@@ -1,0 +1,203 @@
+// kernel_output.cuh -- offsets_kernel (segment-count scan + fused sparse expansion) and expand_kernel (dense / MP segments)
+// (part of libmatchb200; included by engine.cu)
+#pragma once
+
+namespace mb {
+
+// ------------------------------------------------ kernel 2: segment offsets (scan)
+// Exclusive scan of per-segment counts in SCAN_CHUNK pieces; chunk order =
+// ticket order taken at CTA start (no prefetch), so each chunk only waits on
+// chunks already running -- the decoupled look-back never stalls on a queued
+// predecessor.
+__global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
+  __shared__ int64_t wsum[NWARP];
+  __shared__ int64_t s_excl;
+  __shared__ int64_t s_chunk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_chunk = (int64_t)atomicAdd(&P.ticket[TICKET_OFFSETS], 1ULL);
+  __syncthreads();
+  const int64_t ch = s_chunk;
+  const int64_t nseg = P.total_tiles * NWARP;
+  const int64_t base = ch * SCAN_CHUNK;
+  constexpr int PER = SCAN_CHUNK / NT;  // 32 counts per thread, read as 16-byte vectors
+  static_assert(PER % 8 == 0, "vector loads of 8 uint16 counts");
+  uint32_t v[PER];
+  int64_t tsum = 0;
+  const uint4* cv = reinterpret_cast<const uint4*>(P.counts + base + (int64_t)tid * PER);
+#pragma unroll
+  for (int q8 = 0; q8 < PER / 8; q8++) {
+    const uint4 x = cv[q8];  // counts are allocated to a whole number of chunks
+    const uint32_t wds[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int h = 0; h < 8; h++) {
+      const int q = 8 * q8 + h;
+      const int64_t t = base + (int64_t)tid * PER + q;
+      v[q] = t < nseg ? ((wds[h >> 1] >> (16 * (h & 1))) & 0xFFFFu) : 0u;
+      tsum += v[q];
+    }
+  }
+  int64_t inc = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  int64_t chunk_total = 0, wbefore = 0;
+  for (int q = 0; q < NWARP; q++) {
+    chunk_total += wsum[q];
+    wbefore += q < warp ? wsum[q] : 0;
+  }
+  if (warp == 0) {
+    int64_t excl = 0;
+    if (ch == 0) {
+      if (lane == 0) st_relaxed(&P.state[0], pack_state(P.epoch, ST_INCL, (uint64_t)chunk_total));
+    } else {
+      if (lane == 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_AGG, (uint64_t)chunk_total));
+      int64_t j = ch - 1;
+      while (true) {
+        const int64_t idx = j - lane;
+        uint64_t sv;
+        if (idx < 0) {
+          sv = pack_state(P.epoch, ST_INCL, 0);
+        } else {
+          while (true) {
+            sv = ld_relaxed(&P.state[idx]);
+            if ((uint32_t)(sv >> 40) == P.epoch && ((sv >> 38) & 3)) break;
+            __nanosleep(20);
+          }
+        }
+        const uint64_t st = (sv >> 38) & 3;
+        const int64_t val = (int64_t)(sv & ((1ULL << 38) - 1));
+        const uint32_t incl = __ballot_sync(0xffffffffu, st == ST_INCL);
+        int64_t contrib = val;
+        if (incl) contrib = lane <= __ffs(incl) - 1 ? val : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
+        excl += contrib;
+        if (incl) break;
+        j -= 32;
+      }
+      if (lane == 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_INCL, (uint64_t)(excl + chunk_total)));
+    }
+    if (lane == 0) s_excl = excl + (P.out_base ? *P.out_base : 0);
+  }
+  __syncthreads();
+  int64_t run = s_excl + wbefore + inc - tsum;
+  const int64_t seg_per_pat = P.ntiles * NWARP;
+  // Sorted sparse segments (<= LIST_CAP uint16 offsets) are expanded right here,
+  // their offsets never leave registers; dense or unsorted (MP) segments are
+  // queued for expand_kernel with their offset.
+  const bool fuse = P.out && !P.unsorted_lists;
+  int cur_k = -1;
+  int64_t shift = 0;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const int64_t t = base + (int64_t)tid * PER + q;
+    if (t < nseg) {
+      if (v[q] && P.out) {
+        if (fuse && v[q] <= (uint32_t)LIST_CAP) {
+          const int64_t tile = t / NWARP;
+          const int k = (int)(tile / P.ntiles);
+          if (k != cur_k) {
+            shift = P.pats[k].delta + P.off;
+            cur_k = k;
+          }
+          const int64_t pos0 = (tile % P.ntiles) * TILE - shift;
+          const uint16_t* L = P.lists + t * LIST_CAP;
+          for (uint32_t e = 0; e < v[q]; e++)
+            if (run + e < P.cap) P.out[run + e] = pos0 + L[e];
+        } else {
+          P.toff[t] = run;
+          const unsigned long long slot = atomicAdd(&P.ticket[TICKET_DENSE], 1ULL);
+          P.seglist[slot] = t;
+        }
+      }
+      if (t % seg_per_pat == seg_per_pat - 1) P.offsets_plus1[t / seg_per_pat] = run + v[q];
+    }
+    run += v[q];
+  }
+}
+
+// ------------------------------------------------ kernel 3: expansion
+// The segments offsets_kernel queued (dense, or MP's unsorted lists), a warp
+// per segment: unsorted lists get a 32-lane bitonic sort, dense segments
+// expand their 64-word bitmap 32 words at a time through a per-warp smem
+// staging buffer so every global store is a coalesced run.
+constexpr int EXP_WARPS = 4;
+__global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nq = (int64_t)P.ticket[TICKET_DENSE];
+  int cur_k = -1;
+  int64_t shift = 0;
+  for (int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp; qi < nq; qi += (int64_t)gridDim.x * EXP_WARPS) {
+    {
+      const int64_t g = P.seglist[qi];
+      const uint32_t c = P.counts[g];
+      const int64_t tile = g / NWARP;
+      const int k = (int)(tile / P.ntiles);
+      if (k != cur_k) {
+        shift = P.pats[k].delta + P.off;
+        cur_k = k;
+      }
+      const int64_t pos0 = (tile % P.ntiles) * TILE - shift;  // tile-relative offsets below
+      const int64_t o = P.toff[g];
+      if (o >= P.cap) continue;
+      if (c <= LIST_CAP) {
+        uint32_t v = lane < (int)c ? (uint32_t)P.lists[g * LIST_CAP + lane] : 0xFFFFFFFFu;
+        if (P.unsorted_lists) {  // MP fills list slots atomically: warp bitonic sort of <= 32 offsets
+#pragma unroll
+          for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+              const uint32_t o2 = __shfl_xor_sync(0xffffffffu, v, jj);
+              const bool up = ((lane & kk) == 0);
+              const bool lower = ((lane & jj) == 0);
+              v = (lower == up) ? min(v, o2) : max(v, o2);
+            }
+        }
+        if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + v;
+        continue;
+      }
+      // dense: the 64 bitmap words (2 per lane), exclusive popcount prefix, then
+      // one word per step broadcast to the warp -- lane i writes bit i's
+      // position at its rank, so a full word is one coalesced 256-byte store
+      const uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
+      const int64_t segpos = pos0 + (g % NWARP) * SEG;
+      const uint32_t xa = bmw[lane], xb = bmw[32 + lane];
+      const uint32_t pa = __popc(xa), pb = __popc(xb);
+      uint32_t ia = pa, ib = pb;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t va = __shfl_up_sync(0xffffffffu, ia, d);
+        const uint32_t vb = __shfl_up_sync(0xffffffffu, ib, d);
+        if (lane >= d) ia += va, ib += vb;
+      }
+      const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31);
+      const uint32_t ea = ia - pa, eb = ta + ib - pb;
+      const uint32_t below = (1u << lane) - 1u;
+#pragma unroll 4
+      for (int w = 0; w < 32; w++) {
+        const uint32_t x = __shfl_sync(0xffffffffu, xa, w);
+        const uint32_t e = __shfl_sync(0xffffffffu, ea, w);
+        if ((x >> lane) & 1u) {
+          const int64_t idx = o + e + __popc(x & below);
+          if (idx < P.cap) P.out[idx] = segpos + 32 * w + lane;
+        }
+      }
+#pragma unroll 4
+      for (int w = 0; w < 32; w++) {
+        const uint32_t x = __shfl_sync(0xffffffffu, xb, w);
+        const uint32_t e = __shfl_sync(0xffffffffu, eb, w);
+        if ((x >> lane) & 1u) {
+          const int64_t idx = o + e + __popc(x & below);
+          if (idx < P.cap) P.out[idx] = segpos + 32 * (32 + w) + lane;
+        }
+      }
+    }
+  }
+}
+
+
+}  // namespace mb

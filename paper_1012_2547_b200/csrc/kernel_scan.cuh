@@ -1,0 +1,268 @@
+// kernel_scan.cuh -- scan_kernel<Filter>: warp-specialised TMA ring, one 2 KiB segment per consumer warp (K1 filters, K2 shift-or)
+// (part of libmatchb200; included by engine.cu)
+#pragma once
+
+namespace mb {
+
+// ---------------------------------------------------------------- kernel 1: scan
+// Warp-specialised: warp NWARP is the TMA producer (ticket -> bulk copies of
+// the tile+halo and of the pattern into a free stage), warps 0..NWARP-1 are
+// consumers that each own one SEG-position segment of every tile.  Stages are
+// handed over through full/empty mbarriers; there is no block-wide barrier in
+// the loop, so warps drift independently within the ring.
+template <class Filt>
+__global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
+  uint8_t* stages = smem + SM_STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (P.run_if && *P.run_if == 0u) return;  // conditional fallback launch (MP did not overflow)
+  uint32_t* bm = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes) + warp * SEG_WORDS;
+  uint32_t* brk = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4) +
+                  warp * 2 * (P.brk_words + 4);
+  int32_t* nbw = reinterpret_cast<int32_t*>(brk + P.brk_words + 4);
+  uint64_t* so_s = reinterpret_cast<uint64_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
+                                               NWARP * 2 * (P.brk_words + 4) * 4) +
+                   warp * 256;  // K2 only: per-warp shift-or masks
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NWARP) {  // ---------------- producer
+    if (lane == 0) {
+      for (int it = 0;; it++) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
+        const unsigned long long tk = atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
+        if ((int64_t)tk >= P.group_tiles) {
+          hdr[s].tk = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        const int kg = (int)((int64_t)tk / P.ntiles);
+        const int k = P.plist ? P.plist[kg] : kg;  // this launch's family group -> batch index
+        const int64_t tau = (int64_t)tk - (int64_t)kg * P.ntiles;
+        hdr[s].tk = (int64_t)k * P.ntiles + tau;   // global tile id (segment index base)
+        hdr[s].k = k;
+        hdr[s].tau = tau;
+        const int64_t start = tau * TILE - P.pre;
+        const int64_t end = tau * TILE + TILE + P.post;
+        const int64_t cs = start < 0 ? 0 : start;
+        const int64_t ce = end > P.nv16 ? P.nv16 : end;
+        const uint32_t tb = ce > cs ? (uint32_t)(ce - cs) : 0u;
+        const PatDev* pd = P.pats + k;
+        const uint32_t pb = (uint32_t)((pd->m + 15) & ~15LL);
+        uint8_t* st = stages + s * P.stage_bytes;
+        mbar_expect_tx(&full[s], tb + pb);
+        bulk_g2s(st, pd->bytes, pb, &full[s]);
+        if (tb) bulk_g2s(st + P.pat_cap + (cs - start), P.text + cs, tb, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int c0 = warp * SEG;  // this warp's segment of every tile
+  int cur_k = -1;
+  PatDev pd;
+  int64_t blo = 0, bhi = -1;
+  for (int it = 0;; it++) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+    const int64_t tk = hdr[s].tk;
+    if (tk < 0) break;
+    const int k = hdr[s].k;
+    if (k != cur_k) {  // per-pattern parameters stay in registers across tiles
+      pd = P.pats[k];
+      blo = P.off + pd.delta;               // valid bits: s = b - delta - off in [0, n-m]
+      bhi = P.off + pd.delta + P.n - pd.m;  // inclusive (may be < blo)
+      cur_k = k;
+      if constexpr (is_shiftor<Filt>::value) {  // this warp's copy of the 256 shift-or masks
+        for (int i = lane; i < 256; i += 32) so_s[i] = pd.so_masks[i];
+        __syncwarp();
+      }
+    }
+    const int64_t B0 = hdr[s].tau * TILE;
+    const uint8_t* spat = stages + s * P.stage_bytes;
+    const uint8_t* S = spat + P.pat_cap + P.pre;  // S[c] = virtual text byte B0 + c
+    const uint8_t* const sbeg = spat + P.pat_cap;  // staged text window [sbeg, send)
+    const uint8_t* const send = spat + P.stage_bytes;
+    (void)sbeg, (void)send;
+    MB_CHECK(S + c0 + SEG + 4 <= send);
+    const int64_t segb = B0 + c0;
+    const bool interior = segb >= blo && segb + SEG - 1 <= bhi;
+
+    // this lane's 64 positions of the segment: linear bitmap words 2*lane, 2*lane+1
+    uint32_t w0 = 0, w1 = 0;
+    bool have;
+    if constexpr (is_shiftor<Filt>::value) {
+      // ---- K2: exact per-lane shift-or over positions [c0 + 64 lane, +64)
+      MB_CHECK(S + c0 + 64 * lane + 64 + pd.m + 3 <= send);
+      shiftor_lane<Filt::kW>(S + c0 + 64 * lane, (int)pd.m, so_s, w0, w1);
+      if (!interior) {
+        const int64_t b = segb + 64 * lane;
+        uint64_t vm = 0;
+        for (int i = 0; i < 64; i++)
+          if (b + i >= blo && b + i <= bhi) vm |= 1ULL << i;
+        w0 &= (uint32_t)vm;
+        w1 &= (uint32_t)(vm >> 32);
+      }
+      have = __any_sync(0xffffffffu, (w0 | w1) != 0);
+    } else {
+      // ---- filter (fast path): 4 rounds of 512 positions, 16 per lane, masks kept in registers
+      uint32_t mk[SEG / 512];
+      bool anyc = false;
+#pragma unroll
+      for (int r = 0; r < SEG / 512; r++) {
+        const int c = c0 + r * 512 + lane * 16;
+        const uint4 X = *reinterpret_cast<const uint4*>(S + c);
+        const uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
+        mk[r] = Filt::run(w, pd);
+        anyc |= (mk[r] != 0);
+      }
+      have = __any_sync(0xffffffffu, anyc);
+      if (have) {
+        // ---- slow path: validity mask at text edges, linear segment bitmap
+#pragma unroll
+        for (int r = 0; r < SEG / 512; r++) {
+          uint32_t m = mk[r];
+          if (!interior) {
+            const int64_t b = segb + r * 512 + lane * 16;
+            uint32_t vm = 0;
+            for (int i = 0; i < 16; i++)
+              if (b + i >= blo && b + i <= bhi) vm |= 1u << i;
+            m &= vm;
+          }
+          const uint32_t other = __shfl_down_sync(0xffffffffu, m, 1);
+          if (!(lane & 1)) bm[r * 16 + (lane >> 1)] = m | (other << 16);
+        }
+        __syncwarp();
+        w0 = bm[2 * lane];
+        w1 = bm[2 * lane + 1];
+      }
+    }
+    uint32_t cnt = 0;
+    if (have) {
+      // ---- verify (exact filters skip this)
+      if (!pd.exact && __any_sync(0xffffffffu, (w0 | w1) != 0)) {
+        const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
+        if (pd.periodic) {
+          // s matches <=> t[s..s+per) = p[0..per) and no break t[y] != t[y+per] for
+          // y in [s, s+L).  A break y kills starts [y-L+1, y]: walk the few breaks
+          // that reach this lane's 64 starts, mask them out in bulk.
+          const int nwords = (SEG + pd.L + 31) / 32;
+          MB_CHECK(Y0 + c0 >= sbeg && Y0 + c0 + 32 * nwords + pd.per + 8 <= send);
+          warp_breaks(Y0 + c0, pd.per, nwords, brk, nbw);
+          uint64_t cand = ((uint64_t)w1 << 32) | w0;
+          if (cand) {
+            auto nb = [&](int y) -> int {
+              if (y >= 32 * nwords) return 0x7fffffff;
+              const uint32_t x = brk[y >> 5] >> (y & 31);
+              return x ? y + __ffs(x) - 1 : nbw[(y >> 5) + 1];
+            };
+            const int q0 = 64 * lane, q1 = q0 + 63;
+            uint64_t killed = 0;
+            for (int y = nb(q0); y != 0x7fffffff && y - pd.L + 1 <= q1; y = nb(y + 1)) {
+              const int lo = max(q0, y - pd.L + 1) - q0, hi = min(q1, y) - q0;
+              if (lo <= hi) killed |= (hi - lo == 63) ? ~0ULL : (((1ULL << (hi - lo + 1)) - 1) << lo);
+              if (y >= q1) break;
+            }
+            cand &= ~killed;
+            if (pd.per > 4) {  // the 4 anchor bytes do not cover a full period: check one block
+              uint64_t cc = cand;
+              while (cc) {
+                const int i = __ffsll((long long)cc) - 1;
+                cc &= cc - 1;
+                MB_CHECK(Y0 + c0 + q0 + i >= sbeg && Y0 + c0 + q0 + i + pd.per <= send);
+                if (!verify_direct(Y0 + c0 + q0 + i, spat, pd.per)) cand &= ~(1ULL << i);
+              }
+            }
+          }
+          w0 = (uint32_t)cand;
+          w1 = (uint32_t)(cand >> 32);
+        } else if (pd.m >= 64) {
+          // long windows: the whole warp verifies one candidate at a time,
+          // lane l comparing 4-byte words l, l+32, ... (smem text vs pattern)
+          const uint64_t mine = ((uint64_t)w1 << 32) | w0;
+          uint64_t keep = 0;
+          uint32_t active = __ballot_sync(0xffffffffu, mine != 0);
+          while (active) {
+            const int src = __ffs(active) - 1;
+            active &= active - 1;
+            uint64_t cm = ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(mine >> 32), src) << 32) |
+                          __shfl_sync(0xffffffffu, (uint32_t)mine, src);
+            while (cm) {
+              const int i = __ffsll((long long)cm) - 1;
+              cm &= cm - 1;
+              const uint8_t* tw = Y0 + c0 + 64 * src + i;
+              MB_CHECK(tw >= sbeg && tw + pd.m + 8 <= send);
+              bool bad = false;
+              for (int k = 4 * lane; k < pd.m; k += 128) {
+                const uint32_t pw = *reinterpret_cast<const uint32_t*>(spat + k);
+                uint32_t diff = lds32u(tw + k) ^ pw;
+                if (pd.m - k < 4) diff &= (1u << (8 * (pd.m - k))) - 1u;
+                bad |= diff != 0;
+              }
+              if (!__any_sync(0xffffffffu, bad) && lane == src) keep |= 1ULL << i;
+            }
+          }
+          w0 = (uint32_t)keep;
+          w1 = (uint32_t)(keep >> 32);
+        } else {
+          uint32_t ws[2] = {w0, w1};
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            uint32_t cw = ws[h], mw = 0;
+            while (cw) {
+              const int i = __ffs(cw) - 1;
+              cw &= cw - 1;
+              MB_CHECK(Y0 + c0 + 32 * (2 * lane + h) + i >= sbeg && Y0 + c0 + 32 * (2 * lane + h) + i + pd.m <= send);
+              if (verify_direct(Y0 + c0 + 32 * (2 * lane + h) + i, spat, (int)pd.m)) mw |= 1u << i;
+            }
+            ws[h] = mw;
+          }
+          w0 = ws[0];
+          w1 = ws[1];
+        }
+      }
+      // ---- count + compact store (segment g = tile * NWARP + warp)
+      const uint32_t c2 = __popc(w0) + __popc(w1);
+      uint32_t inc = c2;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+      cnt = __shfl_sync(0xffffffffu, inc, 31);
+      const int64_t g = tk * NWARP + warp;
+      if (cnt <= LIST_CAP) {
+        uint32_t j = inc - c2;
+        uint16_t* L = P.lists + g * LIST_CAP;
+        uint64_t bits = ((uint64_t)w1 << 32) | w0;
+        while (bits) {
+          const int i = __ffsll((long long)bits) - 1;
+          bits &= bits - 1;
+          L[j++] = (uint16_t)(c0 + 64 * lane + i);
+        }
+      } else {
+        reinterpret_cast<uint2*>(P.bitmaps + g * SEG_WORDS)[lane] = make_uint2(w0, w1);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      P.counts[tk * NWARP + warp] = (uint16_t)cnt;
+      mbar_arrive(&empty[s]);
+    }
+  }
+}
+
+
+}  // namespace mb
