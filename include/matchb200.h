@@ -116,6 +116,9 @@ int mb_search_batch_host(mb_ctx* ctx, const uint8_t* const* h_patterns, const in
 /* ---- K0: device byte histogram (Text.alphabet_size, core.py:42-44) ---- */
 int mb_histogram(mb_ctx* ctx, const uint8_t* d_text, int64_t n, int64_t* d_hist256, void* stream);
 
+/* Batched searches on this context that took the K5 multi-pattern single pass. */
+int64_t mb_ctx_mp_batches(const mb_ctx* ctx);
+
 /* Number of this library's kernels launched so far in this process. */
 int64_t mb_launch_count(void);
 const char* mb_last_error(void);

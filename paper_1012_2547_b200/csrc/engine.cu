@@ -126,6 +126,7 @@ struct mb_ctx {
   int64_t mp_tab_cap = 0;
   std::vector<uint32_t> h_mp;
   std::vector<double> h_ent;
+  int64_t mp_batches = 0;
   uint32_t epoch = 0;
   unsigned long long* ticket = nullptr;
   PatDev* d_pats = nullptr;
@@ -147,6 +148,7 @@ extern "C" {
 const char* mb_last_error(void) { return g_err.c_str(); }
 const char* mb_version(void) { return "matchb200 0.1.0 (sm_100a)"; }
 int64_t mb_launch_count(void) { return g_launches.load(); }
+int64_t mb_ctx_mp_batches(const mb_ctx* c) { return c ? c->mp_batches : 0; }
 
 int mb_plan_create(const uint8_t* h_pattern, int64_t m, const mb_plan_opts* opts, mb_plan** out) {
   if (!out) return fail(MB_EINVAL, "null out");
@@ -551,6 +553,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // sorted on expand either way (harmless for the already-sorted fallback lists)
     P.run_if = M.overflow;
     mp_used = true;
+    c->mp_batches++;
   }
   if (!mp_used) CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 16 * sizeof(unsigned long long), st));
   // group patterns by family key (stable); a single group needs no index list

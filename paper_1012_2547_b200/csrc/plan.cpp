@@ -230,7 +230,8 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
     byte_probs(pat, m, hist, pr);
     best_aligned(pat, m, pr, &ra);
     best_win4(pat, m, pr, &rw);
-    if (8 * rw < ra && !(m >= 16 && ph->period <= m / 2)) fam = MB_FAM_WIN4;
+    // only where ALIGNED would actually be busy (> 1 hit per 1000 words)
+    if (ra > 1e-3 && 8 * rw < ra && !(m >= 16 && ph->period <= m / 2)) fam = MB_FAM_WIN4;
   }
   if (opts && opts->family == MB_FAM_SAMPLED && !sampled_ok) {
     *err = "sampled q-gram family does not apply to this pattern (m < 272, low entropy or periodic)";

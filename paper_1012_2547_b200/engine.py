@@ -31,7 +31,7 @@ EXPORTS = (
     "mb_plan_create", "mb_plan_destroy", "mb_plan_info", "mb_plan_horspool", "mb_plan_sunday",
     "mb_plan_fwd_masks", "mb_plan_kmp", "mb_plan_gram_hash", "mb_ctx_create", "mb_ctx_destroy",
     "mb_find", "mb_find_batch", "mb_search_host", "mb_search_batch_host", "mb_histogram",
-    "mb_launch_count", "mb_last_error", "mb_version",
+    "mb_launch_count", "mb_last_error", "mb_version", "mb_ctx_mp_batches",
 )
 
 
@@ -96,6 +96,8 @@ def load_library():
         L.mb_search_batch_host.restype = i32
         L.mb_histogram.argtypes = [vp, vp, i64, vp, vp]
         L.mb_histogram.restype = i32
+        L.mb_ctx_mp_batches.argtypes = [vp]
+        L.mb_ctx_mp_batches.restype = i64
         L.mb_launch_count.argtypes = []
         L.mb_launch_count.restype = i64
         L.mb_last_error.argtypes = []
@@ -115,6 +117,11 @@ def _check(rc: int):
     if rc == MB_ENOMEM:
         raise MemoryError(msg)
     raise EngineError(f"matchb200 error {rc}: {msg}")
+
+
+def mp_batches() -> int:
+    """Batched searches of this thread's context that took the K5 multi-pattern pass."""
+    return int(load_library().mb_ctx_mp_batches(context().handle))
 
 
 def launch_count() -> int:

@@ -228,7 +228,9 @@ def test_mp_batched_single_pass(cuda, sigma, m):
     for s in (0, 7, TILE - 3, n - m):  # plant pattern 2 at edges / tile boundary
         t[s : s + m] = pats[2]
     t = bytes(t)
+    before = engine.mp_batches()
     res = mb.search_many(pats, t)
+    assert engine.mp_batches() == before + 1, "selective ALIGNED batch did not take the MP pass"
     for p, r in zip(pats, res):
         assert r == oracle.search(p, t).tolist(), (len(p), p[:4])
 
