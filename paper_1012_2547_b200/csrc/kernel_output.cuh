@@ -49,39 +49,44 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
     chunk_total += wsum[q];
     wbefore += q < warp ? wsum[q] : 0;
   }
-  if (warp == 0) {
-    int64_t excl = 0;
-    if (ch == 0) {
-      if (lane == 0) st_relaxed(&P.state[0], pack_state(P.epoch, ST_INCL, (uint64_t)chunk_total));
-    } else {
-      if (lane == 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_AGG, (uint64_t)chunk_total));
-      int64_t j = ch - 1;
-      while (true) {
-        const int64_t idx = j - lane;
-        uint64_t sv;
-        if (idx < 0) {
-          sv = pack_state(P.epoch, ST_INCL, 0);
-        } else {
-          while (true) {
-            sv = ld_relaxed(&P.state[idx]);
-            if ((uint32_t)(sv >> 40) == P.epoch && ((sv >> 38) & 3)) break;
-            __nanosleep(20);
-          }
-        }
-        const uint64_t st = (sv >> 38) & 3;
-        const int64_t val = (int64_t)(sv & ((1ULL << 38) - 1));
-        const uint32_t incl = __ballot_sync(0xffffffffu, st == ST_INCL);
-        int64_t contrib = val;
-        if (incl) contrib = lane <= __ffs(incl) - 1 ? val : 0;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
-        excl += contrib;
-        if (incl) break;
-        j -= 32;
-      }
-      if (lane == 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_INCL, (uint64_t)(excl + chunk_total)));
+  // block-wide decoupled look-back: the whole CTA reads NT predecessors per
+  // round trip (a 16 GiB single-pattern search has 512 chunks: one round trip)
+  __shared__ int s_incl_min;
+  __shared__ unsigned long long s_sum;
+  if (tid == 0) {
+    st_relaxed(&P.state[ch], pack_state(P.epoch, ch == 0 ? ST_INCL : ST_AGG, (uint64_t)chunk_total));
+    s_excl = 0;
+  }
+  int64_t j = ch - 1;  // newest predecessor of this window
+  while (j >= 0) {     // uniform across the CTA (j, s_incl_min read after barriers)
+    if (tid == 0) {
+      s_incl_min = 0x7fffffff;
+      s_sum = 0;
     }
-    if (lane == 0) s_excl = excl + (P.out_base ? *P.out_base : 0);
+    __syncthreads();
+    const int64_t idx = j - tid;
+    uint64_t sv = 0;
+    if (idx >= 0) {
+      while (true) {
+        sv = ld_relaxed(&P.state[idx]);
+        if ((uint32_t)(sv >> 40) == P.epoch && ((sv >> 38) & 3)) break;
+        __nanosleep(20);
+      }
+      if (((sv >> 38) & 3) == ST_INCL) atomicMin(&s_incl_min, tid);
+    }
+    __syncthreads();
+    const int first = s_incl_min;  // nearest predecessor holding an inclusive prefix
+    if (idx >= 0 && tid <= first) atomicAdd(&s_sum, (unsigned long long)(sv & ((1ULL << 38) - 1)));
+    __syncthreads();
+    if (tid == 0) s_excl += (int64_t)s_sum;
+    if (first != 0x7fffffff || j - NT < 0) break;
+    j -= NT;
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (ch > 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_INCL, (uint64_t)(s_excl + chunk_total)));
+    s_excl += P.out_base ? *P.out_base : 0;
   }
   __syncthreads();
   int64_t run = s_excl + wbefore + inc - tsum;
