@@ -444,10 +444,14 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.pats = d_pats;
   P.K = K;
   const int64_t T = P.total_tiles * NWARP;  // segments
-  const int64_t nchunks = (T + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  // offsets_kernel chunk: the largest of NT*{32,16,8} counts that still gives
+  // >= 2 chunks per SM (short texts otherwise leave the scan on a few SMs)
+  const int scan_per = T >= (int64_t)NT * 32 * 2 * c->nsm ? 32 : T >= (int64_t)NT * 16 * 2 * c->nsm ? 16 : 8;
+  const int64_t chunk = (int64_t)NT * scan_per;
+  const int64_t nchunks = (T + chunk - 1) / chunk;
   int rc;
   // whole chunks (offsets_kernel reads 16-byte vectors) + 2 slots for the MP overflow flag
-  if ((rc = grow(&c->counts, &c->counts_cap, nchunks * SCAN_CHUNK + 8, "counts"))) return rc;
+  if ((rc = grow(&c->counts, &c->counts_cap, nchunks * chunk + 8, "counts"))) return rc;
   if ((rc = grow(&c->lists, &c->lists_cap, T * LIST_CAP, "lists"))) return rc;
   if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * SEG_WORDS, "bitmaps"))) return rc;
   if ((rc = grow(&c->toff, &c->toff_cap, T, "tile offsets"))) return rc;
@@ -472,7 +476,12 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   auto finish = [&](bool unsorted) -> int {
     P.epoch = ++c->epoch;
     P.unsorted_lists = unsorted ? 1 : 0;
-    offsets_kernel<<<(int)nchunks, NT, 0, st>>>(P);
+    if (scan_per == 32)
+      offsets_kernel<32><<<(int)nchunks, NT, 0, st>>>(P);
+    else if (scan_per == 16)
+      offsets_kernel<16><<<(int)nchunks, NT, 0, st>>>(P);
+    else
+      offsets_kernel<8><<<(int)nchunks, NT, 0, st>>>(P);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     if (d_out && cap > 0) {

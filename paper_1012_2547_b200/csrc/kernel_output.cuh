@@ -9,6 +9,7 @@ namespace mb {
 // ticket order taken at CTA start (no prefetch), so each chunk only waits on
 // chunks already running -- the decoupled look-back never stalls on a queued
 // predecessor.
+template <int PER>  // counts per thread: chunk = NT * PER (host picks PER for >= 2 chunks per SM)
 __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   __shared__ int64_t wsum[NWARP];
   __shared__ int64_t s_excl;
@@ -18,8 +19,7 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   __syncthreads();
   const int64_t ch = s_chunk;
   const int64_t nseg = P.total_tiles * NWARP;
-  const int64_t base = ch * SCAN_CHUNK;
-  constexpr int PER = SCAN_CHUNK / NT;  // 32 counts per thread, read as 16-byte vectors
+  const int64_t base = ch * (int64_t)(NT * PER);
   static_assert(PER % 8 == 0, "vector loads of 8 uint16 counts");
   uint32_t v[PER];
   int64_t tsum = 0;

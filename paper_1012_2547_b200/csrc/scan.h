@@ -40,7 +40,6 @@ constexpr int SEG = TILE / NWARP; // positions per consumer-warp segment
 constexpr int SEG_WORDS = SEG / 32;
 constexpr int STAGES = MB_STAGES;  // TMA ring depth
 constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offsets
-constexpr int SCAN_CHUNK = 16384; // segment counts per offsets_kernel CTA
 constexpr int TICKET_OFFSETS = 7; // ticket slot of offsets_kernel (slots 0..6: family groups)
 constexpr int MAX_GROUPS = 7;
 constexpr int TICKET_MP0 = 8;     // MP chunk tickets use slots 8..14 (ticket array has 16)
