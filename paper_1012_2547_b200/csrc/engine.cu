@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -125,7 +126,7 @@ struct mb_ctx {
   uint32_t* mp_tab = nullptr;  // MP tables (bloom, bucket starts, entries) per chunk
   int64_t mp_tab_cap = 0;
   std::vector<uint32_t> h_mp;
-  std::vector<double> h_ent;
+  std::vector<double> h_rate;
   int64_t mp_batches = 0;
   uint32_t epoch = 0;
   unsigned long long* ticket = nullptr;
@@ -424,7 +425,7 @@ static void mp_tables(const PatDev* h_pats, int k0, int kc, int* Bout, std::vect
 // output is CSR in the caller's pattern order whatever the family mix.
 static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
                       int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st,
-                      const double* mp_rate = nullptr) {
+                      const double* mp_rates = nullptr, const int64_t* out_base = nullptr) {
   ScanParams P;
   memset(&P, 0, sizeof(P));
   const uintptr_t addr = (uintptr_t)d_text;
@@ -435,8 +436,14 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   int64_t nbits = 0;
   for (int k = 0; k < K; k++)
     if (h_pats[k].m <= n) nbits = std::max<int64_t>(nbits, P.off + h_pats[k].delta + n - h_pats[k].m + 1);
-  if (nbits == 0) {  // every pattern longer than the text
-    CUDA_TRY(cudaMemsetAsync(offsets_plus1, 0, sizeof(int64_t) * K, st));
+  if (nbits == 0) {  // every pattern longer than the text: no output, offsets stay at the base
+    if (out_base) {
+      fill_kernel<<<(K + 255) / 256, 256, 0, st>>>(offsets_plus1, out_base, K);
+      g_launches++;
+      CUDA_TRY(cudaGetLastError());
+    } else {
+      CUDA_TRY(cudaMemsetAsync(offsets_plus1, 0, sizeof(int64_t) * K, st));
+    }
     return MB_OK;
   }
   P.ntiles = (nbits + TILE - 1) / TILE;
@@ -471,7 +478,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.out = d_out;
   P.cap = d_out ? cap : 0;
   P.offsets_plus1 = offsets_plus1;
-  P.out_base = nullptr;
+  P.out_base = out_base;
 
   auto finish = [&](bool unsorted) -> int {
     P.epoch = ++c->epoch;
@@ -494,7 +501,12 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   };
 
   bool mp_used = false;
-  if (mp_eligible(h_pats, mp_rate, K)) {
+  double mp_rate = 1e30;
+  if (mp_rates) {
+    mp_rate = 0;
+    for (int k = 0; k < K; k++) mp_rate += mp_rates[k];
+  }
+  if (mp_eligible(h_pats, mp_rates ? &mp_rate : nullptr, K)) {
     int pre = 0, post = 0;
     for (int k = 0; k < K; k++) pre = std::max(pre, h_pats[k].pre), post = std::max(post, h_pats[k].post);
     MPParams M;
@@ -641,11 +653,10 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
     c->pats_cap = K;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice, st));
-  double rate = 1e30;
-  bool all_aligned = K >= 8;
-  for (int k = 0; k < K && all_aligned; k++) all_aligned = c->h_pats[k].family == MB_FAM_ALIGNED;
-  if (all_aligned) {
-    rate = 0;
+  // per-pattern expected pooled-gram hits per text word (K5 MP eligibility),
+  // byte probabilities estimated from the batch's pattern bytes
+  c->h_rate.assign(K, 1e30);
+  {
     double hist[256] = {0}, tot = 0;
     for (int k = 0; k < K; k++) {
       const auto& pb = plans[k]->h.pat;
@@ -653,14 +664,33 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
       for (size_t i = 0; i < lim; i++) hist[pb[i]] += 1, tot += 1;
     }
     for (int k = 0; k < K; k++)
-      if (c->h_pats[k].family == MB_FAM_ALIGNED)
+      if (c->h_pats[k].family == MB_FAM_ALIGNED) {
+        double r = 0;
         for (int j = 0; j < 4; j++) {
           double pr = 1;
           for (int i = 0; i < 4; i++) pr *= hist[(c->h_pats[k].G[j] >> (8 * i)) & 0xFF] / tot;
-          rate += pr;
+          r += pr;
         }
+        c->h_rate[k] = r;
+      }
   }
-  return run_search(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets + 1, st, &rate);
+  // Scratch is ~338 B per 2 KiB segment per pattern (counts, list, bitmap,
+  // offset, queue): a batch whose scratch would exceed a budget (a third of
+  // free memory, <= 16 GiB) runs as consecutive sub-batches chained through
+  // d_offsets (each starts its output where the previous one ended).
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  double budget = std::min<double>((double)free_b / 3.0, 16.0 * (1ULL << 30));
+  if (const char* env = getenv("MB_SCRATCH_BUDGET")) budget = atof(env);  // tests force sub-batching
+  const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 338.0;
+  const int kc = (int)std::max<double>(1.0, std::min<double>((double)K, budget / per_pattern));
+  for (int k0 = 0; k0 < K; k0 += kc) {
+    const int kk = std::min(kc, K - k0);
+    int rc = run_search(c, c->d_pats + k0, c->h_pats.data() + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st,
+                        c->h_rate.data() + k0, k0 ? d_offsets + k0 : nullptr);
+    if (rc) return rc;
+  }
+  return MB_OK;
 }
 
 int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, void* stream) {

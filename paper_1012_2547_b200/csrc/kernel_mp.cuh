@@ -122,6 +122,12 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   }
 }
 
+// dst[i] = *src for i < n (CSR ends of patterns that cannot match, chained batches)
+__global__ void fill_kernel(int64_t* dst, const int64_t* src, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = *src;
+}
+
 // K0: byte histogram (Text.alphabet_size, core.py:42-44)
 __global__ void hist_kernel(const uint8_t* t, int64_t n, unsigned long long* hist) {
   __shared__ unsigned int h[256];
