@@ -50,7 +50,10 @@ __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& 
   return nf;
 }
 
-__global__ void __launch_bounds__(SMP_NT) sampled_kernel(const ScanParams P) {
+#ifndef MB_SMP_MINB
+#define MB_SMP_MINB 3
+#endif
+__global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const ScanParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* bloom = reinterpret_cast<uint32_t*>(smem);                 // 2048 words
   uint16_t* bstart = reinterpret_cast<uint16_t*>(smem + 8192);         // <= 1025
