@@ -20,7 +20,7 @@ constexpr int SMP_LIST = 1024;   // per-warp match capacity per unit (bound: 131
 #define MB_SMP_ILP 4
 #endif
 #ifndef MB_SMP_WARPS
-#define MB_SMP_WARPS 16
+#define MB_SMP_WARPS 8
 #endif
 constexpr int SMP_ILP = MB_SMP_ILP;     // samples per lane per batch
 constexpr int SMP_WARPS = MB_SMP_WARPS; // warps per sampled_kernel CTA (independent of the scan tiling)
