@@ -104,6 +104,14 @@ int mb_find(mb_ctx* ctx, const mb_plan* plan, const uint8_t* d_text, int64_t n, 
 int mb_find_batch(mb_ctx* ctx, const mb_plan* const* plans, int K, const uint8_t* d_text, int64_t n,
                   int64_t* d_out, int64_t cap, int64_t* d_offsets, void* stream);
 
+/* Prepared batch (compile once, search many texts): holds the device params of
+ * K plans and the K5 multi-pattern tables.  The plans must outlive the batch. */
+typedef struct mb_batch mb_batch;
+int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out);
+void mb_batch_destroy(mb_batch* batch);
+int mb_find_batch_prepared(mb_ctx* ctx, const mb_batch* batch, const uint8_t* d_text, int64_t n, int64_t* d_out,
+                           int64_t cap, int64_t* d_offsets, void* stream);
+
 /* ---- host-buffer entry (the search_X(pattern, text) analogue, synchronous) ----
  * Copies the text host->device, scans, copies positions device->host.  Returns
  * MB_EOVERFLOW (with *h_count set) if cap is too small. */

@@ -144,6 +144,19 @@ struct mb_ctx {
   cudaStream_t stream = nullptr;
 };
 
+// A prepared batch: device params of K plans + K5 MP tables, built once
+// (mb_batch_create) and reused by every mb_find_batch_prepared call -- the
+// batched analogue of the reference's compile-once / run-many split.
+struct mb_batch {
+  int K = 0;
+  int device = 0;
+  std::vector<PatDev> h_pats;
+  PatDev* d_pats = nullptr;
+  std::vector<double> rates;
+  uint32_t* d_mp = nullptr;
+  std::vector<std::pair<int64_t, int>> mp_chunks;
+};
+
 extern "C" {
 
 const char* mb_last_error(void) { return g_err.c_str(); }
@@ -425,7 +438,8 @@ static void mp_tables(const PatDev* h_pats, int k0, int kc, int* Bout, std::vect
 // output is CSR in the caller's pattern order whatever the family mix.
 static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
                       int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st,
-                      const double* mp_rates = nullptr, const int64_t* out_base = nullptr) {
+                      const double* mp_rates = nullptr, const int64_t* out_base = nullptr,
+                      const uint32_t* mp_dev = nullptr, const std::pair<int64_t, int>* mp_chunks = nullptr) {
   ScanParams P;
   memset(&P, 0, sizeof(P));
   const uintptr_t addr = (uintptr_t)d_text;
@@ -523,23 +537,30 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     M.pats = d_pats;
     M.counts = c->counts;
     M.lists = c->lists;
-    if ((rc = grow(&c->mp_tab, &c->mp_tab_cap, (int64_t)(2048 + 4 * MP_CHUNK + 8 + 8 * MP_CHUNK) * MAX_GROUPS,
-                   "MP tables")))
+    if (!mp_dev && (rc = grow(&c->mp_tab, &c->mp_tab_cap, (int64_t)(2048 + 4 * MP_CHUNK + 8 + 8 * MP_CHUNK) * MAX_GROUPS,
+                              "MP tables")))
       return rc;
     M.overflow = reinterpret_cast<unsigned int*>(c->counts + T);  // 4 spare bytes after the counts
     CUDA_TRY(cudaMemsetAsync(c->counts, 0, sizeof(uint16_t) * (T + 2), st));
     CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 16 * sizeof(unsigned long long), st));
-    c->h_mp.clear();
+    // MP tables: prepared once with the batch (mb_batch_create) or built here
+    const uint32_t* tab = mp_dev;
     std::vector<std::pair<int64_t, int>> chunk_at;  // (table word offset, B) per chunk
-    for (int k0 = 0, ci = 0; k0 < K; k0 += MP_CHUNK, ci++) {
-      std::vector<uint32_t> img;
-      int B = 0;
-      mp_tables(h_pats, k0, std::min(MP_CHUNK, K - k0), &B, img);
-      chunk_at.push_back({(int64_t)c->h_mp.size(), B});
-      c->h_mp.insert(c->h_mp.end(), img.begin(), img.end());
-      while (c->h_mp.size() % 4) c->h_mp.push_back(0);
+    if (mp_dev && mp_chunks) {
+      for (int k0 = 0, ci = 0; k0 < K; k0 += MP_CHUNK, ci++) chunk_at.push_back(mp_chunks[ci]);
+    } else {
+      c->h_mp.clear();
+      for (int k0 = 0; k0 < K; k0 += MP_CHUNK) {
+        std::vector<uint32_t> img;
+        int B = 0;
+        mp_tables(h_pats, k0, std::min(MP_CHUNK, K - k0), &B, img);
+        chunk_at.push_back({(int64_t)c->h_mp.size(), B});
+        c->h_mp.insert(c->h_mp.end(), img.begin(), img.end());
+        while (c->h_mp.size() % 4) c->h_mp.push_back(0);
+      }
+      CUDA_TRY(cudaMemcpyAsync(c->mp_tab, c->h_mp.data(), sizeof(uint32_t) * c->h_mp.size(), cudaMemcpyHostToDevice, st));
+      tab = c->mp_tab;
     }
-    CUDA_TRY(cudaMemcpyAsync(c->mp_tab, c->h_mp.data(), sizeof(uint32_t) * c->h_mp.size(), cudaMemcpyHostToDevice, st));
     static std::mutex mu_mp;
     static bool attr_mp = false;
     {
@@ -553,7 +574,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       const int kc = std::min(MP_CHUNK, K - k0);
       const int B = chunk_at[ci].second;
       const int bs_words = ((1 << B) + 1 + 3) & ~3;
-      M.bloom = c->mp_tab + chunk_at[ci].first;
+      M.bloom = tab + chunk_at[ci].first;
       M.bstart = M.bloom + 2048;
       M.ents = reinterpret_cast<const uint2*>(M.bstart + bs_words);
       M.B = B;
@@ -626,15 +647,58 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
   return run_search(c, dd, &p->dview, 1, d_text, n, d_out, cap, d_count, st);
 }
 
+// per-pattern expected pooled-gram hits per text word (K5 MP eligibility),
+// byte probabilities estimated from the batch's own pattern bytes
+static void batch_rates(const mb_plan* const* plans, const PatDev* h_pats, int K, std::vector<double>* rates) {
+  rates->assign(K, 1e30);
+  double hist[256] = {0}, tot = 0;
+  for (int k = 0; k < K; k++) {
+    const auto& pb = plans[k]->h.pat;
+    const size_t lim = std::min<size_t>(pb.size(), 64);
+    for (size_t i = 0; i < lim; i++) hist[pb[i]] += 1, tot += 1;
+  }
+  for (int k = 0; k < K; k++)
+    if (h_pats[k].family == MB_FAM_ALIGNED) {
+      double r = 0;
+      for (int j = 0; j < 4; j++) {
+        double pr = 1;
+        for (int i = 0; i < 4; i++) pr *= hist[(h_pats[k].G[j] >> (8 * i)) & 0xFF] / tot;
+        r += pr;
+      }
+      (*rates)[k] = r;
+    }
+}
+
+// Run a batch whose params are on the device as sub-batches under the scratch
+// budget (~338 B per 2 KiB segment per pattern: counts, list, bitmap, offset,
+// queue; a third of free memory, <= 16 GiB), chained through d_offsets.
+static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, const double* rates, int K,
+                     const uint8_t* d_text, int64_t n, int64_t* d_out, int64_t cap, int64_t* d_offsets, cudaStream_t st,
+                     const uint32_t* mp_dev, const std::pair<int64_t, int>* mp_chunks) {
+  CUDA_TRY(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  double budget = std::min<double>((double)free_b / 3.0, 16.0 * (1ULL << 30));
+  if (const char* env = getenv("MB_SCRATCH_BUDGET")) budget = atof(env);  // tests force sub-batching
+  const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 338.0;
+  int kc = (int)std::max<double>(1.0, std::min<double>((double)K, budget / per_pattern));
+  if (kc < K && kc >= MP_CHUNK) kc -= kc % MP_CHUNK;  // keep prepared MP tables aligned to sub-batches
+  for (int k0 = 0; k0 < K; k0 += kc) {
+    const int kk = std::min(kc, K - k0);
+    const bool aligned = mp_dev && (k0 % MP_CHUNK) == 0;
+    int rc = run_search(c, d_pats + k0, h_pats + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st, rates + k0,
+                        k0 ? d_offsets + k0 : nullptr, aligned ? mp_dev : nullptr,
+                        aligned ? mp_chunks + k0 / MP_CHUNK : nullptr);
+    if (rc) return rc;
+  }
+  return MB_OK;
+}
+
 int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* d_text, int64_t n,
                   int64_t* d_out, int64_t cap, int64_t* d_offsets, void* stream) {
   if (!c || !plans || K < 1 || !d_offsets) return fail(MB_EINVAL, "bad argument");
   if (n < 0 || cap < 0) return fail(MB_EINVAL, "negative size");
   cudaStream_t st = (cudaStream_t)stream;
-  CUDA_TRY(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
-  // group consecutive runs of the same family into one launch each; the
-  // look-back ticket order makes each group's output CSR-contiguous, so the
-  // groups chain through d_offsets.
   c->h_pats.resize(K);
   for (int k = 0; k < K; k++) {
     if (!plans[k]) return fail(MB_EINVAL, "null plan in batch");
@@ -643,54 +707,78 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
     if (rc) return rc;
     c->h_pats[k] = plans[k]->dview;
   }
-  if (K > c->pats_cap) {
-    cudaFree(c->d_pats);
-    c->d_pats = nullptr;
-    if (cudaMalloc(&c->d_pats, sizeof(PatDev) * K) != cudaSuccess) {
-      c->pats_cap = 0;
-      return fail(MB_ENOMEM, "batch params alloc");
-    }
-    c->pats_cap = K;
-  }
+  int rc;
+  if ((rc = grow(&c->d_pats, &c->pats_cap, K, "batch params"))) return rc;
   CUDA_TRY(cudaMemcpyAsync(c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice, st));
-  // per-pattern expected pooled-gram hits per text word (K5 MP eligibility),
-  // byte probabilities estimated from the batch's pattern bytes
-  c->h_rate.assign(K, 1e30);
-  {
-    double hist[256] = {0}, tot = 0;
-    for (int k = 0; k < K; k++) {
-      const auto& pb = plans[k]->h.pat;
-      const size_t lim = std::min<size_t>(pb.size(), 64);
-      for (size_t i = 0; i < lim; i++) hist[pb[i]] += 1, tot += 1;
+  batch_rates(plans, c->h_pats.data(), K, &c->h_rate);
+  return run_batch(c, c->d_pats, c->h_pats.data(), c->h_rate.data(), K, d_text, n, d_out, cap, d_offsets, st, nullptr,
+                   nullptr);
+}
+
+int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out) {
+  if (!out || !plans || K < 1) return fail(MB_EINVAL, "bad argument");
+  *out = nullptr;
+  mb_batch* b = new mb_batch();
+  b->K = K;
+  b->h_pats.resize(K);
+  for (int k = 0; k < K; k++) {
+    const PatDev* dd = nullptr;
+    int rc = plans[k] ? plan_device(plans[k], &dd) : fail(MB_EINVAL, "null plan in batch");
+    if (rc) {
+      delete b;
+      return rc;
     }
-    for (int k = 0; k < K; k++)
-      if (c->h_pats[k].family == MB_FAM_ALIGNED) {
-        double r = 0;
-        for (int j = 0; j < 4; j++) {
-          double pr = 1;
-          for (int i = 0; i < 4; i++) pr *= hist[(c->h_pats[k].G[j] >> (8 * i)) & 0xFF] / tot;
-          r += pr;
-        }
-        c->h_rate[k] = r;
-      }
+    b->h_pats[k] = plans[k]->dview;
   }
-  // Scratch is ~338 B per 2 KiB segment per pattern (counts, list, bitmap,
-  // offset, queue): a batch whose scratch would exceed a budget (a third of
-  // free memory, <= 16 GiB) runs as consecutive sub-batches chained through
-  // d_offsets (each starts its output where the previous one ended).
-  size_t free_b = 0, total_b = 0;
-  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-  double budget = std::min<double>((double)free_b / 3.0, 16.0 * (1ULL << 30));
-  if (const char* env = getenv("MB_SCRATCH_BUDGET")) budget = atof(env);  // tests force sub-batching
-  const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 338.0;
-  const int kc = (int)std::max<double>(1.0, std::min<double>((double)K, budget / per_pattern));
-  for (int k0 = 0; k0 < K; k0 += kc) {
-    const int kk = std::min(kc, K - k0);
-    int rc = run_search(c, c->d_pats + k0, c->h_pats.data() + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st,
-                        c->h_rate.data() + k0, k0 ? d_offsets + k0 : nullptr);
-    if (rc) return rc;
+  cudaGetDevice(&b->device);
+  batch_rates(plans, b->h_pats.data(), K, &b->rates);
+  std::vector<uint32_t> img;
+  bool all_aligned = true;
+  for (int k = 0; k < K; k++) all_aligned &= b->h_pats[k].family == MB_FAM_ALIGNED;
+  if (all_aligned && K >= 8)
+    for (int k0 = 0; k0 < K; k0 += MP_CHUNK) {
+      std::vector<uint32_t> one;
+      int B = 0;
+      mp_tables(b->h_pats.data(), k0, std::min(MP_CHUNK, K - k0), &B, one);
+      b->mp_chunks.push_back({(int64_t)img.size(), B});
+      img.insert(img.end(), one.begin(), one.end());
+      while (img.size() % 4) img.push_back(0);
+    }
+  if (cudaMalloc(&b->d_pats, sizeof(PatDev) * K) != cudaSuccess ||
+      (!img.empty() && cudaMalloc(&b->d_mp, sizeof(uint32_t) * img.size()) != cudaSuccess)) {
+    cudaFree(b->d_pats);
+    delete b;
+    return fail(MB_ENOMEM, "batch upload alloc");
   }
+  cudaError_t e = cudaMemcpy(b->d_pats, b->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !img.empty())
+    e = cudaMemcpy(b->d_mp, img.data(), sizeof(uint32_t) * img.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(b->d_pats);
+    cudaFree(b->d_mp);
+    delete b;
+    return cuda_fail(e, "batch upload");
+  }
+  *out = b;
   return MB_OK;
+}
+
+void mb_batch_destroy(mb_batch* b) {
+  if (!b) return;
+  cudaFree(b->d_pats);
+  cudaFree(b->d_mp);
+  delete b;
+}
+
+int mb_find_batch_prepared(mb_ctx* c, const mb_batch* b, const uint8_t* d_text, int64_t n, int64_t* d_out,
+                           int64_t cap, int64_t* d_offsets, void* stream) {
+  if (!c || !b || !d_offsets) return fail(MB_EINVAL, "bad argument");
+  if (n < 0 || cap < 0) return fail(MB_EINVAL, "negative size");
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev != b->device) return fail(MB_EINVAL, "batch was prepared on another device");
+  return run_batch(c, b->d_pats, b->h_pats.data(), b->rates.data(), b->K, d_text, n, d_out, cap, d_offsets,
+                   (cudaStream_t)stream, b->d_mp, b->mp_chunks.empty() ? nullptr : b->mp_chunks.data());
 }
 
 int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, void* stream) {

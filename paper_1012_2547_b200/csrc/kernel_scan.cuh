@@ -188,9 +188,10 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
           }
           w0 = (uint32_t)cand;
           w1 = (uint32_t)(cand >> 32);
-        } else if (pd.m >= 64) {
-          // long windows: the whole warp verifies one candidate at a time,
-          // lane l comparing 4-byte words l, l+32, ... (smem text vs pattern)
+        } else if (pd.m >= 64 && __reduce_add_sync(0xffffffffu, __popc(w0) + __popc(w1)) <= 32) {
+          // long windows, few candidates: the whole warp verifies one candidate
+          // at a time, lane l comparing 4-byte words l, l+32, ... (smem text vs
+          // pattern).  Dense candidates (small alphabets) stay lane-parallel.
           const uint64_t mine = ((uint64_t)w1 << 32) | w0;
           uint64_t keep = 0;
           uint32_t active = __ballot_sync(0xffffffffu, mine != 0);

@@ -31,7 +31,8 @@ EXPORTS = (
     "mb_plan_create", "mb_plan_destroy", "mb_plan_info", "mb_plan_horspool", "mb_plan_sunday",
     "mb_plan_fwd_masks", "mb_plan_kmp", "mb_plan_gram_hash", "mb_ctx_create", "mb_ctx_destroy",
     "mb_find", "mb_find_batch", "mb_search_host", "mb_search_batch_host", "mb_histogram",
-    "mb_launch_count", "mb_last_error", "mb_version", "mb_ctx_mp_batches",
+    "mb_launch_count", "mb_last_error", "mb_version", "mb_ctx_mp_batches", "mb_batch_create", "mb_batch_destroy",
+    "mb_find_batch_prepared",
 )
 
 
@@ -96,6 +97,12 @@ def load_library():
         L.mb_search_batch_host.restype = i32
         L.mb_histogram.argtypes = [vp, vp, i64, vp, vp]
         L.mb_histogram.restype = i32
+        L.mb_batch_create.argtypes = [vp, i32, ctypes.POINTER(vp)]
+        L.mb_batch_create.restype = i32
+        L.mb_batch_destroy.argtypes = [vp]
+        L.mb_batch_destroy.restype = None
+        L.mb_find_batch_prepared.argtypes = [vp, vp, vp, i64, vp, i64, vp, vp]
+        L.mb_find_batch_prepared.restype = i32
         L.mb_ctx_mp_batches.argtypes = [vp]
         L.mb_ctx_mp_batches.restype = i64
         L.mb_launch_count.argtypes = []
@@ -348,9 +355,38 @@ def count(plan: Plan, text, stream=None) -> int:
     return int(cnt.item())
 
 
+class Batch:
+    """Prepared batch (mb_batch_create): device params + multi-pattern tables of
+    K plans built once, reused for every text -- compile once, search many."""
+
+    def __init__(self, plans):
+        L = load_library()
+        self.plans = list(plans)  # keep the plans alive for the batch's lifetime
+        K = len(self.plans)
+        arr = (ctypes.c_void_p * K)(*[p.handle.value for p in self.plans])
+        h = ctypes.c_void_p()
+        _check(L.mb_batch_create(arr, K, ctypes.byref(h)))
+        self._h = h
+
+    def __len__(self):
+        return len(self.plans)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.mb_batch_destroy(h)
+            self._h = None
+
+
 def find_batch_into(plans, d_text, out, offsets, stream=None):
     L = load_library()
     ctx = context()
+    if isinstance(plans, Batch):
+        cap = 0 if out is None else out.numel()
+        _check(L.mb_find_batch_prepared(ctx.handle, plans._h, ctypes.c_void_p(d_text.data_ptr() if d_text.numel() else 0),
+                                        d_text.numel(), ctypes.c_void_p(out.data_ptr() if out is not None else 0), cap,
+                                        ctypes.c_void_p(offsets.data_ptr()), _stream_handle(stream)))
+        return
     K = len(plans)
     arr = (ctypes.c_void_p * K)(*[p.handle.value for p in plans])
     cap = 0 if out is None else out.numel()

@@ -235,6 +235,25 @@ def test_mp_batched_single_pass(cuda, sigma, m):
         assert r == oracle.search(p, t).tolist(), (len(p), p[:4])
 
 
+def test_prepared_batch_matches_adhoc(cuda):
+    rng = np.random.default_rng(44)
+    t = rand_bytes(rng, 128, 4 * TILE)
+    d = torch.from_numpy(np.frombuffer(t, dtype=np.uint8).copy()).cuda()
+    pats = [t[i : i + 24] for i in rng.integers(0, len(t) - 24, 700)] + [t[5:9], t[100:2100]]
+    plans = [engine.Plan(p) for p in pats]
+    batch = engine.Batch(plans)
+    before = engine.mp_batches()
+    pos_b, offs_b = engine.find_batch(batch, d)
+    pos_a, offs_a = engine.find_batch(plans, d)
+    assert torch.equal(pos_a, pos_b) and torch.equal(offs_a, offs_b)
+    for k in (0, 1, 500, 700, 701):
+        assert pos_b[offs_b[k] : offs_b[k + 1]].cpu().tolist() == oracle.search(pats[k], t).tolist()
+    mp = engine.Batch([engine.Plan(p) for p in pats[:600]])  # all ALIGNED: prepared MP tables (2 chunks)
+    pos_m, offs_m = engine.find_batch(mp, d)
+    assert engine.mp_batches() >= before + 1
+    assert torch.equal(pos_m, pos_a[: int(offs_a[600])]) and torch.equal(offs_m, offs_a[:601])
+
+
 def test_mp_overflow_falls_back(cuda):
     # a dense, selective-looking batch: every pattern occurs > LIST_CAP times per 2 KiB segment
     rng = np.random.default_rng(5)
