@@ -55,17 +55,19 @@ typedef struct {
   int family;            /* MB_FAM_* request (AUTO = engine choice) */
   int sigma_hint;        /* alphabet size if known (0 = unknown) */
   const int64_t* hist;   /* optional 256-entry text byte histogram for anchor choice */
+  int anchor_words;      /* ALIGNED anchor words 1..3 (window 4w+3 bytes; 0 = engine choice) */
 } mb_plan_opts;
 
 typedef struct {
   int64_t m;
   int family;     /* chosen MB_FAM_* */
-  int anchor;     /* pattern offset of the 7-byte anchor window (ALIGNED) */
+  int anchor;     /* pattern offset of the anchor window (ALIGNED, WIN4) */
   int delta;      /* bitmap index shift: bit b <-> position b - delta */
   int period;     /* smallest period of the pattern (== m if aperiodic) */
   int periodic;   /* 1 if verification uses the period/break-run test */
   int stride;     /* K3 sampling stride S in bytes (0 unless family == MB_FAM_SAMPLED) */
   int gram;       /* K3 gram length q in bytes (0 unless family == MB_FAM_SAMPLED) */
+  int words;      /* ALIGNED anchor words (window 4 words + 3 bytes; 0 for other families) */
 } mb_plan_info_t;
 
 /* ---- plans: the compile_X(p) analogue (comparison.py:70-352 preprocessing) ---- */

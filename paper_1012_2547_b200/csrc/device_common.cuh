@@ -62,6 +62,14 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// predicated 8-byte store without a branch (keeps warp-synchronous loops
+// convergent, so the shuffles around it need no divergence checks)
+__device__ __forceinline__ void st_if(bool c, int64_t* p, int64_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.global.s64 [%0], %1;\n}" ::"l"(p), "l"(v),
+               "r"((uint32_t)c)
+               : "memory");
+}
+
 // look-back flag word: [epoch:24][status:2][value:38]
 constexpr uint64_t ST_AGG = 1, ST_INCL = 2;
 __device__ __forceinline__ uint64_t pack_state(uint32_t epoch, uint64_t st, uint64_t val) {
@@ -127,20 +135,30 @@ struct FiltWIN4 {
 
 // K1/K3 / m >= 7: every occurrence contains one 4-aligned text word inside its
 // 7-byte anchor window [a, a+7); that word equals p[a+j .. a+j+4) for exactly
-// one j in 0..3.  Word k matching G_j marks bitmap position 4k + 3 - j.
+// one j in 0..3.  Word k matching G_j marks bitmap position 4k + 3 - j.  With
+// NW anchor words (window 4 NW + 3 bytes) words k .. k+NW-1 must all match
+// (G[4w + j] = p[a+j+4w .. +4)): small alphabets need NW = 2, 3 to keep the
+// candidate rate low.  w[] holds 4 + NW - 1 >= 5 words.
+template <int NW>
 struct FiltALIGNED {
   __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
-    bool hit = false;
+    if constexpr (NW == 1) {
+      bool hit = false;
 #pragma unroll
-    for (int k = 0; k < 4; k++)
-      hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
-    if (!hit) return 0;
+      for (int k = 0; k < 4; k++)
+        hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
+      if (!hit) return 0;
+    }
     uint32_t mk = 0;
 #pragma unroll
     for (int k = 0; k < 4; k++)
 #pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (w[k] == P.G[j]) mk |= 1u << (4 * k + 3 - j);
+      for (int j = 0; j < 4; j++) {
+        bool h = w[k] == P.G[j];
+        if (NW >= 2) h &= w[k + 1] == P.G[4 + j];
+        if (NW >= 3) h &= w[k + 2] == P.G[8 + j];
+        if (h) mk |= 1u << (4 * k + 3 - j);
+      }
     return mk;
   }
 };
@@ -184,30 +202,41 @@ __device__ __forceinline__ void shiftor_lane(const uint8_t* q, int m, const uint
 }
 
 // ------------------------------------------------------------ verification
-// Direct window compare in shared memory (core.py:131-136 match_at).
+// Direct window compare in shared memory (core.py:131-136 match_at), 4 bytes
+// at a time: text words unaligned (lds32u), pattern 16-byte aligned.  Reads up
+// to s + m + 4.
+__device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {  // unaligned 4-byte smem read
+  const uintptr_t a = (uintptr_t)p;
+  const uint32_t* b = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  return __funnelshift_r(b[0], b[1], 8 * (uint32_t)(a & 3));
+}
 __device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* pat, int m) {
-  for (int k = 0; k < m; k++)
-    if (s[k] != pat[k]) return false;
+  int k = 0;
+  for (; k + 4 <= m; k += 4)
+    if (lds32u(s + k) != *reinterpret_cast<const uint32_t*>(pat + k)) return false;
+  if (k < m) {
+    const uint32_t mask = (1u << (8 * (m - k))) - 1u;
+    if ((lds32u(s + k) ^ *reinterpret_cast<const uint32_t*>(pat + k)) & mask) return false;
+  }
   return true;
 }
 
 // Per-warp break bitmap of a segment: bit q of word i set iff
 // t[y] != t[y + per] for y = y0 + 32 i + q (y relative to the segment's first
 // start position).  nbw[i] = first break at or after word i (relative to y0).
-__device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {  // unaligned 4-byte smem read
-  const uintptr_t a = (uintptr_t)p;
-  const uint32_t* b = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
-  return __funnelshift_r(b[0], b[1], 8 * (uint32_t)(a & 3));
-}
-
 __device__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* brk, int32_t* nbw) {
   const int lane = threadIdx.x & 31;
-  for (int i = lane; i < nwords; i += 32) {  // SWAR: 4 byte pairs per compare
-    const uint8_t* q = Yseg + 32 * i;
-    uint32_t bits = 0;
-#pragma unroll
-    for (int b = 0; b < 32; b += 4) bits |= ((~zero_bytes4(lds32u(q + b) ^ lds32u(q + b + per))) & 0xFu) << b;
-    brk[i] = bits;
+  // 128 bytes (4 break words) per step, lane l on bytes [4l, 4l+4): consecutive
+  // lanes read consecutive smem words (no bank conflicts); the 4-bit SWAR
+  // results of 8 lanes are OR-combined into one break word
+  for (int j = 0; 4 * j < nwords; j++) {
+    const bool ok = 4 * j + (lane >> 3) < nwords;
+    const uint8_t* q = Yseg + 128 * j + 4 * lane;
+    uint32_t nib = ok ? ((~zero_bytes4(lds32u(q) ^ lds32u(q + per))) & 0xFu) << (4 * (lane & 7)) : 0u;
+    nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
+    nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
+    nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
+    if (ok && (lane & 7) == 0) brk[4 * j + (lane >> 3)] = nib;
   }
   __syncwarp();
   const int seg = (nwords + 31) / 32;

@@ -142,6 +142,17 @@ struct mb_ctx {
   int64_t offs_cap = 0;
   std::vector<mb_plan*> tmp_plans;
   cudaStream_t stream = nullptr;
+  // pinned staging for the per-call uploads (batch params, MP tables, family
+  // index lists): pageable cudaMemcpyAsync would block the host until the
+  // stream drains.  Two arenas alternate between calls; an arena is reused
+  // once the event recorded after its copies has completed.
+  struct Stage {
+    uint8_t* h = nullptr;
+    size_t cap = 0, used = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  } stage[2];
+  int stage_i = 0;
 };
 
 // A prepared batch: device params of K plans + K5 MP tables, built once
@@ -197,6 +208,7 @@ int mb_plan_info(const mb_plan* p, mb_plan_info_t* info) {
   info->periodic = p->h.dev.periodic;
   info->stride = p->h.family == MB_FAM_SAMPLED ? p->h.dev.S : 0;
   info->gram = p->h.family == MB_FAM_SAMPLED ? p->h.dev.q : 0;
+  info->words = p->h.family == MB_FAM_ALIGNED ? p->h.dev.nw : 0;
   return MB_OK;
 }
 
@@ -262,10 +274,56 @@ void mb_ctx_destroy(mb_ctx* c) {
   cudaFree(c->d_out);
   cudaFree(c->d_offs);
   if (c->stream) cudaStreamDestroy(c->stream);
+  for (auto& s : c->stage) {
+    if (s.ev) {
+      cudaEventSynchronize(s.ev);
+      cudaEventDestroy(s.ev);
+    }
+    cudaFreeHost(s.h);
+  }
   delete c;
 }
 
 }  // extern "C"
+
+// ---- pinned upload staging (see mb_ctx::stage)
+static int stage_begin(mb_ctx* c) {
+  c->stage_i ^= 1;
+  auto& s = c->stage[c->stage_i];
+  if (s.pending) {
+    CUDA_TRY(cudaEventSynchronize(s.ev));
+    s.pending = false;
+  }
+  s.used = 0;
+  return MB_OK;
+}
+static int stage_upload(mb_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return MB_OK;
+  auto& s = c->stage[c->stage_i];
+  const size_t need = s.used + ((bytes + 15) & ~(size_t)15);
+  if (need > s.cap) {
+    if (s.used) CUDA_TRY(cudaStreamSynchronize(st));  // this call's earlier copies still read the old arena
+    cudaFreeHost(s.h);
+    s.h = nullptr;
+    s.cap = 0;
+    s.used = 0;
+    const size_t ncap = std::max<size_t>(2 * ((bytes + 15) & ~(size_t)15), 1 << 16);
+    if (cudaMallocHost(&s.h, ncap) != cudaSuccess) return fail(MB_ENOMEM, "pinned staging alloc");
+    s.cap = ncap;
+  }
+  memcpy(s.h + s.used, src, bytes);
+  CUDA_TRY(cudaMemcpyAsync(dst, s.h + s.used, bytes, cudaMemcpyHostToDevice, st));
+  s.used += (bytes + 15) & ~(size_t)15;
+  return MB_OK;
+}
+static int stage_end(mb_ctx* c, cudaStream_t st) {
+  auto& s = c->stage[c->stage_i];
+  if (!s.used) return MB_OK;
+  if (!s.ev) CUDA_TRY(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(s.ev, st));
+  s.pending = true;
+  return MB_OK;
+}
 
 // grow-only device scratch
 template <class T>
@@ -365,6 +423,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
 static int family_key(const PatDev& d) {
   if (d.family == MB_FAM_SWAR) return (int)(10 + d.m);
   if (d.family == MB_FAM_SHIFTOR) return d.m <= 32 ? 20 : 21;
+  if (d.family == MB_FAM_ALIGNED) return 30 + d.nw;
   return d.family;
 }
 
@@ -377,7 +436,10 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
       if (d.m == 2) return launch_group<FiltSWAR<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
       return launch_group<FiltSWAR<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
     case MB_FAM_WIN4: return launch_group<FiltWIN4>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
-    case MB_FAM_ALIGNED: return launch_group<FiltALIGNED>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+    case MB_FAM_ALIGNED:
+      if (d.nw == 3) return launch_group<FiltALIGNED<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+      if (d.nw == 2) return launch_group<FiltALIGNED<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+      return launch_group<FiltALIGNED<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
     case MB_FAM_SAMPLED: return launch_group<SampledTag>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
     case MB_FAM_SHIFTOR: {
       int64_t maxm = 0;
@@ -389,16 +451,21 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
   return fail(MB_EINVAL, "unknown kernel family");
 }
 
-// MP eligibility (K5): a batch of >= 8 anchor-filter (ALIGNED) patterns whose
-// pooled anchors stay selective.  `rate` is the expected number of gram hits
-// per text word, sum over patterns k and j of prod_i p(G_kj[i]), with byte
-// probabilities p estimated from all pattern bytes of the batch (patterns are
-// drawn from the text); MP runs when rate <= 0.05.
+// MP eligibility (K5): a batch of >= 8 patterns of length >= 7 (any family:
+// the pass uses each plan's mpG grams) whose pooled anchors stay selective.
+// `rate` is the expected number of gram hits per text word, sum over patterns
+// k and j of prod_i p(mpG_kj[i]), with byte probabilities p estimated from all
+// pattern bytes of the batch (patterns are drawn from the text); MP runs when
+// rate <= 0.05.  A batch of sampled-filter (K3) patterns alone reads ~1/S of
+// the text per pattern, so it takes the pass only from 64 patterns on.
 static bool mp_eligible(const PatDev* h_pats, const double* rate, int K) {
   if (!rate || K < 8 || K > MP_CHUNK * MAX_GROUPS || *rate > 0.05) return false;
-  for (int k = 0; k < K; k++)
-    if (h_pats[k].family != MB_FAM_ALIGNED) return false;
-  return true;
+  bool all_sampled = true;
+  for (int k = 0; k < K; k++) {
+    if (h_pats[k].m < 7) return false;
+    all_sampled &= h_pats[k].family == MB_FAM_SAMPLED;
+  }
+  return !all_sampled || K >= 64;
 }
 
 // Host-built MP tables for patterns [k0, k0 + kc): bloom, bucket starts, entries.
@@ -414,7 +481,7 @@ static void mp_tables(const PatDev* h_pats, int k0, int kc, int* Bout, std::vect
   std::vector<uint32_t> cnt(nb, 0);
   for (int i = 0; i < kc; i++)
     for (int j = 0; j < 4; j++) {
-      const uint32_t h = h_pats[k0 + i].G[j] * 0x9E3779B1u;
+      const uint32_t h = h_pats[k0 + i].mpG[j] * 0x9E3779B1u;
       bloom[h >> 21] |= 1u << ((h >> 16) & 31);
       cnt[h >> (32 - B)]++;
     }
@@ -423,11 +490,11 @@ static void mp_tables(const PatDev* h_pats, int k0, int kc, int* Bout, std::vect
   uint32_t* ents = bstart + bs_words;
   for (int i = 0; i < kc; i++)
     for (int j = 0; j < 4; j++) {
-      const uint32_t g = h_pats[k0 + i].G[j];
+      const uint32_t g = h_pats[k0 + i].mpG[j];
       const uint32_t b = (g * 0x9E3779B1u) >> (32 - B);
       const uint32_t e = fill[b]++;
       ents[2 * e] = g;
-      ents[2 * e + 1] = ((uint32_t)i << 16) | (uint32_t)(h_pats[k0 + i].anchor + j);
+      ents[2 * e + 1] = ((uint32_t)i << 16) | (uint32_t)(h_pats[k0 + i].mpa + j);
     }
   *Bout = B;
 }
@@ -521,8 +588,13 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     for (int k = 0; k < K; k++) mp_rate += mp_rates[k];
   }
   if (mp_eligible(h_pats, mp_rates ? &mp_rate : nullptr, K)) {
-    int pre = 0, post = 0;
-    for (int k = 0; k < K; k++) pre = std::max(pre, h_pats[k].pre), post = std::max(post, h_pats[k].post);
+    // staged margins for verification around each gram hit: window [x - mpa - 3, x - mpa - 3 + m)
+    int64_t pre64 = 0, post64 = 0;
+    for (int k = 0; k < K; k++) {
+      pre64 = std::max<int64_t>(pre64, h_pats[k].mpa + 3);
+      post64 = std::max<int64_t>(post64, h_pats[k].m - h_pats[k].mpa + 8);
+    }
+    const int pre = (int)((pre64 + 15) & ~15LL), post = (int)((post64 + 15) & ~15LL) + 16;
     MPParams M;
     memset(&M, 0, sizeof(M));
     M.text = P.text;
@@ -558,7 +630,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
         c->h_mp.insert(c->h_mp.end(), img.begin(), img.end());
         while (c->h_mp.size() % 4) c->h_mp.push_back(0);
       }
-      CUDA_TRY(cudaMemcpyAsync(c->mp_tab, c->h_mp.data(), sizeof(uint32_t) * c->h_mp.size(), cudaMemcpyHostToDevice, st));
+      if ((rc = stage_upload(c, c->mp_tab, c->h_mp.data(), sizeof(uint32_t) * c->h_mp.size(), st))) return rc;
       tab = c->mp_tab;
     }
     static std::mutex mu_mp;
@@ -582,8 +654,18 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       M.kbase = k0;
       M.ticket = c->ticket + TICKET_MP0 + ci;
       const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * M.stage_bytes + 8192 + 4 * bs_words + 8 * M.nents;
+      static std::mutex mu_occ;
+      static size_t occ_smem = 0;
+      static int occ_val = 0;
       int per_sm = 0;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mp_scan_kernel, NT + 32, smem));
+      {
+        std::lock_guard<std::mutex> g(mu_occ);
+        if (occ_smem != smem) {
+          CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val, mp_scan_kernel, NT + 32, smem));
+          occ_smem = smem;
+        }
+        per_sm = occ_val;
+      }
       if (per_sm < 1) return fail(MB_ECUDA, "MP kernel does not fit on an SM");
       const int64_t grid = std::min<int64_t>(M.ntiles_text, (int64_t)c->nsm * per_sm);
       mp_scan_kernel<<<(int)grid, NT + 32, smem, st>>>(M);
@@ -618,7 +700,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     if ((rc = grow(&c->plist, &c->plist_cap, K, "family index lists"))) return rc;
     c->h_plist.clear();
     for (auto& g : groups) c->h_plist.insert(c->h_plist.end(), g.begin(), g.end());
-    CUDA_TRY(cudaMemcpyAsync(c->plist, c->h_plist.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, st));
+    if ((rc = stage_upload(c, c->plist, c->h_plist.data(), sizeof(int32_t) * K, st))) return rc;
     int base = 0;
     for (size_t g = 0; g < groups.size(); g++) {
       if ((rc = launch_family(c, P, h_pats, groups[g].data(), c->plist + base, (int)groups[g].size(), (int)g, st)))
@@ -644,7 +726,10 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
   const PatDev* dd = nullptr;
   int rc = plan_device(p, &dd);
   if (rc) return rc;
-  return run_search(c, dd, &p->dview, 1, d_text, n, d_out, cap, d_count, st);
+  if ((rc = stage_begin(c))) return rc;
+  rc = run_search(c, dd, &p->dview, 1, d_text, n, d_out, cap, d_count, st);
+  const int rc2 = stage_end(c, st);
+  return rc ? rc : rc2;
 }
 
 // per-pattern expected pooled-gram hits per text word (K5 MP eligibility),
@@ -658,11 +743,11 @@ static void batch_rates(const mb_plan* const* plans, const PatDev* h_pats, int K
     for (size_t i = 0; i < lim; i++) hist[pb[i]] += 1, tot += 1;
   }
   for (int k = 0; k < K; k++)
-    if (h_pats[k].family == MB_FAM_ALIGNED) {
+    if (h_pats[k].m >= 7) {
       double r = 0;
       for (int j = 0; j < 4; j++) {
         double pr = 1;
-        for (int i = 0; i < 4; i++) pr *= hist[(h_pats[k].G[j] >> (8 * i)) & 0xFF] / tot;
+        for (int i = 0; i < 4; i++) pr *= hist[(h_pats[k].mpG[j] >> (8 * i)) & 0xFF] / tot;
         r += pr;
       }
       (*rates)[k] = r;
@@ -676,11 +761,15 @@ static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, cons
                      const uint8_t* d_text, int64_t n, int64_t* d_out, int64_t cap, int64_t* d_offsets, cudaStream_t st,
                      const uint32_t* mp_dev, const std::pair<int64_t, int>* mp_chunks) {
   CUDA_TRY(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
-  size_t free_b = 0, total_b = 0;
-  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-  double budget = std::min<double>((double)free_b / 3.0, 16.0 * (1ULL << 30));
-  if (const char* env = getenv("MB_SCRATCH_BUDGET")) budget = atof(env);  // tests force sub-batching
   const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 338.0;
+  double budget = 1.0 * (1ULL << 30);  // batches needing <= 1 GiB of scratch skip the memory query
+  if (const char* env = getenv("MB_SCRATCH_BUDGET")) {
+    budget = atof(env);  // tests force sub-batching
+  } else if (per_pattern * K > budget) {
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    budget = std::max(budget, std::min<double>((double)free_b / 3.0, 16.0 * (1ULL << 30)));
+  }
   int kc = (int)std::max<double>(1.0, std::min<double>((double)K, budget / per_pattern));
   if (kc < K && kc >= MP_CHUNK) kc -= kc % MP_CHUNK;  // keep prepared MP tables aligned to sub-batches
   for (int k0 = 0; k0 < K; k0 += kc) {
@@ -709,10 +798,13 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
   }
   int rc;
   if ((rc = grow(&c->d_pats, &c->pats_cap, K, "batch params"))) return rc;
-  CUDA_TRY(cudaMemcpyAsync(c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice, st));
+  if ((rc = stage_begin(c))) return rc;
+  if ((rc = stage_upload(c, c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, st))) return rc;
   batch_rates(plans, c->h_pats.data(), K, &c->h_rate);
-  return run_batch(c, c->d_pats, c->h_pats.data(), c->h_rate.data(), K, d_text, n, d_out, cap, d_offsets, st, nullptr,
-                   nullptr);
+  rc = run_batch(c, c->d_pats, c->h_pats.data(), c->h_rate.data(), K, d_text, n, d_out, cap, d_offsets, st, nullptr,
+                 nullptr);
+  const int rc2 = stage_end(c, st);
+  return rc ? rc : rc2;
 }
 
 int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out) {
@@ -733,9 +825,9 @@ int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out) {
   cudaGetDevice(&b->device);
   batch_rates(plans, b->h_pats.data(), K, &b->rates);
   std::vector<uint32_t> img;
-  bool all_aligned = true;
-  for (int k = 0; k < K; k++) all_aligned &= b->h_pats[k].family == MB_FAM_ALIGNED;
-  if (all_aligned && K >= 8)
+  bool all_long = true;  // every pattern has K5 grams (m >= 7)
+  for (int k = 0; k < K; k++) all_long &= b->h_pats[k].m >= 7;
+  if (all_long && K >= 8)
     for (int k0 = 0; k0 < K; k0 += MP_CHUNK) {
       std::vector<uint32_t> one;
       int B = 0;
@@ -777,8 +869,12 @@ int mb_find_batch_prepared(mb_ctx* c, const mb_batch* b, const uint8_t* d_text, 
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   if (dev != b->device) return fail(MB_EINVAL, "batch was prepared on another device");
-  return run_batch(c, b->d_pats, b->h_pats.data(), b->rates.data(), b->K, d_text, n, d_out, cap, d_offsets,
-                   (cudaStream_t)stream, b->d_mp, b->mp_chunks.empty() ? nullptr : b->mp_chunks.data());
+  int rc = stage_begin(c);
+  if (rc) return rc;
+  rc = run_batch(c, b->d_pats, b->h_pats.data(), b->rates.data(), b->K, d_text, n, d_out, cap, d_offsets,
+                 (cudaStream_t)stream, b->d_mp, b->mp_chunks.empty() ? nullptr : b->mp_chunks.data());
+  const int rc2 = stage_end(c, (cudaStream_t)stream);
+  return rc ? rc : rc2;
 }
 
 int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, void* stream) {

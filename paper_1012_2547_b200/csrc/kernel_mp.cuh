@@ -5,15 +5,16 @@
 namespace mb {
 
 // ------------------------------------------------ kernel 1c: batched multi-pattern pass (K5 "MP")
-// One TMA pass over the text serves a whole batch of anchor-filter (K1
-// ALIGNED) patterns: each 4-aligned text word X is hashed once; a bloom bit
-// test in smem rejects almost every word, and a hit walks the bucket of
-// {gram, pattern, anchor+j} entries.  A verified occurrence (k, s) maps to the
-// same bitmap bit b = s + off + a_k + 3 as the single-pattern ALIGNED plan, so
-// it lands in the consumer's own segment of pattern k's segment layout: one
-// 16-bit atomic count and an (unordered) list slot; offsets/expand are shared
-// (expand sorts MP lists).  Segments above LIST_CAP set `overflow` and the
-// host re-runs the batch through the per-pattern path.
+// One TMA pass over the text serves a whole batch: each 4-aligned text word X
+// is hashed once; a bloom bit test in smem rejects almost every word, and a
+// hit walks the bucket of {gram, pattern, mpa+j} entries (every plan with
+// m >= 7 carries one-word anchor grams mpG for this pass, whatever its own
+// family).  A verified occurrence (k, s) is recorded at pattern k's own bitmap
+// bit b = s + off + delta_k -- the bit its family's scan would set -- in the
+// segment holding b (usually this warp's; a far delta puts it in another
+// segment or tile): one 16-bit atomic count and an (unordered) list slot;
+// offsets/expand are shared (expand sorts MP lists).  Segments above LIST_CAP
+// set `overflow` and the per-pattern scans re-run the batch on the device.
 __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
   StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
@@ -104,14 +105,16 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
           bool ok = true;
           for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);
           if (!ok) continue;
-          // same bit as the single-pattern ALIGNED plan: b = sv + a + 3 -> this lane's chunk
+          // the family scan's bit for start sv: b = sv + delta (virtual, off included)
           const int64_t b = sv + pd->delta;
-          const int64_t g = ((int64_t)(P.kbase + kl) * P.ntiles + tau) * NWARP + warp;
+          const int64_t tb = b / TILE;
+          MB_CHECK(b >= 0 && tb < P.ntiles);
+          const int64_t g = ((int64_t)(P.kbase + kl) * P.ntiles + tb) * NWARP + (b - tb * TILE) / SEG;
           unsigned int* wptr = reinterpret_cast<unsigned int*>(P.counts) + (g >> 1);
           const unsigned int sh = 16u * (unsigned)(g & 1);
           const unsigned int old = (atomicAdd(wptr, 1u << sh) >> sh) & 0xFFFFu;
           if (old < (unsigned)LIST_CAP)
-            P.lists[g * LIST_CAP + old] = (uint16_t)(b - B0);
+            P.lists[g * LIST_CAP + old] = (uint16_t)(b - tb * TILE);
           else
             atomicExch(P.overflow, 1u);
         }

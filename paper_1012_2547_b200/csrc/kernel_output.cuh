@@ -10,8 +10,9 @@ namespace mb {
 // chunks already running -- the decoupled look-back never stalls on a queued
 // predecessor.
 template <int PER>  // counts per thread: chunk = NT * PER (host picks PER for >= 2 chunks per SM)
-__global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
+__global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   __shared__ int64_t wsum[NWARP];
+  __shared__ uint32_t s_cnt[PER / 2 * NT];
   __shared__ int64_t s_excl;
   __shared__ int64_t s_chunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -21,21 +22,23 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   const int64_t nseg = P.total_tiles * NWARP;
   const int64_t base = ch * (int64_t)(NT * PER);
   static_assert(PER % 8 == 0, "vector loads of 8 uint16 counts");
-  uint32_t v[PER];
-  int64_t tsum = 0;
+  // PER uint16 counts kept packed two per register (2 CTAs per SM fit)
+  uint32_t v2[PER / 2];
+  uint32_t tsum32 = 0;
   const uint4* cv = reinterpret_cast<const uint4*>(P.counts + base + (int64_t)tid * PER);
 #pragma unroll
   for (int q8 = 0; q8 < PER / 8; q8++) {
     const uint4 x = cv[q8];  // counts are allocated to a whole number of chunks
-    const uint32_t wds[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-    for (int h = 0; h < 8; h++) {
-      const int q = 8 * q8 + h;
-      const int64_t t = base + (int64_t)tid * PER + q;
-      v[q] = t < nseg ? ((wds[h >> 1] >> (16 * (h & 1))) & 0xFFFFu) : 0u;
-      tsum += v[q];
-    }
+    v2[4 * q8] = x.x, v2[4 * q8 + 1] = x.y, v2[4 * q8 + 2] = x.z, v2[4 * q8 + 3] = x.w;
   }
+  if (base + (int64_t)NT * PER > nseg) {  // last chunk: zero the slots past the last segment
+#pragma unroll
+    for (int q = 0; q < PER; q++)
+      if (base + (int64_t)tid * PER + q >= nseg) v2[q >> 1] &= (q & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+  }
+#pragma unroll
+  for (int h = 0; h < PER / 2; h++) tsum32 += (v2[h] & 0xFFFFu) + (v2[h] >> 16);
+  const int64_t tsum = tsum32;
   int64_t inc = tsum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -91,18 +94,28 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
   __syncthreads();
   int64_t run = s_excl + wbefore + inc - tsum;
   const int64_t seg_per_pat = P.ntiles * NWARP;
-  // Sorted sparse segments (<= LIST_CAP uint16 offsets) are expanded right here,
-  // their offsets never leave registers; dense or unsorted (MP) segments are
-  // queued for expand_kernel with their offset.
+  // Sorted sparse segments (<= LIST_CAP uint16 offsets) are expanded right here;
+  // dense or unsorted (MP) segments are queued for expand_kernel with their offset.
   const bool fuse = P.out && !P.unsorted_lists;
   int cur_k = -1;
   int64_t shift = 0;
+  // pattern of this thread's first segment and the segment's rank within it
+  // (one division per thread; the CSR end is written at rank seg_per_pat - 1)
+  int64_t kq = (base + (int64_t)tid * PER) / seg_per_pat;
+  int64_t rem = base + (int64_t)tid * PER - kq * seg_per_pat;
+  // the counts go through shared memory (transposed: conflict-free) so the
+  // output loop below is not unrolled and the kernel stays at 2 CTAs per SM
 #pragma unroll
+  for (int h = 0; h < PER / 2; h++) s_cnt[h * NT + tid] = v2[h];
+  // nothing to emit and no pattern ends in this thread's range: done
+  if (tsum == 0 && rem + PER < seg_per_pat) return;
+#pragma unroll 1
   for (int q = 0; q < PER; q++) {
     const int64_t t = base + (int64_t)tid * PER + q;
+    const uint32_t vq = (s_cnt[(q >> 1) * NT + tid] >> (16 * (q & 1))) & 0xFFFFu;
     if (t < nseg) {
-      if (v[q] && P.out) {
-        if (fuse && v[q] <= (uint32_t)LIST_CAP) {
+      if (vq && P.out) {
+        if (fuse && vq <= (uint32_t)LIST_CAP) {
           const int64_t tile = t / NWARP;
           const int k = (int)(tile / P.ntiles);
           if (k != cur_k) {
@@ -111,7 +124,7 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
           }
           const int64_t pos0 = (tile % P.ntiles) * TILE - shift;
           const uint16_t* L = P.lists + t * LIST_CAP;
-          for (uint32_t e = 0; e < v[q]; e++)
+          for (uint32_t e = 0; e < vq; e++)
             if (run + e < P.cap) P.out[run + e] = pos0 + L[e];
         } else {
           P.toff[t] = run;
@@ -119,9 +132,10 @@ __global__ void __launch_bounds__(NT) offsets_kernel(const ScanParams P) {
           P.seglist[slot] = t;
         }
       }
-      if (t % seg_per_pat == seg_per_pat - 1) P.offsets_plus1[t / seg_per_pat] = run + v[q];
+      if (rem == seg_per_pat - 1) P.offsets_plus1[kq] = run + vq;
     }
-    run += v[q];
+    run += vq;
+    if (++rem == seg_per_pat) rem = 0, kq++;
   }
 }
 
@@ -182,23 +196,21 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
       const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31);
       const uint32_t ea = ia - pa, eb = ta + ib - pb;
       const uint32_t below = (1u << lane) - 1u;
-#pragma unroll 4
+      // 32-bit ranks against the room left in the output (o < cap checked above)
+      const uint32_t lim = (uint32_t)(P.cap - o < (int64_t)SEG ? P.cap - o : (int64_t)SEG);
+      int64_t* const dst = P.out + o;
+      const int64_t v0 = segpos + lane;
+#pragma unroll 8
       for (int w = 0; w < 32; w++) {
         const uint32_t x = __shfl_sync(0xffffffffu, xa, w);
-        const uint32_t e = __shfl_sync(0xffffffffu, ea, w);
-        if ((x >> lane) & 1u) {
-          const int64_t idx = o + e + __popc(x & below);
-          if (idx < P.cap) P.out[idx] = segpos + 32 * w + lane;
-        }
+        const uint32_t r = __shfl_sync(0xffffffffu, ea, w) + __popc(x & below);
+        st_if((((x >> lane) & 1u) != 0) & (r < lim), dst + r, v0 + 32 * w);
       }
-#pragma unroll 4
+#pragma unroll 8
       for (int w = 0; w < 32; w++) {
         const uint32_t x = __shfl_sync(0xffffffffu, xb, w);
-        const uint32_t e = __shfl_sync(0xffffffffu, eb, w);
-        if ((x >> lane) & 1u) {
-          const int64_t idx = o + e + __popc(x & below);
-          if (idx < P.cap) P.out[idx] = segpos + 32 * (32 + w) + lane;
-        }
+        const uint32_t r = __shfl_sync(0xffffffffu, eb, w) + __popc(x & below);
+        st_if((((x >> lane) & 1u) != 0) & (r < lim), dst + r, v0 + 32 * (32 + w));
       }
     }
   }

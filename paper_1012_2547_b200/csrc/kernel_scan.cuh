@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
     const uint8_t* const sbeg = spat + P.pat_cap;  // staged text window [sbeg, send)
     const uint8_t* const send = spat + P.stage_bytes;
     (void)sbeg, (void)send;
-    MB_CHECK(S + c0 + SEG + 4 <= send);
+    MB_CHECK(S + c0 + SEG + 8 <= send);
     const int64_t segb = B0 + c0;
     const bool interior = segb >= blo && segb + SEG - 1 <= bhi;
 
@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
       for (int r = 0; r < SEG / 512; r++) {
         const int c = c0 + r * 512 + lane * 16;
         const uint4 X = *reinterpret_cast<const uint4*>(S + c);
-        const uint32_t w[5] = {X.x, X.y, X.z, X.w, *reinterpret_cast<const uint32_t*>(S + c + 16)};
+        const uint2 Y = *reinterpret_cast<const uint2*>(S + c + 16);
+        const uint32_t w[6] = {X.x, X.y, X.z, X.w, Y.x, Y.y};
         mk[r] = Filt::run(w, pd);
         anyc |= (mk[r] != 0);
       }
@@ -181,18 +182,33 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
               while (cc) {
                 const int i = __ffsll((long long)cc) - 1;
                 cc &= cc - 1;
-                MB_CHECK(Y0 + c0 + q0 + i >= sbeg && Y0 + c0 + q0 + i + pd.per <= send);
+                MB_CHECK(Y0 + c0 + q0 + i >= sbeg && Y0 + c0 + q0 + i + pd.per + 4 <= send);
                 if (!verify_direct(Y0 + c0 + q0 + i, spat, pd.per)) cand &= ~(1ULL << i);
               }
             }
           }
           w0 = (uint32_t)cand;
           w1 = (uint32_t)(cand >> 32);
-        } else if (pd.m >= 64 && __reduce_add_sync(0xffffffffu, __popc(w0) + __popc(w1)) <= 32) {
-          // long windows, few candidates: the whole warp verifies one candidate
-          // at a time, lane l comparing 4-byte words l, l+32, ... (smem text vs
-          // pattern).  Dense candidates (small alphabets) stay lane-parallel.
-          const uint64_t mine = ((uint64_t)w1 << 32) | w0;
+        } else if (pd.m >= 64) {
+          // long windows: each lane rejects its candidates on the first 16
+          // bytes; the survivors (rare unless the window really matches) are
+          // verified by the whole warp one at a time, lane l comparing 4-byte
+          // words l, l+32, ... -- long partial matches cost m/128 steps, not m/4
+          uint64_t mine = ((uint64_t)w1 << 32) | w0, surv = 0;
+          {
+            const uint4 p16 = *reinterpret_cast<const uint4*>(spat);
+            uint64_t cc = mine;
+            while (cc) {
+              const int i = __ffsll((long long)cc) - 1;
+              cc &= cc - 1;
+              const uint8_t* tw = Y0 + c0 + 64 * lane + i;
+              MB_CHECK(tw >= sbeg && tw + 24 <= send);
+              if (lds32u(tw) == p16.x && lds32u(tw + 4) == p16.y && lds32u(tw + 8) == p16.z &&
+                  lds32u(tw + 12) == p16.w)
+                surv |= 1ULL << i;
+            }
+          }
+          mine = surv;
           uint64_t keep = 0;
           uint32_t active = __ballot_sync(0xffffffffu, mine != 0);
           while (active) {
@@ -204,9 +220,9 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
               const int i = __ffsll((long long)cm) - 1;
               cm &= cm - 1;
               const uint8_t* tw = Y0 + c0 + 64 * src + i;
-              MB_CHECK(tw >= sbeg && tw + pd.m + 8 <= send);
+              MB_CHECK(tw >= sbeg && tw + pd.m + 8 <= send);  // lds32u reads up to tw + k + 8
               bool bad = false;
-              for (int k = 4 * lane; k < pd.m; k += 128) {
+              for (int k = 16 + 4 * lane; k < pd.m; k += 128) {
                 const uint32_t pw = *reinterpret_cast<const uint32_t*>(spat + k);
                 uint32_t diff = lds32u(tw + k) ^ pw;
                 if (pd.m - k < 4) diff &= (1u << (8 * (pd.m - k))) - 1u;
@@ -225,7 +241,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
             while (cw) {
               const int i = __ffs(cw) - 1;
               cw &= cw - 1;
-              MB_CHECK(Y0 + c0 + 32 * (2 * lane + h) + i >= sbeg && Y0 + c0 + 32 * (2 * lane + h) + i + pd.m <= send);
+              MB_CHECK(Y0 + c0 + 32 * (2 * lane + h) + i >= sbeg && Y0 + c0 + 32 * (2 * lane + h) + i + pd.m + 4 <= send);
               if (verify_direct(Y0 + c0 + 32 * (2 * lane + h) + i, spat, (int)pd.m)) mw |= 1u << i;
             }
             ws[h] = mw;

@@ -66,6 +66,15 @@ static inline uint32_t load_le32(const uint8_t* p) {
 // exact, tested family selectable through mb_plan_opts.family.
 constexpr double K2_MAX_ENTROPY = -1.0;
 
+// ALIGNED anchor-word thresholds (expected one-/two-word anchor hits per text
+// word above which one more word is added); tuned on config 2.
+#ifndef MB_ALIGNED2_RATE
+#define MB_ALIGNED2_RATE 4e-3
+#endif
+#ifndef MB_ALIGNED3_RATE
+#define MB_ALIGNED3_RATE 5e-2
+#endif
+
 static inline int round16(int64_t x) { return (int)((x + 15) & ~(int64_t)15); }
 
 
@@ -134,7 +143,8 @@ static bool build_sampled(const uint8_t* pat, int64_t m, PlanHost* ph) {
 
 // Filter-rate model: expected anchor hits per aligned text word, with byte
 // probabilities from the caller's text histogram or, as a proxy, the
-// pattern's own (smoothed) byte counts.
+// pattern's own byte counts, lightly smoothed (1.28 pseudo-counts spread over
+// all 256 bytes: heavier smoothing hides a small alphabet from short patterns).
 static void byte_probs(const uint8_t* p, int64_t m, const int64_t* hist, double* pr) {
   if (hist) {
     double tot = 0;
@@ -143,21 +153,40 @@ static void byte_probs(const uint8_t* p, int64_t m, const int64_t* hist, double*
   } else {
     double cnt[256] = {0};
     for (int64_t i = 0; i < m; i++) cnt[p[i]] += 1;
-    for (int c = 0; c < 256; c++) pr[c] = (cnt[c] + 0.05) / ((double)m + 12.8);
+    for (int c = 0; c < 256; c++) pr[c] = (cnt[c] + 0.005) / ((double)m + 1.28);
   }
 }
 static double gram_prob(const uint8_t* g, const double* pr) { return pr[g[0]] * pr[g[1]] * pr[g[2]] * pr[g[3]]; }
 
-// ALIGNED: the 7-byte window minimising sum_j P(p[a+j..a+j+4)), j = 0..3.
-static int best_aligned(const uint8_t* p, int64_t m, const double* pr, double* rate) {
+// ALIGNED with nw anchor words: the (4 nw + 3)-byte window minimising
+// sum_j prod_w P(p[a+j+4w .. +4)), j = 0..3 (a word k of the text is a
+// candidate when words k, k+1, .., k+nw-1 all equal their grams).
+static int best_aligned(const uint8_t* p, int64_t m, const double* pr, int nw, double* rate) {
   int best = 0;
   double br = 1e300;
-  for (int64_t a = 0; a + 7 <= m; a++) {
-    const double r = gram_prob(p + a, pr) + gram_prob(p + a + 1, pr) + gram_prob(p + a + 2, pr) + gram_prob(p + a + 3, pr);
+  for (int64_t a = 0; a + 4 * nw + 3 <= m; a++) {
+    double r = 0;
+    for (int j = 0; j < 4; j++) {
+      double g = 1;
+      for (int w = 0; w < nw; w++) g *= gram_prob(p + a + j + 4 * w, pr);
+      r += g;
+    }
     if (r < br * (1 - 1e-12)) br = r, best = (int)a;
   }
   *rate = br;
   return best;
+}
+// Anchor words for ALIGNED: one more word doubles the filter's compares but
+// divides the candidate rate by ~P(gram); worth it once the one-word filter
+// would send most segments down the verify path (small alphabets).
+static int choose_aligned_words(const uint8_t* p, int64_t m, const double* pr) {
+  double r1, r2, r3;
+  best_aligned(p, m, pr, 1, &r1);
+  if (m < 11 || r1 < MB_ALIGNED2_RATE) return 1;
+  best_aligned(p, m, pr, 2, &r2);
+  if (m < 15 || r2 < MB_ALIGNED3_RATE) return 2;
+  best_aligned(p, m, pr, 3, &r3);
+  return r3 < r2 ? 3 : 2;
 }
 // WIN4: one 4-byte window tested at all 4 byte phases of a word: 4 * P(gram).
 static int best_win4(const uint8_t* p, int64_t m, const double* pr, double* rate) {
@@ -228,10 +257,17 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
     // (a^(m-1)b: 'aaab' vs three 'aaaa' grams) WIN4 is far more selective.
     double pr[256], ra, rw;
     byte_probs(pat, m, hist, pr);
-    best_aligned(pat, m, pr, &ra);
-    best_win4(pat, m, pr, &rw);
-    // only where ALIGNED would actually be busy (> 1 hit per 1000 words)
-    if (ra > 1e-3 && 8 * rw < ra && !(m >= 16 && ph->period <= m / 2)) fam = MB_FAM_WIN4;
+    const int nw = (opts && opts->anchor_words) ? opts->anchor_words : choose_aligned_words(pat, m, pr);
+    // only where ALIGNED would actually be busy (> 1 hit per 1000 words); an
+    // invalid forced anchor_words is left for the ALIGNED case to reject
+    if (nw >= 1 && nw <= 3 && 4 * nw + 3 <= m) {
+      best_aligned(pat, m, pr, nw, &ra);
+      best_win4(pat, m, pr, &rw);
+      // WIN4 must win by 8x over the cheap one-word filter, by 2x over the
+      // wider (costlier) multi-word ones
+      const double margin = nw == 1 ? 8.0 : 2.0;
+      if (ra > 1e-3 && margin * rw < ra && !(m >= 16 && ph->period <= m / 2)) fam = MB_FAM_WIN4;
+    }
   }
   if (opts && opts->family == MB_FAM_SAMPLED && !sampled_ok) {
     *err = "sampled q-gram family does not apply to this pattern (m < 272, low entropy or periodic)";
@@ -276,10 +312,18 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
     case MB_FAM_ALIGNED: {
       double pr[256], ra;
       byte_probs(pat, m, hist, pr);
-      int a = best_aligned(pat, m, pr, &ra);
+      const bool per_verify = m >= 16 && ph->period <= m / 2;  // periodic: break-run test (below) does the work
+      int nw = (opts && opts->anchor_words) ? opts->anchor_words : per_verify ? 1 : choose_aligned_words(pat, m, pr);
+      if (nw < 1 || nw > 3 || 4 * nw + 3 > m) {
+        *err = "anchor_words must be 1..3 with 4 * anchor_words + 3 <= m";
+        return MB_EINVAL;
+      }
+      int a = best_aligned(pat, m, pr, nw, &ra);
       ph->anchor = a;
+      d.nw = nw;
       d.delta = a + 3;
-      for (int j = 0; j < 4; j++) d.G[j] = load_le32(pat + a + j);
+      for (int w = 0; w < nw; w++)
+        for (int j = 0; j < 4; j++) d.G[4 * w + j] = load_le32(pat + a + j + 4 * w);
       d.exact = 0;
       // Long periodic patterns (a^m, (ab)^k ...) verify through the period /
       // break-run test so dense matches cost O(1) each.
@@ -307,6 +351,14 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       break;
   }
   d.anchor = ph->anchor;
+  // K5 (batched multi-pattern pass) grams: the one-word ALIGNED anchor, for
+  // every pattern long enough, so any family can join a batched pass
+  if (m >= 7) {
+    double pr[256], r1;
+    byte_probs(pat, m, hist, pr);
+    d.mpa = best_aligned(pat, m, pr, 1, &r1);
+    for (int j = 0; j < 4; j++) d.mpG[j] = load_le32(pat + d.mpa + j);
+  }
   // staged-tile margins (bytes before / after the tile's bit range)
   d.pre = round16(d.delta);
   d.post = round16(m - d.delta + 40) + 16;

@@ -27,12 +27,14 @@ struct PatDev {
   int32_t exact;    // filter alone decides (no verification)
   int32_t pre;      // staged bytes before the tile's first bit (multiple of 16)
   int32_t post;     // staged bytes after the tile's last bit (multiple of 16)
-  uint32_t G[4];    // filter words (family specific)
+  uint32_t G[12];   // filter words (family specific); ALIGNED: G[4w + j] = p[a+j+4w .. +4)
   // K3 sampled q-gram filter (family MB_FAM_SAMPLED)
   int32_t S;        // sampling stride in bytes (multiple of 16, >= 256)
   int32_t q;        // gram bytes (4, 8, 16 or 32)
   int32_t B;        // log2 of the bucket count
-  int32_t pad_;
+  int32_t nw;       // ALIGNED: anchor words (window 4 nw + 3 bytes), 1..3
+  int32_t mpa;      // K5 batched pass: 7-byte anchor window offset (m >= 7), whatever the family
+  uint32_t mpG[4];  // K5 grams p[mpa+j .. mpa+j+4), j = 0..3
   const uint32_t* bloom;   // 65536-bit filter over gram hashes (device)
   const uint16_t* bstart;  // (1 << B) + 1 bucket starts (device)
   const uint16_t* bent;    // S entries: pattern offsets j sorted by bucket (device)

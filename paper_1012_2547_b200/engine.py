@@ -42,13 +42,13 @@ class EngineError(RuntimeError):
 
 class _PlanOpts(ctypes.Structure):
     _fields_ = [("family", ctypes.c_int), ("sigma_hint", ctypes.c_int),
-                ("hist", ctypes.POINTER(ctypes.c_int64))]
+                ("hist", ctypes.POINTER(ctypes.c_int64)), ("anchor_words", ctypes.c_int)]
 
 
 class _PlanInfo(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int64), ("family", ctypes.c_int), ("anchor", ctypes.c_int),
                 ("delta", ctypes.c_int), ("period", ctypes.c_int), ("periodic", ctypes.c_int),
-                ("stride", ctypes.c_int), ("gram", ctypes.c_int)]
+                ("stride", ctypes.c_int), ("gram", ctypes.c_int), ("words", ctypes.c_int)]
 
 
 _lib = None
@@ -146,6 +146,7 @@ class PlanInfo:
     periodic: bool
     stride: int = 0  # K3 sampling stride (bytes)
     gram: int = 0    # K3 gram length (bytes)
+    words: int = 0   # ALIGNED anchor words (window 4 * words + 3 bytes)
 
 
 class Plan:
@@ -154,7 +155,7 @@ class Plan:
 
     __slots__ = ("_h", "pattern", "m", "__weakref__")
 
-    def __init__(self, pattern: bytes, family: str = "auto", hist=None):
+    def __init__(self, pattern: bytes, family: str = "auto", hist=None, anchor_words: int = 0):
         L = load_library()
         p = bytes(pattern)
         if not p:
@@ -162,6 +163,7 @@ class Plan:
         opts = _PlanOpts()
         opts.family = FAMILIES[family]
         opts.sigma_hint = 0
+        opts.anchor_words = int(anchor_words)
         hist_arr = None
         if hist is not None:
             hist_arr = np.ascontiguousarray(np.asarray(hist, dtype=np.int64).reshape(256))
@@ -187,7 +189,7 @@ class Plan:
         i = _PlanInfo()
         _check(load_library().mb_plan_info(self._h, ctypes.byref(i)))
         return PlanInfo(i.m, FAMILY_NAMES.get(i.family, str(i.family)), i.anchor, i.delta, i.period, bool(i.periodic),
-                        i.stride, i.gram)
+                        i.stride, i.gram, i.words)
 
     # -- H1 host tables (bit-identical to the reference's functions) --
     def horspool_table(self) -> list[int]:

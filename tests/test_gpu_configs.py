@@ -64,7 +64,7 @@ def test_config3_full(cuda):
         pats = inputs.config3_patterns(t, m)
         before = engine.mp_batches()
         pos, offs = engine.find_batch([engine.Plan(p) for p in pats], d)
-        if m in (16, 64, 256):
+        if m in (16, 64, 256, 1024):
             assert engine.mp_batches() == before + 1, f"cfg3 m={m} batch did not take the MP pass"
         pos = pos.cpu().numpy()
         offs = offs.numpy()

@@ -18,6 +18,7 @@ from paper_1012_2547_b200 import engine
 
 pytestmark = pytest.mark.gpu
 TILE = 16384
+SEG = 2048
 
 
 def gpu_positions(p: bytes, t, family="auto") -> np.ndarray:
@@ -233,6 +234,36 @@ def test_mp_batched_single_pass(cuda, sigma, m):
     assert engine.mp_batches() == before + 1, "selective ALIGNED batch did not take the MP pass"
     for p, r in zip(pats, res):
         assert r == oracle.search(p, t).tolist(), (len(p), p[:4])
+
+
+def test_mp_mixed_family_batch(cuda):
+    """K5 pass over a batch mixing families (ALIGNED 1/2 words, WIN4, shift-or,
+    sampled with deltas up to S-1 > one segment): every hit lands in its own
+    family's bitmap coordinates, so the CSR equals the oracle per pattern."""
+    rng = np.random.default_rng(2718)
+    n = 5 * TILE + 123
+    t = bytearray(rand_bytes(rng, 256, n))
+    specs = [(24, "auto", 0)] * 100 + [(24, "win4", 0)] * 40 + [(40, "shiftor", 0)] * 20 + \
+            [(64, "auto", 2)] * 10 + [(int(m), "auto", 0) for m in rng.integers(300, 1500, 30)]
+    pats, plans = [], []
+    for m, fam, nw in specs:
+        i = int(rng.integers(0, n - m))
+        p = bytes(t[i : i + m])
+        pats.append(p)
+        plans.append(engine.Plan(p, fam, anchor_words=nw))
+    for s in (0, SEG - 5, TILE - 3, n - len(pats[-1])):  # plant a sampled-family pattern at edges
+        t[s : s + len(pats[-1])] = pats[-1]
+    t = bytes(t)
+    fams = {pl.info().family for pl in plans}
+    assert {"aligned", "win4", "shiftor", "sampled"} <= fams, fams
+    d = torch.from_numpy(np.frombuffer(t, dtype=np.uint8).copy()).cuda()
+    for obj in (plans, engine.Batch(plans)):
+        before = engine.mp_batches()
+        pos, offs = engine.find_batch(obj, d)
+        assert engine.mp_batches() == before + 1, "mixed batch did not take the MP pass"
+        pos = pos.cpu().numpy()
+        for k, p in enumerate(pats):
+            assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(p, t)), (k, len(p))
 
 
 def test_prepared_batch_matches_adhoc(cuda):

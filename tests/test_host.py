@@ -156,6 +156,24 @@ def test_plan_info_families():
         engine.Plan(b"x" * 65, family="shiftor")
 
 
+def test_aligned_anchor_words():
+    """Small alphabets widen the ALIGNED anchor to 2 words (11-byte window);
+    large alphabets keep one word; forced values are validated."""
+    rng = np.random.default_rng(3)
+    for sigma, words in ((2, 2), (4, 2), (64, 1), (256, 1)):
+        p = rng.integers(0, sigma, 64, dtype=np.uint8).tobytes()
+        info = engine.Plan(p).info()
+        assert (info.family, info.words) == ("aligned", words), sigma
+    p = rng.integers(0, 256, 40, dtype=np.uint8).tobytes()
+    for nw in (1, 2, 3):
+        assert engine.Plan(p, anchor_words=nw).info().words == nw
+    with pytest.raises(ValueError):
+        engine.Plan(p[:10], anchor_words=2)   # window 11 > m
+    with pytest.raises(ValueError):
+        engine.Plan(p, anchor_words=4)
+    assert engine.Plan(p[:4]).info().words == 0  # not ALIGNED
+
+
 def test_inputs_mirror_reference_generators():
     rng_bytes = np.random.Generator(np.random.PCG64(7)).integers(0, 4, size=10007, dtype=np.uint8)
     assert np.array_equal(inputs.rand_text_np(4, 10007, 7, chunk=4096), rng_bytes)
