@@ -62,6 +62,11 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// programmatic dependent launch: wait for the preceding grid's results /
+// let the next grid's CTAs be scheduled
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // predicated 8-byte store without a branch (keeps warp-synchronous loops
 // convergent, so the shuffles around it need no divergence checks)
 __device__ __forceinline__ void st_if(bool c, int64_t* p, int64_t v) {

@@ -286,6 +286,24 @@ void mb_ctx_destroy(mb_ctx* c) {
 
 }  // extern "C"
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// before its predecessor in the stream completes and must call pdl_wait()
+// before touching the predecessor's results.
+template <class K>
+static cudaError_t launch_pdl(K kernel, int grid, int block, cudaStream_t st, const ScanParams& P) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, P);
+}
+
 // ---- pinned upload staging (see mb_ctx::stage)
 static int stage_begin(mb_ctx* c) {
   c->stage_i ^= 1;
@@ -564,17 +582,20 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   auto finish = [&](bool unsorted) -> int {
     P.epoch = ++c->epoch;
     P.unsorted_lists = unsorted ? 1 : 0;
+    // programmatic dependent launches: offsets/expand CTAs are scheduled as the
+    // previous grid drains and wait in-kernel (griddepcontrol.wait) for its
+    // results -- the launch gap and the scan's tail overlap
     if (scan_per == 32)
-      offsets_kernel<32><<<(int)nchunks, NT, 0, st>>>(P);
+      CUDA_TRY(launch_pdl(offsets_kernel<32>, (int)nchunks, NT, st, P));
     else if (scan_per == 16)
-      offsets_kernel<16><<<(int)nchunks, NT, 0, st>>>(P);
+      CUDA_TRY(launch_pdl(offsets_kernel<16>, (int)nchunks, NT, st, P));
     else
-      offsets_kernel<8><<<(int)nchunks, NT, 0, st>>>(P);
+      CUDA_TRY(launch_pdl(offsets_kernel<8>, (int)nchunks, NT, st, P));
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     if (d_out && cap > 0) {
       const int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS, (int64_t)c->nsm * 16);
-      expand_kernel<<<(int)eg, EXP_WARPS * 32, 0, st>>>(P);
+      CUDA_TRY(launch_pdl(expand_kernel, (int)eg, EXP_WARPS * 32, st, P));
       g_launches++;
       CUDA_TRY(cudaGetLastError());
     }

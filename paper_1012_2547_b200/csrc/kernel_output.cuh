@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   __shared__ int64_t s_excl;
   __shared__ int64_t s_chunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();  // counts / lists / bitmaps of the count kernel(s)
   if (tid == 0) s_chunk = (int64_t)atomicAdd(&P.ticket[TICKET_OFFSETS], 1ULL);
   __syncthreads();
   const int64_t ch = s_chunk;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
 constexpr int EXP_WARPS = 4;
 __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();  // queue and offsets of offsets_kernel
   const int64_t nq = (int64_t)P.ticket[TICKET_DENSE];
   int cur_k = -1;
   int64_t shift = 0;
