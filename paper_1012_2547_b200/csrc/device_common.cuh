@@ -67,14 +67,6 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// predicated 8-byte store without a branch (keeps warp-synchronous loops
-// convergent, so the shuffles around it need no divergence checks)
-__device__ __forceinline__ void st_if(bool c, int64_t* p, int64_t v) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.global.s64 [%0], %1;\n}" ::"l"(p), "l"(v),
-               "r"((uint32_t)c)
-               : "memory");
-}
-
 // look-back flag word: [epoch:24][status:2][value:38]
 constexpr uint64_t ST_AGG = 1, ST_INCL = 2;
 __device__ __forceinline__ uint64_t pack_state(uint32_t epoch, uint64_t st, uint64_t val) {

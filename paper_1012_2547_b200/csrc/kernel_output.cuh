@@ -142,31 +142,61 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
 
 // ------------------------------------------------ kernel 3: expansion
 // The segments offsets_kernel queued (dense, or MP's unsorted lists), a warp
-// per segment: unsorted lists get a 32-lane bitonic sort, dense segments
-// expand their 64-word bitmap 32 words at a time through a per-warp smem
-// staging buffer so every global store is a coalesced run.
+// per segment, software-pipelined: the queue entry two steps ahead and the
+// count / offset / list / bitmap words one step ahead are in flight while the
+// current segment is written.  Unsorted (MP) lists get a 32-lane bitonic
+// sort; dense segments are staged in smem as uint16 offsets, then streamed out
+// with coalesced 256-byte stores.
 constexpr int EXP_WARPS = 4;
+
+struct ExpSeg {  // one queued segment as a lane holds it
+  int64_t g, o;
+  uint32_t c, lv, xa, xb;
+};
+__device__ __forceinline__ ExpSeg exp_load(const ScanParams& P, int64_t g, int lane) {
+  ExpSeg e;
+  e.g = g;
+  e.c = P.counts[g];
+  e.o = P.toff[g];
+  e.lv = P.lists[g * LIST_CAP + lane];  // meaningful when c <= LIST_CAP
+  e.xa = P.bitmaps[g * SEG_WORDS + lane];  // meaningful when c > LIST_CAP
+  e.xb = P.bitmaps[g * SEG_WORDS + 32 + lane];
+  return e;
+}
+
 __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint16_t s_run[EXP_WARPS][SEG];  // dense segments: staged offsets per warp
+  uint16_t* const sb = s_run[warp];
   pdl_wait();  // queue and offsets of offsets_kernel
   const int64_t nq = (int64_t)P.ticket[TICKET_DENSE];
+  const int64_t stride = (int64_t)gridDim.x * EXP_WARPS;
+  int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp;
+  if (qi >= nq) return;
+  ExpSeg cur = exp_load(P, P.seglist[qi], lane);
+  int64_t g_nxt = qi + stride < nq ? P.seglist[qi + stride] : -1;
   int cur_k = -1;
   int64_t shift = 0;
-  for (int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp; qi < nq; qi += (int64_t)gridDim.x * EXP_WARPS) {
-    {
-      const int64_t g = P.seglist[qi];
-      const uint32_t c = P.counts[g];
-      const int64_t tile = g / NWARP;
-      const int k = (int)(tile / P.ntiles);
-      if (k != cur_k) {
-        shift = P.pats[k].delta + P.off;
-        cur_k = k;
-      }
-      const int64_t pos0 = (tile % P.ntiles) * TILE - shift;  // tile-relative offsets below
-      const int64_t o = P.toff[g];
-      if (o >= P.cap) continue;
+  while (true) {
+    ExpSeg nxt;
+    int64_t g_nn = -1;
+    if (g_nxt >= 0) {  // prefetch: issued before the current segment's work
+      nxt = exp_load(P, g_nxt, lane);
+      if (qi + 2 * stride < nq) g_nn = P.seglist[qi + 2 * stride];
+    }
+    const int64_t g = cur.g;
+    const uint32_t c = cur.c;
+    const int64_t o = cur.o;
+    const int64_t tile = g / NWARP;
+    const int k = (int)(tile / P.ntiles);
+    if (k != cur_k) {
+      shift = P.pats[k].delta + P.off;
+      cur_k = k;
+    }
+    const int64_t pos0 = (tile % P.ntiles) * TILE - shift;  // tile-relative offsets below
+    if (o < P.cap) {
       if (c <= LIST_CAP) {
-        uint32_t v = lane < (int)c ? (uint32_t)P.lists[g * LIST_CAP + lane] : 0xFFFFFFFFu;
+        uint32_t v = lane < (int)c ? (cur.lv & 0xFFFFu) : 0xFFFFFFFFu;
         if (P.unsorted_lists) {  // MP fills list slots atomically: warp bitonic sort of <= 32 offsets
 #pragma unroll
           for (int kk = 2; kk <= 32; kk <<= 1)
@@ -179,42 +209,46 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
             }
         }
         if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + v;
-        continue;
-      }
-      // dense: the 64 bitmap words (2 per lane), exclusive popcount prefix, then
-      // one word per step broadcast to the warp -- lane i writes bit i's
-      // position at its rank, so a full word is one coalesced 256-byte store
-      const uint32_t* bmw = P.bitmaps + g * SEG_WORDS;
-      const int64_t segpos = pos0 + (g % NWARP) * SEG;
-      const uint32_t xa = bmw[lane], xb = bmw[32 + lane];
-      const uint32_t pa = __popc(xa), pb = __popc(xb);
-      uint32_t ia = pa, ib = pb;
+      } else {
+        // dense: exclusive popcount prefix of the 64 words (2 per lane); each
+        // lane extracts its words' set bits into the warp's smem run (index
+        // XOR-swizzled by its 32-entry block so all-ones words do not pile onto
+        // two banks); the warp then streams the c positions out coalesced
+        const int64_t segpos = pos0 + (g % NWARP) * SEG;
+        const uint32_t pa = __popc(cur.xa), pb = __popc(cur.xb);
+        uint32_t ia = pa, ib = pb;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t va = __shfl_up_sync(0xffffffffu, ia, d);
-        const uint32_t vb = __shfl_up_sync(0xffffffffu, ib, d);
-        if (lane >= d) ia += va, ib += vb;
-      }
-      const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31);
-      const uint32_t ea = ia - pa, eb = ta + ib - pb;
-      const uint32_t below = (1u << lane) - 1u;
-      // 32-bit ranks against the room left in the output (o < cap checked above)
-      const uint32_t lim = (uint32_t)(P.cap - o < (int64_t)SEG ? P.cap - o : (int64_t)SEG);
-      int64_t* const dst = P.out + o;
-      const int64_t v0 = segpos + lane;
-#pragma unroll 8
-      for (int w = 0; w < 32; w++) {
-        const uint32_t x = __shfl_sync(0xffffffffu, xa, w);
-        const uint32_t r = __shfl_sync(0xffffffffu, ea, w) + __popc(x & below);
-        st_if((((x >> lane) & 1u) != 0) & (r < lim), dst + r, v0 + 32 * w);
-      }
-#pragma unroll 8
-      for (int w = 0; w < 32; w++) {
-        const uint32_t x = __shfl_sync(0xffffffffu, xb, w);
-        const uint32_t r = __shfl_sync(0xffffffffu, eb, w) + __popc(x & below);
-        st_if((((x >> lane) & 1u) != 0) & (r < lim), dst + r, v0 + 32 * (32 + w));
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t va = __shfl_up_sync(0xffffffffu, ia, d);
+          const uint32_t vb = __shfl_up_sync(0xffffffffu, ib, d);
+          if (lane >= d) ia += va, ib += vb;
+        }
+        const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31);
+        uint32_t x = cur.xa, e = ia - pa;
+        while (x) {
+          const uint32_t b = __ffs(x) - 1;
+          x &= x - 1;
+          sb[e ^ ((e >> 5) & 31u)] = (uint16_t)(32u * lane + b);
+          e++;
+        }
+        x = cur.xb, e = ta + ib - pb;
+        while (x) {
+          const uint32_t b = __ffs(x) - 1;
+          x &= x - 1;
+          sb[e ^ ((e >> 5) & 31u)] = (uint16_t)(32u * (32 + lane) + b);
+          e++;
+        }
+        __syncwarp();
+        const uint32_t lim = (uint32_t)(P.cap - o < (int64_t)c ? P.cap - o : (int64_t)c);
+        int64_t* const dst = P.out + o;
+        for (uint32_t i = lane; i < lim; i += 32) dst[i] = segpos + sb[i ^ ((i >> 5) & 31u)];
+        __syncwarp();  // the next segment overwrites sb
       }
     }
+    if (g_nxt < 0) break;
+    qi += stride;
+    cur = nxt;
+    g_nxt = g_nn;
   }
 }
 
