@@ -203,9 +203,11 @@ __device__ __forceinline__ void shiftor_lane(const uint8_t* q, int m, const uint
 // at a time: text words unaligned (lds32u), pattern 16-byte aligned.  Reads up
 // to s + m + 4.
 __device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {  // unaligned 4-byte smem read
-  const uintptr_t a = (uintptr_t)p;
-  const uint32_t* b = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
-  return __funnelshift_r(b[0], b[1], 8 * (uint32_t)(a & 3));
+  // pointer arithmetic (not an integer round trip) keeps the shared address
+  // space visible to the compiler: LDS, not generic LD
+  const uint32_t mis = (uint32_t)((uintptr_t)p & 3);
+  const uint32_t* b = reinterpret_cast<const uint32_t*>(p - mis);
+  return __funnelshift_r(b[0], b[1], 8 * mis);
 }
 __device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* pat, int m) {
   int k = 0;
@@ -221,21 +223,11 @@ __device__ __forceinline__ bool verify_direct(const uint8_t* s, const uint8_t* p
 // Per-warp break bitmap of a segment: bit q of word i set iff
 // t[y] != t[y + per] for y = y0 + 32 i + q (y relative to the segment's first
 // start position).  nbw[i] = first break at or after word i (relative to y0).
-__device__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* brk, int32_t* nbw) {
+__device__ __forceinline__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* brk, int32_t* nbw);
+// nbw[i] = first set bit of brk[] at or after word i (0x7fffffff if none);
+// nbw[nwords] = none.  Reads brk[0..nwords).
+__device__ __forceinline__ void warp_next_set(int nwords, const uint32_t* brk, int32_t* nbw) {
   const int lane = threadIdx.x & 31;
-  // 128 bytes (4 break words) per step, lane l on bytes [4l, 4l+4): consecutive
-  // lanes read consecutive smem words (no bank conflicts); the 4-bit SWAR
-  // results of 8 lanes are OR-combined into one break word
-  for (int j = 0; 4 * j < nwords; j++) {
-    const bool ok = 4 * j + (lane >> 3) < nwords;
-    const uint8_t* q = Yseg + 128 * j + 4 * lane;
-    uint32_t nib = ok ? ((~zero_bytes4(lds32u(q) ^ lds32u(q + per))) & 0xFu) << (4 * (lane & 7)) : 0u;
-    nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
-    nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
-    nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
-    if (ok && (lane & 7) == 0) brk[4 * j + (lane >> 3)] = nib;
-  }
-  __syncwarp();
   const int seg = (nwords + 31) / 32;
   const int lo = lane * seg, hi = min(nwords, lo + seg);
   int first = 0x7fffffff;
@@ -255,6 +247,69 @@ __device__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* 
   }
   if (lane == 0) nbw[nwords] = 0x7fffffff;
   __syncwarp();
+}
+
+__device__ __forceinline__ void warp_breaks(const uint8_t* Yseg, int per, int nwords, uint32_t* brk, int32_t* nbw) {
+  const int lane = threadIdx.x & 31;
+  // 128 bytes (4 break words) per step, lane l on bytes [4l, 4l+4): consecutive
+  // lanes read consecutive smem words (no bank conflicts); the 4-bit SWAR
+  // results of 8 lanes are OR-combined into one break word
+  for (int j = 0; 4 * j < nwords; j++) {
+    const bool ok = 4 * j + (lane >> 3) < nwords;
+    const uint8_t* q = Yseg + 128 * j + 4 * lane;
+    uint32_t nib = ok ? ((~zero_bytes4(lds32u(q) ^ lds32u(q + per))) & 0xFu) << (4 * (lane & 7)) : 0u;
+    nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
+    nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
+    nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
+    if (ok && (lane & 7) == 0) brk[4 * j + (lane >> 3)] = nib;
+  }
+  __syncwarp();
+  warp_next_set(nwords, brk, nbw);
+}
+
+// OR a run of nbits (<= 32) flag bits into the bitmap at bit position y
+__device__ __forceinline__ void or_bits(uint32_t* bm, int y, uint32_t bits) {
+  if (!bits) return;
+  atomicOr(&bm[y >> 5], bits << (y & 31));
+  if (y & 31) {
+    const uint32_t hi = bits >> (32 - (y & 31));
+    if (hi) atomicOr(&bm[(y >> 5) + 1], hi);
+  }
+}
+
+// Run patterns c^m (period 1): nz bitmap of the bytes != c over Y positions
+// [0, 32 nwords) of a segment (Y0 + c0 = position 0).  The bulk [delta,
+// delta + SEG) is the segment's own staged bytes, read as the filter read
+// them (16 per lane and round, one LDS.128) and compared with c as words, so a
+// clean chunk costs four compares; only the edge ranges go byte-exact through
+// a warp loop.  Then nbw = next nz at or after each word.
+__device__ __forceinline__ void warp_run_nz(const uint8_t* Yseg, const uint8_t* Sseg, int delta, uint32_t c4,
+                                            int nwords, uint32_t* brk, int32_t* nbw) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < nwords; i += 32) brk[i] = 0;
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < SEG / 512; r++) {
+    const uint4 X = *reinterpret_cast<const uint4*>(Sseg + r * 512 + lane * 16);
+    const uint32_t a = X.x ^ c4, b = X.y ^ c4, c = X.z ^ c4, d = X.w ^ c4;
+    if (a | b | c | d) {
+      const uint32_t nz = ((~zero_bytes4(a)) & 0xFu) | (((~zero_bytes4(b)) & 0xFu) << 4) |
+                          (((~zero_bytes4(c)) & 0xFu) << 8) | (((~zero_bytes4(d)) & 0xFu) << 12);
+      or_bits(brk, delta + r * 512 + lane * 16, nz);
+    }
+  }
+  // edges: [0, delta) and [delta + SEG, 32 nwords), 4 bytes per lane and step
+  const int e1 = delta + SEG, end = 32 * nwords;
+  const int n0 = (delta + 3) / 4, n1 = (end - e1 + 3) / 4;
+  for (int q = lane; q < n0 + n1; q += 32) {
+    const int y = q < n0 ? 4 * q : e1 + 4 * (q - n0);
+    const int lim = q < n0 ? delta : end;
+    uint32_t nz = (~zero_bytes4(lds32u(Yseg + y) ^ c4)) & 0xFu;
+    if (lim - y < 4) nz &= (1u << (lim - y)) - 1u;
+    or_bits(brk, y, nz);
+  }
+  __syncwarp();
+  warp_next_set(nwords, brk, nbw);
 }
 
 

@@ -11,6 +11,8 @@
 #include <string.h>
 
 #include <atomic>
+#include <map>
+#include <tuple>
 #include <cmath>
 #include <mutex>
 #include <string>
@@ -286,6 +288,22 @@ void mb_ctx_destroy(mb_ctx* c) {
 
 }  // extern "C"
 
+// Occupancy (CTAs per SM) of a kernel at a dynamic smem size, cached.
+static cudaError_t occupancy(const void* fn, int threads, size_t smem, int* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_tuple(fn, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, threads, smem);
+  if (e == cudaSuccess) cache[key] = *out;
+  return e;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // before its predecessor in the stream completes and must call pdl_wait()
 // before touching the predecessor's results.
@@ -371,7 +389,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
   for (int i = 0; i < gk; i++) {
     const PatDev& d = h_pats[h_idx[i]];
     maxm = std::max<int64_t>(maxm, d.m);
-    if (d.periodic) maxL = std::max(maxL, d.L), any_periodic = true;
+    if (d.periodic) maxL = std::max(maxL, d.L + 1), any_periodic = true;  // +1: period-1 runs use m
     pre = std::max(pre, d.pre);
     post = std::max(post, d.post);
   }
@@ -386,47 +404,40 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
   P.brk_words = any_periodic ? ((((SEG + maxL + 31) / 32) + 1 + 3) & ~3) : 0;
   if constexpr (std::is_same<F, SampledTag>::value) {
     const size_t smem_s = 8192 + 2064 + 8192 + SMP_WARPS * SMP_LIST * 4 + 16 + P.pat_cap + 16;
-    static std::mutex mu_s;
-    static bool attr_s = false;
-    static size_t occ_smem_s = 0;
-    static int occ_s = 0;
+    static std::once_flag attr_once_s;
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once_s, [&] {
+      attr_err = cudaFuncSetAttribute(sampled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
+    CUDA_TRY(attr_err);
     int per_sm_s = 0;
-    {
-      std::lock_guard<std::mutex> g(mu_s);
-      if (!attr_s) {
-        CUDA_TRY(cudaFuncSetAttribute(sampled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_s = true;
-      }
-      if (occ_smem_s != smem_s) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, sampled_kernel, SMP_NT, smem_s));
-        occ_smem_s = smem_s;
-      }
-      per_sm_s = occ_s;
-    }
+    CUDA_TRY(occupancy((const void*)sampled_kernel, SMP_NT, smem_s, &per_sm_s));
     if (per_sm_s < 1) return fail(MB_ECUDA, "sampled kernel does not fit on an SM");
     const int64_t wunits = (P.ntiles * NWARP + SMP_SEGS - 1) / SMP_SEGS;
     const int64_t units = ((wunits + SMP_WARPS - 1) / SMP_WARPS) * gk;
     const int64_t grid_s = std::min<int64_t>(units, (int64_t)c->nsm * per_sm_s);
     sampled_kernel<<<(int)grid_s, SMP_NT, smem_s, st>>>(P);
   } else {
-    const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
-                        (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * 256 * 8 : 0);
-    static std::mutex mu;
-    static bool attr_done = false;
-    static size_t occ_smem = 0;
-    static int occ_val = 0;
+    auto smem_for = [&](int ns) {
+      return (size_t)SM_STAGES + (size_t)ns * P.stage_bytes + NWARP * SEG_WORDS * 4 +
+             (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * 256 * 8 : 0);
+    };
+    static std::once_flag attr_once;
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+      attr_err = cudaFuncSetAttribute(scan_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
+    CUDA_TRY(attr_err);
+    // 3 stages, unless that leaves one CTA per SM where 2 stages fit two
+    // (large halos: long periodic patterns keep 2 x 17 warps per SM busy)
+    P.nstages = STAGES;
+    size_t smem = smem_for(STAGES);
     int per_sm = 0;
-    {
-      std::lock_guard<std::mutex> g(mu);
-      if (!attr_done) {
-        CUDA_TRY(cudaFuncSetAttribute(scan_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_done = true;
-      }
-      if (occ_smem != smem) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val, scan_kernel<F>, NT + 32, smem));
-        occ_smem = smem;
-      }
-      per_sm = occ_val;
+    CUDA_TRY(occupancy((const void*)scan_kernel<F>, NT + 32, smem, &per_sm));
+    if (per_sm < 2 && STAGES > 2) {
+      int per_sm2 = 0;
+      CUDA_TRY(occupancy((const void*)scan_kernel<F>, NT + 32, smem_for(2), &per_sm2));
+      if (per_sm2 > per_sm) P.nstages = 2, smem = smem_for(2), per_sm = per_sm2;
     }
     if (per_sm < 1) return fail(MB_ECUDA, "scan kernel does not fit on an SM");
     const int64_t grid = std::min<int64_t>(P.group_tiles, (int64_t)c->nsm * per_sm);
@@ -675,18 +686,8 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       M.kbase = k0;
       M.ticket = c->ticket + TICKET_MP0 + ci;
       const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * M.stage_bytes + 8192 + 4 * bs_words + 8 * M.nents;
-      static std::mutex mu_occ;
-      static size_t occ_smem = 0;
-      static int occ_val = 0;
       int per_sm = 0;
-      {
-        std::lock_guard<std::mutex> g(mu_occ);
-        if (occ_smem != smem) {
-          CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val, mp_scan_kernel, NT + 32, smem));
-          occ_smem = smem;
-        }
-        per_sm = occ_val;
-      }
+      CUDA_TRY(occupancy((const void*)mp_scan_kernel, NT + 32, smem, &per_sm));
       if (per_sm < 1) return fail(MB_ECUDA, "MP kernel does not fit on an SM");
       const int64_t grid = std::min<int64_t>(M.ntiles_text, (int64_t)c->nsm * per_sm);
       mp_scan_kernel<<<(int)grid, NT + 32, smem, st>>>(M);

@@ -19,16 +19,17 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   uint8_t* stages = smem + SM_STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (P.run_if && *P.run_if == 0u) return;  // conditional fallback launch (MP did not overflow)
-  uint32_t* bm = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes) + warp * SEG_WORDS;
-  uint32_t* brk = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4) +
+  const int NS = P.nstages;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(stages + NS * P.stage_bytes) + warp * SEG_WORDS;
+  uint32_t* brk = reinterpret_cast<uint32_t*>(stages + NS * P.stage_bytes + NWARP * SEG_WORDS * 4) +
                   warp * 2 * (P.brk_words + 4);
   int32_t* nbw = reinterpret_cast<int32_t*>(brk + P.brk_words + 4);
-  uint64_t* so_s = reinterpret_cast<uint64_t*>(stages + STAGES * P.stage_bytes + NWARP * SEG_WORDS * 4 +
+  uint64_t* so_s = reinterpret_cast<uint64_t*>(stages + NS * P.stage_bytes + NWARP * SEG_WORDS * 4 +
                                                NWARP * 2 * (P.brk_words + 4) * 4) +
                    warp * 256;  // K2 only: per-warp shift-or masks
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) {
+    for (int s = 0; s < NS; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWARP);
     }
@@ -39,8 +40,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   if (warp == NWARP) {  // ---------------- producer
     if (lane == 0) {
       for (int it = 0;; it++) {
-        const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
+        const int s = it % NS;
+        if (it >= NS) mbar_wait(&empty[s], (uint32_t)(it / NS - 1) & 1u);
         const unsigned long long tk = atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
         if ((int64_t)tk >= P.group_tiles) {
           hdr[s].tk = -1;
@@ -75,8 +76,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   PatDev pd;
   int64_t blo = 0, bhi = -1;
   for (int it = 0;; it++) {
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+    const int s = it % NS;
+    mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
     const int64_t tk = hdr[s].tk;
     if (tk < 0) break;
     const int k = hdr[s].k;
@@ -159,9 +160,15 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
           // s matches <=> t[s..s+per) = p[0..per) and no break t[y] != t[y+per] for
           // y in [s, s+L).  A break y kills starts [y-L+1, y]: walk the few breaks
           // that reach this lane's 64 starts, mask them out in bulk.
-          const int nwords = (SEG + pd.L + 31) / 32;
+          // Period 1 (c^m): the same test with "byte != c" for "break" and
+          // m for L, built from word compares of the staged segment.
+          const int Lk = pd.per == 1 ? (int)pd.m : pd.L;
+          const int nwords = (SEG + Lk + 31) / 32;
           MB_CHECK(Y0 + c0 >= sbeg && Y0 + c0 + 32 * nwords + pd.per + 8 <= send);
-          warp_breaks(Y0 + c0, pd.per, nwords, brk, nbw);
+          if (pd.per == 1)
+            warp_run_nz(Y0 + c0, S + c0, pd.delta, 0x01010101u * spat[0], nwords, brk, nbw);
+          else
+            warp_breaks(Y0 + c0, pd.per, nwords, brk, nbw);
           uint64_t cand = ((uint64_t)w1 << 32) | w0;
           if (cand) {
             auto nb = [&](int y) -> int {
@@ -171,8 +178,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
             };
             const int q0 = 64 * lane, q1 = q0 + 63;
             uint64_t killed = 0;
-            for (int y = nb(q0); y != 0x7fffffff && y - pd.L + 1 <= q1; y = nb(y + 1)) {
-              const int lo = max(q0, y - pd.L + 1) - q0, hi = min(q1, y) - q0;
+            for (int y = nb(q0); y != 0x7fffffff && y - Lk + 1 <= q1; y = nb(y + 1)) {
+              const int lo = max(q0, y - Lk + 1) - q0, hi = min(q1, y) - q0;
               if (lo <= hi) killed |= (hi - lo == 63) ? ~0ULL : (((1ULL << (hi - lo + 1)) - 1) << lo);
               if (y >= q1) break;
             }

@@ -2,18 +2,21 @@
 //
 // A search (or a batch of K patterns over one text) is three kernels:
 //
-//  1. scan_kernel<Filter>  (persistent, dynamic tile tickets, no inter-CTA waits)
-//       TMA 1D bulk copy of tile + halo into a 4-stage smem ring (mbarrier)
-//       -> filter: each lane scans 16 staged bytes per round (packed-word
-//          compare) -> candidate bits -> tile bitmap in smem
-//       -> verify (only if a candidate exists and the filter is not exact):
-//          direct window compare, or period/break-run test, in smem
-//       -> per-tile count; matches stored compactly: <= LIST_CAP tile-local
-//          uint16 offsets, else the tile's 2 KiB bitmap
-//  2. offsets_kernel  exclusive scan of tile counts (decoupled look-back over
-//       4096-count chunks) -> global output offset per tile, CSR pattern ends
-//  3. expand_kernel   warp per tile: list / bitmap -> ascending int64
-//       positions at out[offset ..]
+//  1. count kernel -- scan_kernel<Filter> (persistent, dynamic tile tickets,
+//       no inter-CTA waits): TMA 1D bulk copy of tile + halo into a 2-3 stage
+//       smem ring (mbarrier full/empty) -> filter: each lane tests 16 staged
+//       bytes per round (packed-word compares) -> candidate bits -> verify
+//       (only if a candidate exists and the filter is not exact): direct
+//       window compare, warp-cooperative compare, or the period / break-run
+//       test -> per-segment (2 KiB) count, matches stored as <= LIST_CAP
+//       tile-relative uint16 offsets, else the segment's 256-byte bitmap.
+//       Alternatives producing the same segment layout: sampled_kernel (K3,
+//       long patterns), mp_scan_kernel (K5, one pass for a whole batch).
+//  2. offsets_kernel -- exclusive scan of the segment counts (decoupled
+//       look-back over NT*PER-count chunks) -> CSR pattern ends; sparse
+//       sorted segments are expanded in place, the rest queued
+//  3. expand_kernel -- warp per queued segment: list / bitmap -> ascending
+//       int64 positions at out[offset ..]
 //
 // Bitmap coordinates: tile tau of a pattern covers bitmap indices
 // b in [tau*TILE, (tau+1)*TILE); index b stands for start position
@@ -38,7 +41,7 @@ constexpr int TILE = NWARP * 2048; // bitmap positions per tile (one TMA stage):
 constexpr int NT = NWARP * 32;    // consumer threads
 constexpr int SEG = TILE / NWARP; // positions per consumer-warp segment
 constexpr int SEG_WORDS = SEG / 32;
-constexpr int STAGES = MB_STAGES;  // TMA ring depth
+constexpr int STAGES = MB_STAGES;  // TMA ring depth (max; scan_kernel may run with 2, see ScanParams.nstages)
 constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offsets
 constexpr int TICKET_OFFSETS = 7; // ticket slot of offsets_kernel (slots 0..6: family groups)
 constexpr int MAX_GROUPS = 7;
@@ -72,6 +75,7 @@ struct ScanParams {
   int stage_bytes;
   int brk_words;        // per-warp break-bitmap words (multiple of 4; 0 if no periodic pattern)
   int pat_cap;          // pattern bytes reserved in smem (multiple of 16)
+  int nstages;          // TMA ring depth of this launch (2..STAGES): 2 when 3 would cost a CTA per SM
   unsigned long long* ticket;  // [g]: tile tickets of family group g, [TICKET_OFFSETS]: scan chunks
   int ticket_slot;      // this launch's ticket counter
   const int32_t* plist; // family group -> batch pattern index (null: identity)

@@ -21,6 +21,53 @@ __global__ void k_write(int64_t* __restrict__ out, size_t n, int64_t base) {
   }
 }
 
+// region-per-warp: each warp writes whole 16 KB runs (2048 int64), 256 B per
+// store instruction -- the dense-segment output pattern of expand_kernel
+__global__ void k_region(int64_t* __restrict__ out, size_t nseg, int64_t base) {
+  const int lane = threadIdx.x & 31;
+  const size_t w0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t g = w0; g < nseg; g += nw) {
+    int64_t* d = out + g * 2048 + 5;  // odd offset: runs are not 256-B aligned in expand either
+    for (int i = lane; i < 2048 - 5; i += 32) d[i] = base + (int64_t)(g * 2048 + i);
+  }
+}
+// region-per-CTA: the whole block writes one 16 KB run at a time
+__global__ void k_region_cta(int64_t* __restrict__ out, size_t nseg, int64_t base) {
+  for (size_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+    int64_t* d = out + g * 2048 + 5;
+    for (int i = threadIdx.x; i < 2048 - 5; i += blockDim.x) d[i] = base + (int64_t)(g * 2048 + i);
+  }
+}
+float run_region_cta(int64_t* d, size_t n, int grid, int block) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const size_t nseg = n / 2048;
+  k_region_cta<<<grid, block>>>(d, nseg, 7);
+  cudaEventRecord(a);
+  for (int r = 0; r < 10; r++) k_region_cta<<<grid, block>>>(d, nseg, r);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  return nseg * (2048 - 5) * 8.0 * 10 / (ms * 1e-3) / 1e9;
+}
+float run_region(int64_t* d, size_t n, int grid, int block) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const size_t nseg = n / 2048;
+  k_region<<<grid, block>>>(d, nseg, 7);
+  cudaEventRecord(a);
+  for (int r = 0; r < 10; r++) k_region<<<grid, block>>>(d, nseg, r);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  return nseg * (2048 - 5) * 8.0 * 10 / (ms * 1e-3) / 1e9;
+}
+
 template <int VEC, bool CS>
 float run(int64_t* d, size_t n, int grid) {
   cudaEvent_t a, b;
@@ -47,6 +94,10 @@ int main() {
     printf("grid %5d  v1 %7.0f  v1.cs %7.0f  v2 %7.0f  v2.cs %7.0f GB/s\n", grid, run<1, false>(d, n, grid),
            run<1, true>(d, n, grid), run<2, false>(d, n, grid), run<2, true>(d, n, grid));
   }
+  for (int mult : {4, 8, 16}) printf("region-per-warp grid %5d x 128: %7.0f GB/s\n", nsm * mult, run_region(d, n, nsm * mult, 128));
+  for (int mult : {2, 4}) printf("region-per-warp grid %5d x 512: %7.0f GB/s\n", nsm * mult, run_region(d, n, nsm * mult, 512));
+  for (int mult : {4, 8, 16}) printf("region-per-CTA grid %5d x 128: %7.0f GB/s\n", nsm * mult, run_region_cta(d, n, nsm * mult, 128));
+  for (int mult : {2, 4}) printf("region-per-CTA grid %5d x 512: %7.0f GB/s\n", nsm * mult, run_region_cta(d, n, nsm * mult, 512));
   cudaFree(d);
   return 0;
 }
