@@ -10,8 +10,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <map>
+#include <unordered_map>
 #include <tuple>
 #include <cmath>
 #include <mutex>
@@ -107,6 +109,22 @@ static int plan_device(const mb_plan* p, const PatDev** out) {
   return MB_OK;
 }
 
+// One batch-level pass over the text (K5; see plan_pass).
+struct BatchPass {
+  int kind = 0;
+  int q = 0;
+  std::vector<uint32_t> img;                    // all chunks, each 16-byte aligned
+  struct Chunk {
+    int64_t off;  // word offset in img
+    int B;        // log2 buckets
+    int nent;     // entries
+  };
+  std::vector<Chunk> chunks;  // one per MP_CHUNK patterns
+  int pre = 0, post = 0;                        // staged margins the verification needs
+  std::vector<uint32_t> need;                   // per pattern: 0 = in the pass, 1 = per-pattern scan
+  int64_t words() const { return (int64_t)img.size(); }
+};
+
 struct mb_ctx {
   int device = 0;
   int nsm = 0;
@@ -125,10 +143,11 @@ struct mb_ctx {
   int32_t* plist = nullptr;
   int64_t plist_cap = 0;
   std::vector<int32_t> h_plist;
-  uint32_t* mp_tab = nullptr;  // MP tables (bloom, bucket starts, entries) per chunk
+  uint32_t* mp_tab = nullptr;  // batch-pass tables (bloom, bucket starts, entries) per chunk
   int64_t mp_tab_cap = 0;
-  std::vector<uint32_t> h_mp;
-  std::vector<double> h_rate;
+  uint32_t* need = nullptr;    // per-pattern scan flags of a batch pass
+  int64_t need_cap = 0;
+  BatchPass pass;  // ad-hoc batches: planned per call
   int64_t mp_batches = 0;
   uint32_t epoch = 0;
   unsigned long long* ticket = nullptr;
@@ -165,9 +184,8 @@ struct mb_batch {
   int device = 0;
   std::vector<PatDev> h_pats;
   PatDev* d_pats = nullptr;
-  std::vector<double> rates;
-  uint32_t* d_mp = nullptr;
-  std::vector<std::pair<int64_t, int>> mp_chunks;
+  BatchPass pass;
+  uint32_t* d_mp = nullptr;  // pass tables on the device
 };
 
 extern "C" {
@@ -270,6 +288,7 @@ void mb_ctx_destroy(mb_ctx* c) {
   cudaFree(c->seglist);
   cudaFree(c->plist);
   cudaFree(c->mp_tab);
+  cudaFree(c->need);
   cudaFree(c->ticket);
   cudaFree(c->d_pats);
   cudaFree(c->d_text);
@@ -480,52 +499,188 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
   return fail(MB_EINVAL, "unknown kernel family");
 }
 
-// MP eligibility (K5): a batch of >= 8 patterns of length >= 7 (any family:
-// the pass uses each plan's mpG grams) whose pooled anchors stay selective.
-// `rate` is the expected number of gram hits per text word, sum over patterns
-// k and j of prod_i p(mpG_kj[i]), with byte probabilities p estimated from all
-// pattern bytes of the batch (patterns are drawn from the text); MP runs when
-// rate <= 0.05.  A batch of sampled-filter (K3) patterns alone reads ~1/S of
-// the text per pattern, so it takes the pass only from 64 patterns on.
-static bool mp_eligible(const PatDev* h_pats, const double* rate, int K) {
-  if (!rate || K < 8 || K > MP_CHUNK * MAX_GROUPS || *rate > 0.05) return false;
-  bool all_sampled = true;
-  for (int k = 0; k < K; k++) {
-    if (h_pats[k].m < 7) return false;
-    all_sampled &= h_pats[k].family == MB_FAM_SAMPLED;
-  }
-  return !all_sampled || K >= 64;
-}
+// ---- K5 batch passes: one pass over the text for a whole batch.
+//
+// kind 1 (aligned-word pass, mp_scan_kernel): >= 8 patterns of length >= 7
+// (any family: the pass uses each plan's one-word anchor grams mpG) whose
+// pooled grams hit <= 0.05 times per aligned text word; a batch of sampled
+// (K3) patterns alone reads ~1/S of the text per pattern, so it takes the
+// pass only from 64 patterns on.
+// kind 2 (byte-offset pass, mpb_scan_kernel<q>): otherwise, >= 8 patterns of
+// length >= 2 with one q-byte gram each (q = 8, 4, 3 or 2 by the shortest
+// pattern), taken when every pattern expects <= 10 occurrences per 2 KiB
+// segment (LIST_CAP headroom) and the pooled grams hit <= 8 times per text
+// position.
+// Byte probabilities p are estimated from the batch's own pattern bytes
+// (patterns are drawn from the text).  Tables are built per MP_CHUNK
+// patterns: bloom (64 Kbit), bucket starts, entries.
 
-// Host-built MP tables for patterns [k0, k0 + kc): bloom, bucket starts, entries.
-static void mp_tables(const PatDev* h_pats, int k0, int kc, int* Bout, std::vector<uint32_t>& img) {
-  const int nent = 4 * kc;
+static inline uint32_t pass_hash(uint32_t lo, uint32_t hi) { return lo * 0x9E3779B1u ^ hi * 0x85EBCA77u; }
+
+template <class Ent>
+static void pass_chunk(int kc, int ent_words, const Ent& ent_of, std::vector<uint32_t>& img, int* Bout, int* nout) {
+  // ent_of(i, j, &hash, words[ent_words]) -> false if pattern i has no entry j
+  std::vector<std::pair<uint32_t, std::vector<uint32_t>>> ents;
+  for (int i = 0; i < kc; i++)
+    for (int j = 0; j < 4; j++) {
+      uint32_t h = 0;
+      std::vector<uint32_t> w(ent_words, 0u);
+      if (ent_of(i, j, &h, w.data())) ents.push_back({h, std::move(w)});
+    }
+  const int nent = (int)ents.size();
   int B = 4;
   while ((1 << B) < nent) B++;
   const int nb = 1 << B;
   const int bs_words = (nb + 1 + 3) & ~3;
-  img.assign(2048 + bs_words + 2 * nent, 0u);
-  uint32_t* bloom = img.data();
+  const size_t base = img.size();
+  img.resize(base + 2048 + bs_words + (size_t)ent_words * nent, 0u);
+  uint32_t* bloom = img.data() + base;
   uint32_t* bstart = bloom + 2048;
+  uint32_t* out = bstart + bs_words;
   std::vector<uint32_t> cnt(nb, 0);
-  for (int i = 0; i < kc; i++)
-    for (int j = 0; j < 4; j++) {
-      const uint32_t h = h_pats[k0 + i].mpG[j] * 0x9E3779B1u;
-      bloom[h >> 21] |= 1u << ((h >> 16) & 31);
-      cnt[h >> (32 - B)]++;
-    }
+  for (auto& e : ents) {
+    bloom[e.first >> 21] |= 1u << ((e.first >> 16) & 31);
+    cnt[e.first >> (32 - B)]++;
+  }
   for (int b = 0; b < nb; b++) bstart[b + 1] = bstart[b] + cnt[b];
   std::vector<uint32_t> fill(bstart, bstart + nb);
-  uint32_t* ents = bstart + bs_words;
-  for (int i = 0; i < kc; i++)
-    for (int j = 0; j < 4; j++) {
-      const uint32_t g = h_pats[k0 + i].mpG[j];
-      const uint32_t b = (g * 0x9E3779B1u) >> (32 - B);
-      const uint32_t e = fill[b]++;
-      ents[2 * e] = g;
-      ents[2 * e + 1] = ((uint32_t)i << 16) | (uint32_t)(h_pats[k0 + i].mpa + j);
-    }
+  for (auto& e : ents) {
+    const uint32_t slot = fill[e.first >> (32 - B)]++;
+    for (int w = 0; w < ent_words; w++) out[(size_t)ent_words * slot + w] = e.second[w];
+  }
+  while (img.size() % 4) img.push_back(0);
   *Bout = B;
+  *nout = nent;
+}
+
+static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, BatchPass* bp) {
+  *bp = BatchPass();
+  if (K < 8 || K > MP_CHUNK * MAX_GROUPS) return;
+  double hist[256] = {0}, tot = 0;
+  int64_t minm = INT64_MAX;
+  for (int k = 0; k < K; k++) {
+    const auto& pb = plans[k]->h.pat;
+    const size_t lim = std::min<size_t>(pb.size(), 64);
+    for (size_t i = 0; i < lim; i++) hist[pb[i]] += 1, tot += 1;
+    minm = std::min<int64_t>(minm, h_pats[k].m);
+  }
+  double pr[256];
+  for (int c = 0; c < 256; c++) pr[c] = hist[c] / tot;
+  auto gp = [&](const uint8_t* g, int q) {
+    double r = 1;
+    for (int i = 0; i < q; i++) r *= pr[g[i]];
+    return r;
+  };
+  // kind 1
+  if (minm >= 7) {
+    double rate = 0;
+    bool all_sampled = true;
+    for (int k = 0; k < K; k++) {
+      all_sampled &= h_pats[k].family == MB_FAM_SAMPLED;
+      for (int j = 0; j < 4; j++) {
+        uint8_t g[4];
+        memcpy(g, &h_pats[k].mpG[j], 4);
+        rate += gp(g, 4);
+      }
+    }
+    if (rate <= 0.05 && (!all_sampled || K >= 64)) {
+      bp->kind = 1;
+      bp->need.assign(K, 0u);
+      int64_t pre = 0, post = 0;
+      for (int k = 0; k < K; k++) {
+        pre = std::max<int64_t>(pre, h_pats[k].mpa + 3);
+        post = std::max<int64_t>(post, h_pats[k].m - h_pats[k].mpa + 8);
+      }
+      bp->pre = (int)((pre + 15) & ~15LL);
+      bp->post = (int)((post + 15) & ~15LL) + 16;
+      for (int k0 = 0; k0 < K; k0 += MP_CHUNK) {
+        const int64_t off = (int64_t)bp->img.size();
+        int B = 0, ne = 0;
+        pass_chunk(std::min(MP_CHUNK, K - k0), 2,
+                   [&](int i, int j, uint32_t* h, uint32_t* w) {
+                     w[0] = h_pats[k0 + i].mpG[j];
+                     w[1] = ((uint32_t)i << 16) | (uint32_t)(h_pats[k0 + i].mpa + j);
+                     *h = w[0] * 0x9E3779B1u;  // the aligned pass hashes the word alone
+                     return true;
+                   },
+                   bp->img, &B, &ne);
+        bp->chunks.push_back({off, B, ne});
+      }
+      return;
+    }
+  }
+  // kind 2: sparse patterns (<= 8 expected occurrences per 2 KiB segment, <= 2
+  // if self-overlapping: a^8 clusters in a binary text) take the pass, the
+  // others keep their per-pattern scan; worth it when most are sparse
+  std::vector<uint32_t> need(K, 1u);
+  int64_t qm = INT64_MAX;
+  int n_in = 0;
+  for (int k = 0; k < K; k++) {
+    const auto& pb = plans[k]->h.pat;
+    const int64_t m = (int64_t)pb.size();
+    if (m < 2 || h_pats[k].family == MB_FAM_SAMPLED) continue;  // K3 reads ~1/S of the text on its own
+    const double per_seg = 2048.0 * gp(pb.data(), (int)std::min<int64_t>(m, 32));
+    if (per_seg > (plans[k]->h.period < m ? 2.0 : 8.0)) continue;
+    need[k] = 0u;
+    n_in++;
+    qm = std::min(qm, m);
+  }
+  if (n_in < 8 || 2 * n_in < K) return;
+  const int q = qm >= 8 ? 8 : qm >= 4 ? 4 : (int)qm;
+  std::vector<int32_t> anchor(K, 0);
+  std::unordered_map<uint64_t, int> used;  // gram value -> patterns already anchored on it
+  double pooled = 0;
+  for (int k = 0; k < K; k++) {
+    if (need[k]) continue;
+    const auto& pb = plans[k]->h.pat;
+    const int64_t m = (int64_t)pb.size();
+    // rarest window, spread over distinct gram values (a value shared by many
+    // patterns makes every text hit on it walk all of them)
+    int best = 0;
+    double bcost = 1e300, bpr = 0;
+    uint64_t bval = 0;
+    for (int64_t a = 0; a + q <= m; a++) {
+      uint64_t v = 0;
+      memcpy(&v, pb.data() + a, q);
+      const double r = gp(pb.data() + a, q);
+      auto it = used.find(v);
+      const double cost = r * (1 + (it == used.end() ? 0 : it->second));
+      if (cost < bcost * (1 - 1e-12)) bcost = cost, bpr = r, best = (int)a, bval = v;
+    }
+    anchor[k] = best;
+    used[bval]++;
+    pooled += bpr;
+  }
+  if (pooled > 8.0) return;
+  bp->kind = 2;
+  bp->q = q;
+  bp->need = need;
+  int64_t pre = 0, post = 0;
+  for (int k = 0; k < K; k++) {
+    if (need[k]) continue;
+    pre = std::max<int64_t>(pre, anchor[k]);
+    post = std::max<int64_t>(post, h_pats[k].m - anchor[k] + 8);
+  }
+  bp->pre = (int)((pre + 15) & ~15LL);
+  bp->post = (int)((std::max<int64_t>(post, 24) + 15) & ~15LL) + 16;
+  for (int k0 = 0; k0 < K; k0 += MP_CHUNK) {
+    const int64_t off = (int64_t)bp->img.size();
+    int B = 0, ne = 0;
+    pass_chunk(std::min(MP_CHUNK, K - k0), 4,
+               [&](int i, int j, uint32_t* h, uint32_t* w) {
+                 if (j || need[k0 + i]) return false;  // one gram per pattern in the pass
+                 const auto& pb = plans[k0 + i]->h.pat;
+                 uint8_t g[8] = {0};
+                 memcpy(g, pb.data() + anchor[k0 + i], q);
+                 memcpy(&w[0], g, 4);
+                 memcpy(&w[1], g + 4, 4);
+                 w[2] = ((uint32_t)i << 16) | (uint32_t)anchor[k0 + i];
+                 *h = pass_hash(w[0], w[1]);
+                 return true;
+               },
+               bp->img, &B, &ne);
+    bp->chunks.push_back({off, B, ne});
+  }
 }
 
 // One search (K = 1) or batch: per family group one count kernel (or, for a
@@ -534,8 +689,8 @@ static void mp_tables(const PatDev* h_pats, int k0, int kc, int* Bout, std::vect
 // output is CSR in the caller's pattern order whatever the family mix.
 static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
                       int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st,
-                      const double* mp_rates = nullptr, const int64_t* out_base = nullptr,
-                      const uint32_t* mp_dev = nullptr, const std::pair<int64_t, int>* mp_chunks = nullptr) {
+                      const int64_t* out_base = nullptr, const BatchPass* bp = nullptr,
+                      const uint32_t* d_tab = nullptr, int chunk0 = 0) {
   ScanParams P;
   memset(&P, 0, sizeof(P));
   const uintptr_t addr = (uintptr_t)d_text;
@@ -614,19 +769,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   };
 
   bool mp_used = false;
-  double mp_rate = 1e30;
-  if (mp_rates) {
-    mp_rate = 0;
-    for (int k = 0; k < K; k++) mp_rate += mp_rates[k];
-  }
-  if (mp_eligible(h_pats, mp_rates ? &mp_rate : nullptr, K)) {
-    // staged margins for verification around each gram hit: window [x - mpa - 3, x - mpa - 3 + m)
-    int64_t pre64 = 0, post64 = 0;
-    for (int k = 0; k < K; k++) {
-      pre64 = std::max<int64_t>(pre64, h_pats[k].mpa + 3);
-      post64 = std::max<int64_t>(post64, h_pats[k].m - h_pats[k].mpa + 8);
-    }
-    const int pre = (int)((pre64 + 15) & ~15LL), post = (int)((post64 + 15) & ~15LL) + 16;
+  if (bp && bp->kind && d_tab) {
     MPParams M;
     memset(&M, 0, sizeof(M));
     M.text = P.text;
@@ -635,62 +778,66 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     M.nv16 = P.nv16;
     M.ntiles_text = (P.nv16 + TILE - 1) / TILE;
     M.ntiles = P.ntiles;
-    M.pre = pre;
-    M.post = post;
-    M.stage_bytes = (pre + TILE + post + 127) & ~127;
+    M.pre = bp->pre;
+    M.post = bp->post;
+    M.stage_bytes = (M.pre + TILE + M.post + 127) & ~127;
     M.pats = d_pats;
     M.counts = c->counts;
     M.lists = c->lists;
-    if (!mp_dev && (rc = grow(&c->mp_tab, &c->mp_tab_cap, (int64_t)(2048 + 4 * MP_CHUNK + 8 + 8 * MP_CHUNK) * MAX_GROUPS,
-                              "MP tables")))
-      return rc;
     M.overflow = reinterpret_cast<unsigned int*>(c->counts + T);  // 4 spare bytes after the counts
     CUDA_TRY(cudaMemsetAsync(c->counts, 0, sizeof(uint16_t) * (T + 2), st));
+    // per-pattern scan flags: patterns left out of the pass start at 1 (and so
+    // does the any-flag that gates the per-pattern scan launches)
+    if ((rc = grow(&c->need, &c->need_cap, K, "pass flags"))) return rc;
+    const int kbase = chunk0 * MP_CHUNK;
+    if ((rc = stage_upload(c, c->need, bp->need.data() + kbase, sizeof(uint32_t) * K, st))) return rc;
+    bool any_out = false;
+    for (int k = 0; k < K; k++) any_out |= bp->need[kbase + k] != 0;
+    if (any_out) CUDA_TRY(cudaMemsetAsync(M.overflow, 1, 1, st));
+    M.need = c->need;
     CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 16 * sizeof(unsigned long long), st));
-    // MP tables: prepared once with the batch (mb_batch_create) or built here
-    const uint32_t* tab = mp_dev;
-    std::vector<std::pair<int64_t, int>> chunk_at;  // (table word offset, B) per chunk
-    if (mp_dev && mp_chunks) {
-      for (int k0 = 0, ci = 0; k0 < K; k0 += MP_CHUNK, ci++) chunk_at.push_back(mp_chunks[ci]);
-    } else {
-      c->h_mp.clear();
-      for (int k0 = 0; k0 < K; k0 += MP_CHUNK) {
-        std::vector<uint32_t> img;
-        int B = 0;
-        mp_tables(h_pats, k0, std::min(MP_CHUNK, K - k0), &B, img);
-        chunk_at.push_back({(int64_t)c->h_mp.size(), B});
-        c->h_mp.insert(c->h_mp.end(), img.begin(), img.end());
-        while (c->h_mp.size() % 4) c->h_mp.push_back(0);
-      }
-      if ((rc = stage_upload(c, c->mp_tab, c->h_mp.data(), sizeof(uint32_t) * c->h_mp.size(), st))) return rc;
-      tab = c->mp_tab;
-    }
-    static std::mutex mu_mp;
-    static bool attr_mp = false;
+    const void* fn = bp->kind == 1 ? (const void*)mp_scan_kernel
+                     : bp->q == 8  ? (const void*)mpb_scan_kernel<8>
+                     : bp->q == 4  ? (const void*)mpb_scan_kernel<4>
+                     : bp->q == 3  ? (const void*)mpb_scan_kernel<3>
+                                   : (const void*)mpb_scan_kernel<2>;
     {
+      static std::mutex mu_mp;
+      static std::vector<const void*> attr_done;
       std::lock_guard<std::mutex> g(mu_mp);
-      if (!attr_mp) {
-        CUDA_TRY(cudaFuncSetAttribute(mp_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_mp = true;
+      if (std::find(attr_done.begin(), attr_done.end(), fn) == attr_done.end()) {
+        CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_done.push_back(fn);
       }
     }
-    for (int k0 = 0, ci = 0; k0 < K; k0 += MP_CHUNK, ci++) {
-      const int kc = std::min(MP_CHUNK, K - k0);
-      const int B = chunk_at[ci].second;
+    const int ent_words = bp->kind == 1 ? 2 : 4;
+    for (int k0 = 0, ci = chunk0; k0 < K; k0 += MP_CHUNK, ci++) {
+      const int B = bp->chunks[ci].B;
       const int bs_words = ((1 << B) + 1 + 3) & ~3;
-      M.bloom = tab + chunk_at[ci].first;
+      M.bloom = d_tab + bp->chunks[ci].off;
       M.bstart = M.bloom + 2048;
       M.ents = reinterpret_cast<const uint2*>(M.bstart + bs_words);
+      M.ents4 = reinterpret_cast<const uint4*>(M.bstart + bs_words);
       M.B = B;
-      M.nents = 4 * kc;
+      M.nents = bp->chunks[ci].nent;
       M.kbase = k0;
-      M.ticket = c->ticket + TICKET_MP0 + ci;
-      const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * M.stage_bytes + 8192 + 4 * bs_words + 8 * M.nents;
+      M.ticket = c->ticket + TICKET_MP0 + (ci - chunk0);
+      const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * M.stage_bytes + 8192 + 4 * bs_words +
+                          (size_t)4 * ent_words * M.nents;
       int per_sm = 0;
-      CUDA_TRY(occupancy((const void*)mp_scan_kernel, NT + 32, smem, &per_sm));
-      if (per_sm < 1) return fail(MB_ECUDA, "MP kernel does not fit on an SM");
-      const int64_t grid = std::min<int64_t>(M.ntiles_text, (int64_t)c->nsm * per_sm);
-      mp_scan_kernel<<<(int)grid, NT + 32, smem, st>>>(M);
+      CUDA_TRY(occupancy(fn, NT + 32, smem, &per_sm));
+      if (per_sm < 1) return fail(MB_ECUDA, "batched pass kernel does not fit on an SM");
+      const int grid = (int)std::min<int64_t>(M.ntiles_text, (int64_t)c->nsm * per_sm);
+      if (bp->kind == 1)
+        mp_scan_kernel<<<grid, NT + 32, smem, st>>>(M);
+      else if (bp->q == 8)
+        mpb_scan_kernel<8><<<grid, NT + 32, smem, st>>>(M);
+      else if (bp->q == 4)
+        mpb_scan_kernel<4><<<grid, NT + 32, smem, st>>>(M);
+      else if (bp->q == 3)
+        mpb_scan_kernel<3><<<grid, NT + 32, smem, st>>>(M);
+      else
+        mpb_scan_kernel<2><<<grid, NT + 32, smem, st>>>(M);
       g_launches++;
       CUDA_TRY(cudaGetLastError());
     }
@@ -698,6 +845,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // a segment overflowed (kernels read the flag and exit otherwise); lists are
     // sorted on expand either way (harmless for the already-sorted fallback lists)
     P.run_if = M.overflow;
+    P.need = c->need;
     mp_used = true;
     c->mp_batches++;
   }
@@ -754,34 +902,12 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
   return rc ? rc : rc2;
 }
 
-// per-pattern expected pooled-gram hits per text word (K5 MP eligibility),
-// byte probabilities estimated from the batch's own pattern bytes
-static void batch_rates(const mb_plan* const* plans, const PatDev* h_pats, int K, std::vector<double>* rates) {
-  rates->assign(K, 1e30);
-  double hist[256] = {0}, tot = 0;
-  for (int k = 0; k < K; k++) {
-    const auto& pb = plans[k]->h.pat;
-    const size_t lim = std::min<size_t>(pb.size(), 64);
-    for (size_t i = 0; i < lim; i++) hist[pb[i]] += 1, tot += 1;
-  }
-  for (int k = 0; k < K; k++)
-    if (h_pats[k].m >= 7) {
-      double r = 0;
-      for (int j = 0; j < 4; j++) {
-        double pr = 1;
-        for (int i = 0; i < 4; i++) pr *= hist[(h_pats[k].mpG[j] >> (8 * i)) & 0xFF] / tot;
-        r += pr;
-      }
-      (*rates)[k] = r;
-    }
-}
-
 // Run a batch whose params are on the device as sub-batches under the scratch
 // budget (~338 B per 2 KiB segment per pattern: counts, list, bitmap, offset,
 // queue; a third of free memory, <= 16 GiB), chained through d_offsets.
-static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, const double* rates, int K,
-                     const uint8_t* d_text, int64_t n, int64_t* d_out, int64_t cap, int64_t* d_offsets, cudaStream_t st,
-                     const uint32_t* mp_dev, const std::pair<int64_t, int>* mp_chunks) {
+static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text, int64_t n,
+                     int64_t* d_out, int64_t cap, int64_t* d_offsets, cudaStream_t st, const BatchPass* bp,
+                     const uint32_t* d_tab) {
   CUDA_TRY(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
   const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 338.0;
   double budget = 1.0 * (1ULL << 30);  // batches needing <= 1 GiB of scratch skip the memory query
@@ -793,13 +919,13 @@ static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, cons
     budget = std::max(budget, std::min<double>((double)free_b / 3.0, 16.0 * (1ULL << 30)));
   }
   int kc = (int)std::max<double>(1.0, std::min<double>((double)K, budget / per_pattern));
-  if (kc < K && kc >= MP_CHUNK) kc -= kc % MP_CHUNK;  // keep prepared MP tables aligned to sub-batches
+  if (kc < K && kc >= MP_CHUNK) kc -= kc % MP_CHUNK;  // keep the pass tables' chunks aligned to sub-batches
   for (int k0 = 0; k0 < K; k0 += kc) {
     const int kk = std::min(kc, K - k0);
-    const bool aligned = mp_dev && (k0 % MP_CHUNK) == 0;
-    int rc = run_search(c, d_pats + k0, h_pats + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st, rates + k0,
-                        k0 ? d_offsets + k0 : nullptr, aligned ? mp_dev : nullptr,
-                        aligned ? mp_chunks + k0 / MP_CHUNK : nullptr);
+    // the pass runs on sub-batches made of whole table chunks
+    const bool whole = bp && bp->kind && (k0 % MP_CHUNK) == 0 && (kk % MP_CHUNK == 0 || k0 + kk == K);
+    int rc = run_search(c, d_pats + k0, h_pats + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st,
+                        k0 ? d_offsets + k0 : nullptr, whole ? bp : nullptr, whole ? d_tab : nullptr, k0 / MP_CHUNK);
     if (rc) return rc;
   }
   return MB_OK;
@@ -822,9 +948,12 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
   if ((rc = grow(&c->d_pats, &c->pats_cap, K, "batch params"))) return rc;
   if ((rc = stage_begin(c))) return rc;
   if ((rc = stage_upload(c, c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, st))) return rc;
-  batch_rates(plans, c->h_pats.data(), K, &c->h_rate);
-  rc = run_batch(c, c->d_pats, c->h_pats.data(), c->h_rate.data(), K, d_text, n, d_out, cap, d_offsets, st, nullptr,
-                 nullptr);
+  plan_pass(plans, c->h_pats.data(), K, &c->pass);
+  if (c->pass.kind) {
+    if ((rc = grow(&c->mp_tab, &c->mp_tab_cap, c->pass.words(), "batch pass tables"))) return rc;
+    if ((rc = stage_upload(c, c->mp_tab, c->pass.img.data(), sizeof(uint32_t) * c->pass.img.size(), st))) return rc;
+  }
+  rc = run_batch(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets, st, &c->pass, c->mp_tab);
   const int rc2 = stage_end(c, st);
   return rc ? rc : rc2;
 }
@@ -845,19 +974,8 @@ int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out) {
     b->h_pats[k] = plans[k]->dview;
   }
   cudaGetDevice(&b->device);
-  batch_rates(plans, b->h_pats.data(), K, &b->rates);
-  std::vector<uint32_t> img;
-  bool all_long = true;  // every pattern has K5 grams (m >= 7)
-  for (int k = 0; k < K; k++) all_long &= b->h_pats[k].m >= 7;
-  if (all_long && K >= 8)
-    for (int k0 = 0; k0 < K; k0 += MP_CHUNK) {
-      std::vector<uint32_t> one;
-      int B = 0;
-      mp_tables(b->h_pats.data(), k0, std::min(MP_CHUNK, K - k0), &B, one);
-      b->mp_chunks.push_back({(int64_t)img.size(), B});
-      img.insert(img.end(), one.begin(), one.end());
-      while (img.size() % 4) img.push_back(0);
-    }
+  plan_pass(plans, b->h_pats.data(), K, &b->pass);
+  const std::vector<uint32_t>& img = b->pass.img;
   if (cudaMalloc(&b->d_pats, sizeof(PatDev) * K) != cudaSuccess ||
       (!img.empty() && cudaMalloc(&b->d_mp, sizeof(uint32_t) * img.size()) != cudaSuccess)) {
     cudaFree(b->d_pats);
@@ -893,8 +1011,8 @@ int mb_find_batch_prepared(mb_ctx* c, const mb_batch* b, const uint8_t* d_text, 
   if (dev != b->device) return fail(MB_EINVAL, "batch was prepared on another device");
   int rc = stage_begin(c);
   if (rc) return rc;
-  rc = run_batch(c, b->d_pats, b->h_pats.data(), b->rates.data(), b->K, d_text, n, d_out, cap, d_offsets,
-                 (cudaStream_t)stream, b->d_mp, b->mp_chunks.empty() ? nullptr : b->mp_chunks.data());
+  rc = run_batch(c, b->d_pats, b->h_pats.data(), b->K, d_text, n, d_out, cap, d_offsets, (cudaStream_t)stream,
+                 &b->pass, b->d_mp);
   const int rc2 = stage_end(c, (cudaStream_t)stream);
   return rc ? rc : rc2;
 }

@@ -15,6 +15,50 @@ namespace mb {
 // segment or tile): one 16-bit atomic count and an (unordered) list slot;
 // offsets/expand are shared (expand sorts MP lists).  Segments above LIST_CAP
 // set `overflow` and the per-pattern scans re-run the batch on the device.
+// A verified occurrence of batch pattern k whose family scan would set bit b
+// (virtual start + delta): one 16-bit atomic count and an unordered list slot
+// in the segment holding b (segment layout of ScanParams); overflow past
+// LIST_CAP hands the pattern to its per-pattern scan (need[k], any-flag).
+__device__ __forceinline__ void mp_record(const MPParams& P, int k, int64_t b) {
+  const int64_t tb = b / TILE;
+  MB_CHECK(b >= 0 && tb < P.ntiles);
+  const int64_t g = ((int64_t)k * P.ntiles + tb) * NWARP + (b - tb * TILE) / SEG;
+  unsigned int* wptr = reinterpret_cast<unsigned int*>(P.counts) + (g >> 1);
+  const unsigned int sh = 16u * (unsigned)(g & 1);
+  const unsigned int old = (atomicAdd(wptr, 1u << sh) >> sh) & 0xFFFFu;
+  if (old < (unsigned)LIST_CAP) {
+    P.lists[g * LIST_CAP + old] = (uint16_t)(b - tb * TILE);
+  } else {  // this pattern falls back to its own family scan
+    P.need[k] = 1u;
+    atomicExch(P.overflow, 1u);
+  }
+}
+
+// TMA producer of the batched passes: text tiles (+ halo) into the ring.
+__device__ __forceinline__ void mp_produce(const MPParams& P, StageHdr* hdr, uint64_t* full, uint64_t* empty,
+                                           uint8_t* stages) {
+  for (int it = 0;; it++) {
+    const int s = it % STAGES;
+    if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
+    const unsigned long long tk = atomicAdd(P.ticket, 1ULL);
+    if ((int64_t)tk >= P.ntiles_text) {
+      hdr[s].tk = -1;
+      mbar_arrive(&full[s]);
+      break;
+    }
+    hdr[s].tk = (int64_t)tk;
+    hdr[s].tau = (int64_t)tk;
+    const int64_t start = (int64_t)tk * TILE - P.pre;
+    const int64_t end = (int64_t)tk * TILE + TILE + P.post;
+    const int64_t cs = start < 0 ? 0 : start;
+    const int64_t ce = end > P.nv16 ? P.nv16 : end;
+    const uint32_t tb = ce > cs ? (uint32_t)(ce - cs) : 0u;
+    uint8_t* st = stages + s * P.stage_bytes;
+    mbar_expect_tx(&full[s], tb);
+    if (tb) bulk_g2s(st + (cs - start), P.text + cs, tb, &full[s]);
+  }
+}
+
 __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
   StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
@@ -38,28 +82,7 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   __syncthreads();
 
   if (warp == NWARP) {  // ---------------- producer: text tiles only
-    if (lane == 0) {
-      for (int it = 0;; it++) {
-        const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
-        const unsigned long long tk = atomicAdd(P.ticket, 1ULL);
-        if ((int64_t)tk >= P.ntiles_text) {
-          hdr[s].tk = -1;
-          mbar_arrive(&full[s]);
-          break;
-        }
-        hdr[s].tk = (int64_t)tk;
-        hdr[s].tau = (int64_t)tk;
-        const int64_t start = (int64_t)tk * TILE - P.pre;
-        const int64_t end = (int64_t)tk * TILE + TILE + P.post;
-        const int64_t cs = start < 0 ? 0 : start;
-        const int64_t ce = end > P.nv16 ? P.nv16 : end;
-        const uint32_t tb = ce > cs ? (uint32_t)(ce - cs) : 0u;
-        uint8_t* st = stages + s * P.stage_bytes;
-        mbar_expect_tx(&full[s], tb);
-        if (tb) bulk_g2s(st + (cs - start), P.text + cs, tb, &full[s]);
-      }
-    }
+    if (lane == 0) mp_produce(P, hdr, full, empty, stages);
     return;
   }
 
@@ -105,18 +128,96 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
           bool ok = true;
           for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);
           if (!ok) continue;
-          // the family scan's bit for start sv: b = sv + delta (virtual, off included)
-          const int64_t b = sv + pd->delta;
-          const int64_t tb = b / TILE;
-          MB_CHECK(b >= 0 && tb < P.ntiles);
-          const int64_t g = ((int64_t)(P.kbase + kl) * P.ntiles + tb) * NWARP + (b - tb * TILE) / SEG;
-          unsigned int* wptr = reinterpret_cast<unsigned int*>(P.counts) + (g >> 1);
-          const unsigned int sh = 16u * (unsigned)(g & 1);
-          const unsigned int old = (atomicAdd(wptr, 1u << sh) >> sh) & 0xFFFFu;
-          if (old < (unsigned)LIST_CAP)
-            P.lists[g * LIST_CAP + old] = (uint16_t)(b - tb * TILE);
-          else
-            atomicExch(P.overflow, 1u);
+          mp_record(P, P.kbase + kl, sv + pd->delta);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+// ------------------------------------------------ kernel 1d: batched pass over every byte offset (K5b "MPB")
+// For batches the aligned-word pass cannot take (patterns shorter than 7,
+// small alphabets): each pattern contributes one q-byte gram (its rarest, at
+// offset a_k; q in {2, 3, 4, 8} for the whole batch) and every text position's
+// q-byte window is hashed once: bloom bit in smem, then a bucket of
+// {gram, pattern, a_k} entries, the full pattern verified in the staged tile,
+// the occurrence recorded as in the aligned pass.  Q = q.
+template <int Q>
+__global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
+  uint8_t* stages = smem + SM_STAGES;
+  uint32_t* bloom = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes);
+  uint32_t* bstart = bloom + 2048;
+  uint4* ents = reinterpret_cast<uint4*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 2048; i += NT + 32) bloom[i] = P.bloom[i];
+  for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
+  for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents4[i];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NWARP) {
+    if (lane == 0) mp_produce(P, hdr, full, empty, stages);
+    return;
+  }
+  constexpr uint32_t QMASK = Q >= 4 ? 0xFFFFFFFFu : ((1u << (8 * Q)) - 1u);
+  const int c0 = warp * SEG;
+  for (int it = 0;; it++) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+    const int64_t tau = hdr[s].tk;
+    if (tau < 0) break;
+    const int64_t B0 = tau * TILE;
+    const uint8_t* S = stages + s * P.stage_bytes + P.pre;  // S[c] = virtual byte B0 + c
+#pragma unroll 1
+    for (int r = 0; r < SEG / 512; r++) {
+      const int c = c0 + r * 512 + lane * 16;
+      MB_CHECK(S + c + 24 <= stages + (s + 1) * P.stage_bytes);
+      const uint4 X = *reinterpret_cast<const uint4*>(S + c);
+      const uint2 Y = *reinterpret_cast<const uint2*>(S + c + 16);
+      const uint32_t w[6] = {X.x, X.y, X.z, X.w, Y.x, Y.y};
+      uint32_t hits = 0;
+#pragma unroll
+      for (int p = 0; p < 16; p++) {
+        const uint32_t lo = __funnelshift_r(w[p >> 2], w[(p >> 2) + 1], 8 * (p & 3)) & QMASK;
+        const uint32_t hi = Q == 8 ? __funnelshift_r(w[(p >> 2) + 1], w[(p >> 2) + 2], 8 * (p & 3)) : 0u;
+        const uint32_t h = lo * 0x9E3779B1u ^ hi * 0x85EBCA77u;
+        hits |= ((bloom[h >> 21] >> ((h >> 16) & 31)) & 1u) << p;
+      }
+      while (hits) {  // bucket walk + verification
+        const int p = __ffs(hits) - 1;
+        hits &= hits - 1;
+        const uint32_t lo = __funnelshift_r(w[p >> 2], w[(p >> 2) + 1], 8 * (p & 3)) & QMASK;
+        const uint32_t hi = Q == 8 ? __funnelshift_r(w[(p >> 2) + 1], w[(p >> 2) + 2], 8 * (p & 3)) : 0u;
+        const uint32_t h = lo * 0x9E3779B1u ^ hi * 0x85EBCA77u;
+        const uint32_t bk = h >> (32 - P.B);
+        const int64_t x = B0 + c + p;  // virtual position of the window
+        for (uint32_t e = bstart[bk]; e < bstart[bk + 1]; e++) {
+          const uint4 en = ents[e];
+          if (en.x != lo || en.y != hi) continue;
+          const int kl = (int)(en.z >> 16);
+          const int a = (int)(en.z & 0xFFFFu);
+          const int64_t sv = x - a;  // virtual start
+          const int64_t spos = sv - P.off;
+          const PatDev* pd = P.pats + P.kbase + kl;
+          const int64_t m = pd->m;
+          if (spos < 0 || spos + m > P.n) continue;
+          const uint8_t* tp = S + (sv - B0);
+          MB_CHECK(tp >= stages + s * P.stage_bytes && tp + m <= stages + (s + 1) * P.stage_bytes);
+          const uint8_t* pp = pd->bytes;
+          bool ok = true;
+          for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);
+          if (ok) mp_record(P, P.kbase + kl, sv + pd->delta);
         }
       }
     }

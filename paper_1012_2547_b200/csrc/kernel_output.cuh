@@ -9,6 +9,21 @@ namespace mb {
 // ticket order taken at CTA start (no prefetch), so each chunk only waits on
 // chunks already running -- the decoupled look-back never stalls on a queued
 // predecessor.
+// 8-input sorting network (19 compare-exchanges)
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
+  const uint32_t lo = min(a, b), hi = max(a, b);
+  a = lo;
+  b = hi;
+}
+__device__ __forceinline__ void sort8(uint32_t* v) {
+  cswap(v[0], v[2]); cswap(v[1], v[3]); cswap(v[4], v[6]); cswap(v[5], v[7]);
+  cswap(v[0], v[4]); cswap(v[1], v[5]); cswap(v[2], v[6]); cswap(v[3], v[7]);
+  cswap(v[0], v[1]); cswap(v[2], v[3]); cswap(v[4], v[5]); cswap(v[6], v[7]);
+  cswap(v[2], v[4]); cswap(v[3], v[5]);
+  cswap(v[1], v[4]); cswap(v[3], v[6]);
+  cswap(v[1], v[2]); cswap(v[3], v[4]); cswap(v[5], v[6]);
+}
+
 template <int PER>  // counts per thread: chunk = NT * PER (host picks PER for >= 2 chunks per SM)
 __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   __shared__ int64_t wsum[NWARP];
@@ -97,7 +112,10 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   const int64_t seg_per_pat = P.ntiles * NWARP;
   // Sorted sparse segments (<= LIST_CAP uint16 offsets) are expanded right here;
   // dense or unsorted (MP) segments are queued for expand_kernel with their offset.
-  const bool fuse = P.out && !P.unsorted_lists;
+  // sorted lists are expanded here whole; unsorted (batch-pass) lists up to 8
+  // entries are sorted in registers (a 19-comparator network) and expanded
+  // here too, longer ones go to expand_kernel's warp sort
+  const uint32_t fuse_max = !P.out ? 0u : P.unsorted_lists ? 8u : (uint32_t)LIST_CAP;
   int cur_k = -1;
   int64_t shift = 0;
   // pattern of this thread's first segment and the segment's rank within it
@@ -116,7 +134,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     const uint32_t vq = (s_cnt[(q >> 1) * NT + tid] >> (16 * (q & 1))) & 0xFFFFu;
     if (t < nseg) {
       if (vq && P.out) {
-        if (fuse && vq <= (uint32_t)LIST_CAP) {
+        if (vq <= fuse_max) {
           const int64_t tile = t / NWARP;
           const int k = (int)(tile / P.ntiles);
           if (k != cur_k) {
@@ -125,8 +143,21 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
           }
           const int64_t pos0 = (tile % P.ntiles) * TILE - shift;
           const uint16_t* L = P.lists + t * LIST_CAP;
-          for (uint32_t e = 0; e < vq; e++)
-            if (run + e < P.cap) P.out[run + e] = pos0 + L[e];
+          if (!P.unsorted_lists) {
+            for (uint32_t e = 0; e < vq; e++)
+              if (run + e < P.cap) P.out[run + e] = pos0 + L[e];
+          } else {
+            const uint4 raw = *reinterpret_cast<const uint4*>(L);  // 8 slots (64-byte aligned list)
+            uint32_t v[8] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16,
+                             raw.z & 0xFFFFu, raw.z >> 16, raw.w & 0xFFFFu, raw.w >> 16};
+#pragma unroll
+            for (int e = 0; e < 8; e++)
+              if ((uint32_t)e >= vq) v[e] = 0xFFFFFFFFu;
+            sort8(v);
+#pragma unroll
+            for (int e = 0; e < 8; e++)
+              if ((uint32_t)e < vq && run + e < P.cap) P.out[run + e] = pos0 + v[e];
+          }
         } else {
           P.toff[t] = run;
           const unsigned long long slot = atomicAdd(&P.ticket[TICKET_DENSE], 1ULL);

@@ -77,6 +77,10 @@ __global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const Scan
     if (t >= total) break;
     const int kg = (int)(t / units);
     const int k = P.plist ? P.plist[kg] : kg;  // family group -> batch index
+    if (P.need && !P.need[k]) {  // covered by the batch pass: jump to the next pattern's units
+      if (tid == 0) atomicMax(&P.ticket[P.ticket_slot], (unsigned long long)(kg + 1) * (unsigned long long)units);
+      continue;
+    }
     const int64_t u = t - (int64_t)kg * units;
     if (k != cur_k) {  // load this pattern's tables (uniform across the CTA)
       pd = P.pats[k];

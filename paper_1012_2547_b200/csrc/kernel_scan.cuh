@@ -42,14 +42,22 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
       for (int it = 0;; it++) {
         const int s = it % NS;
         if (it >= NS) mbar_wait(&empty[s], (uint32_t)(it / NS - 1) & 1u);
-        const unsigned long long tk = atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
+        unsigned long long tk;
+        int kg = 0, k = 0;
+        for (;;) {
+          tk = atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
+          if ((int64_t)tk >= P.group_tiles) break;
+          kg = (int)((int64_t)tk / P.ntiles);
+          k = P.plist ? P.plist[kg] : kg;  // this launch's family group -> batch index
+          if (!P.need || P.need[k]) break;
+          // covered by the batch pass: jump the counter to the next pattern's tiles
+          atomicMax(&P.ticket[P.ticket_slot], (unsigned long long)(kg + 1) * (unsigned long long)P.ntiles);
+        }
         if ((int64_t)tk >= P.group_tiles) {
           hdr[s].tk = -1;
           mbar_arrive(&full[s]);
           break;
         }
-        const int kg = (int)((int64_t)tk / P.ntiles);
-        const int k = P.plist ? P.plist[kg] : kg;  // this launch's family group -> batch index
         const int64_t tau = (int64_t)tk - (int64_t)kg * P.ntiles;
         hdr[s].tk = (int64_t)k * P.ntiles + tau;   // global tile id (segment index base)
         hdr[s].k = k;

@@ -93,7 +93,8 @@ struct ScanParams {
   int64_t* offsets_plus1;   // entry k <- inclusive prefix after pattern k
   const int64_t* out_base;  // device: output index where this launch starts (null = 0)
   int unsorted_lists;       // lists were filled in arbitrary order (MP path): sort on expand
-  const unsigned int* run_if;  // count kernels exit at once unless *run_if != 0 (MP fallback)
+  const unsigned int* run_if;  // count kernels exit at once unless *run_if != 0 (batch-pass fallback)
+  const unsigned int* need;    // per batch pattern: 0 = the batch pass covered it (skip its tiles), else scan
 };
 
 // Batched multi-pattern single pass (K5 "MP"): every anchor gram of every
@@ -107,13 +108,15 @@ struct MPParams {
   unsigned long long* ticket;
   const uint32_t* bloom;   // 65536 bits over gram * 0x9E3779B1 >> 16
   const uint32_t* bstart;  // (1 << B) + 1 bucket starts
-  const uint2* ents;       // {gram, (batch index << 16) | (anchor + j)} sorted by bucket
+  const uint2* ents;       // aligned pass: {gram, (batch index << 16) | (anchor + j)} sorted by bucket
+  const uint4* ents4;      // byte-offset pass: {gram lo, gram hi, (batch index << 16) | a, 0} sorted by bucket
   int B, nents;
   int kbase;               // batch index of this chunk's first pattern
   const PatDev* pats;      // whole batch
   uint16_t* counts;        // segment layout, zeroed before the launch
   uint16_t* lists;
-  unsigned int* overflow;  // set if a segment exceeds LIST_CAP (host re-runs the segment path)
+  unsigned int* overflow;  // any-flag: some pattern needs its per-pattern scan (run_if of the scans)
+  unsigned int* need;      // per batch pattern: set when one of its segments exceeds LIST_CAP
 };
 
 }  // namespace mb

@@ -266,6 +266,42 @@ def test_mp_mixed_family_batch(cuda):
             assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(p, t)), (k, len(p))
 
 
+@pytest.mark.parametrize("sigma,lo,hi", [(16, 2, 3), (64, 4, 6), (256, 2, 9), (4, 8, 20), (8, 5, 40), (32, 3, 300)])
+def test_mpb_byte_offset_pass(cuda, sigma, lo, hi):
+    """K5b byte-offset pass (short patterns / small alphabets): planted edges,
+    duplicates, patterns longer than the text; ad-hoc and prepared batches."""
+    rng = np.random.default_rng(sigma * 100 + lo)
+    n = 3 * TILE + 777
+    t = bytearray(rand_bytes(rng, sigma, n))
+    ms = rng.integers(lo, hi + 1, 240)
+    pats = [bytes(t[i : i + m]) for i, m in zip(rng.integers(0, n - hi, 240), ms)]
+    pats += [pats[0], rand_bytes(rng, sigma, lo), rand_bytes(rng, sigma, hi)]
+    for s in (0, 1, SEG - 1, TILE - 2, n - len(pats[3])):
+        t[s : s + len(pats[3])] = pats[3]
+    t = bytes(t)
+    d = torch.from_numpy(np.frombuffer(t, dtype=np.uint8).copy()).cuda()
+    plans = [engine.Plan(p) for p in pats]
+    for obj in (plans, engine.Batch(plans)):
+        before = engine.mp_batches()
+        pos, offs = engine.find_batch(obj, d)
+        assert engine.mp_batches() == before + 1, "batch did not take a batched pass"
+        pos = pos.cpu().numpy()
+        for k, p in enumerate(pats):
+            assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(p, t)), (k, p)
+
+
+def test_mpb_overflow_falls_back(cuda):
+    # selective-looking short patterns, but one of them repeats > LIST_CAP times in a segment
+    rng = np.random.default_rng(77)
+    t = bytearray(rand_bytes(rng, 64, 2 * TILE))
+    t[5000:5400] = b"xy" * 200
+    t = bytes(t)
+    pats = [t[i : i + 2] for i in rng.integers(0, len(t) - 2, 40)] + [b"xy", b"yx"]
+    res = mb.search_many(pats, t)
+    for p, r in zip(pats, res):
+        assert r == oracle.search(p, t).tolist()
+
+
 def test_prepared_batch_matches_adhoc(cuda):
     rng = np.random.default_rng(44)
     t = rand_bytes(rng, 128, 4 * TILE)

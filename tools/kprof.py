@@ -13,10 +13,19 @@ if mode == "cfg5":
     c = engine.count(pl, d)
     out = torch.empty(max(c, 1), dtype=torch.int64, device="cuda"); cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     run = lambda: engine.find_into(pl, d, out, cnt)
+elif mode == "rand":  # rand <MiB> <m> <family>
+    n, m, fam = int(sys.argv[2]) << 20, int(sys.argv[3]), sys.argv[4]
+    t = inputs.rand_text_np(256, n, 11); d = torch.from_numpy(t).cuda()
+    pl = engine.Plan(t[n // 2 : n // 2 + m].tobytes(), fam)
+    c = engine.count(pl, d)
+    out = torch.empty(max(c, 1), dtype=torch.int64, device="cuda"); cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    run = lambda: engine.find_into(pl, d, out, cnt)
 else:
     sigma, m = int(sys.argv[2]), int(sys.argv[3])
-    t = inputs.config2_text(sigma); d = torch.from_numpy(t).cuda()
-    b = engine.Batch([engine.Plan(p) for p in inputs.config2_patterns(t, sigma, m)])
+    t = inputs.config2_text(sigma) if sigma != 95 else inputs.config3()
+    d = torch.from_numpy(t).cuda()
+    pats = inputs.config2_patterns(t, sigma, m) if sigma != 95 else inputs.config3_patterns(t, m)
+    b = engine.Batch([engine.Plan(p) for p in pats])
     offs = torch.zeros(501, dtype=torch.int64, device="cuda")
     engine.find_batch_into(b, d, None, offs); out = torch.empty(max(int(offs[-1]), 1), dtype=torch.int64, device="cuda")
     run = lambda: engine.find_batch_into(b, d, out, offs)
