@@ -91,6 +91,7 @@ __device__ __forceinline__ uint32_t shr8(uint32_t lo, uint32_t hi, int k) {
 // K1 / m <= 3: byte d of x_k is zero iff t[v..v+m) == p (v = 4k + d).
 template <int M>
 struct FiltSWAR {
+  static constexpr bool kAlwaysExact = true;  // no verification code in this instantiation
   __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
     uint32_t x[4], acc = 0;
 #pragma unroll
@@ -168,6 +169,11 @@ struct FiltSO {
   static constexpr bool kShiftOr = true;
   static constexpr int kW = W;
 };
+template <class F, class = void>
+struct always_exact : std::false_type {};
+template <class F>
+struct always_exact<F, std::void_t<decltype(F::kAlwaysExact)>> : std::true_type {};
+
 template <class F, class = void>
 struct is_shiftor : std::false_type {};
 template <class F>

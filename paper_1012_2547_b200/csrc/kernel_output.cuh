@@ -69,38 +69,48 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     wbefore += q < warp ? wsum[q] : 0;
   }
   // block-wide decoupled look-back: the whole CTA reads NT predecessors per
-  // round trip (a 16 GiB single-pattern search has 512 chunks: one round trip)
-  __shared__ int s_incl_min;
-  __shared__ unsigned long long s_sum;
+  // round trip (a 16 GiB single-pattern search has 512 chunks: one round
+  // trip); the nearest inclusive predecessor and the sum up to it are found
+  // with warp ballots / shuffles and one word per warp in smem (no smem atomics)
+  __shared__ int s_first[NWARP];
+  __shared__ unsigned long long s_part[NWARP];
   if (tid == 0) {
     st_relaxed(&P.state[ch], pack_state(P.epoch, ch == 0 ? ST_INCL : ST_AGG, (uint64_t)chunk_total));
     s_excl = 0;
   }
   int64_t j = ch - 1;  // newest predecessor of this window
-  while (j >= 0) {     // uniform across the CTA (j, s_incl_min read after barriers)
-    if (tid == 0) {
-      s_incl_min = 0x7fffffff;
-      s_sum = 0;
-    }
-    __syncthreads();
+  while (j >= 0) {     // uniform across the CTA (j, first read after barriers)
     const int64_t idx = j - tid;
     uint64_t sv = 0;
+    bool incl = false;
     if (idx >= 0) {
       while (true) {
         sv = ld_relaxed(&P.state[idx]);
         if ((uint32_t)(sv >> 40) == P.epoch && ((sv >> 38) & 3)) break;
         __nanosleep(20);
       }
-      if (((sv >> 38) & 3) == ST_INCL) atomicMin(&s_incl_min, tid);
+      incl = ((sv >> 38) & 3) == ST_INCL;
     }
+    const uint32_t bi = __ballot_sync(0xffffffffu, incl);
+    if (lane == 0) s_first[warp] = bi ? warp * 32 + __ffs(bi) - 1 : 0x7fffffff;
     __syncthreads();
-    const int first = s_incl_min;  // nearest predecessor holding an inclusive prefix
-    if (idx >= 0 && tid <= first) atomicAdd(&s_sum, (unsigned long long)(sv & ((1ULL << 38) - 1)));
+    int first = 0x7fffffff;  // nearest predecessor holding an inclusive prefix
+#pragma unroll
+    for (int w = 0; w < NWARP; w++) first = min(first, s_first[w]);
+    unsigned long long v = (idx >= 0 && tid <= first) ? (sv & ((1ULL << 38) - 1)) : 0ULL;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+    if (lane == 0) s_part[warp] = v;
     __syncthreads();
-    if (tid == 0) s_excl += (int64_t)s_sum;
+    if (tid == 0) {
+      unsigned long long sum = 0;
+#pragma unroll
+      for (int w = 0; w < NWARP; w++) sum += s_part[w];
+      s_excl += (int64_t)sum;
+    }
     if (first != 0x7fffffff || j - NT < 0) break;
     j -= NT;
-    __syncthreads();
+    __syncthreads();  // s_first / s_part are rewritten next round
   }
   __syncthreads();
   if (tid == 0) {

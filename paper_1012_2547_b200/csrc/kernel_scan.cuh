@@ -39,9 +39,11 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
 
   if (warp == NWARP) {  // ---------------- producer
     if (lane == 0) {
+      // ring position without divisions: stage s, its use count's parity ph
+      int s = 0;
+      uint32_t ph = 0;
       for (int it = 0;; it++) {
-        const int s = it % NS;
-        if (it >= NS) mbar_wait(&empty[s], (uint32_t)(it / NS - 1) & 1u);
+        if (it >= NS) mbar_wait(&empty[s], ph ^ 1u);
         unsigned long long tk;
         int kg = 0, k = 0;
         for (;;) {
@@ -73,6 +75,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
         mbar_expect_tx(&full[s], tb + pb);
         bulk_g2s(st, pd->bytes, pb, &full[s]);
         if (tb) bulk_g2s(st + P.pat_cap + (cs - start), P.text + cs, tb, &full[s]);
+        if (++s == NS) s = 0, ph ^= 1u;
       }
     }
     return;
@@ -83,9 +86,10 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   int cur_k = -1;
   PatDev pd;
   int64_t blo = 0, bhi = -1;
-  for (int it = 0;; it++) {
-    const int s = it % NS;
-    mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
+  int s = 0;
+  uint32_t ph = 0;
+  for (;; s = (s + 1 == NS) ? (ph ^= 1u, 0) : s + 1) {
+    mbar_wait(&full[s], ph);
     const int64_t tk = hdr[s].tk;
     if (tk < 0) break;
     const int k = hdr[s].k;
@@ -162,7 +166,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
     uint32_t cnt = 0;
     if (have) {
       // ---- verify (exact filters skip this)
-      if (!pd.exact && __any_sync(0xffffffffu, (w0 | w1) != 0)) {
+      if (!always_exact<Filt>::value && !is_shiftor<Filt>::value && !pd.exact &&
+          __any_sync(0xffffffffu, (w0 | w1) != 0)) {
         const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
         if (pd.periodic) {
           // s matches <=> t[s..s+per) = p[0..per) and no break t[y] != t[y+per] for
