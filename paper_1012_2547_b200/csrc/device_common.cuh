@@ -67,6 +67,19 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// (pattern, tile within the pattern) of a global tile index: 32-bit division
+// while the index fits (every realistic batch), 64-bit otherwise
+__device__ __forceinline__ void split_tile(int64_t tile, int64_t ntiles, int* k, int64_t* tau) {
+  if ((uint64_t)tile < 0xFFFFFFFFull && (uint64_t)ntiles < 0xFFFFFFFFull) {
+    const uint32_t q = (uint32_t)tile / (uint32_t)ntiles;
+    *k = (int)q;
+    *tau = (int64_t)((uint32_t)tile - q * (uint32_t)ntiles);
+  } else {
+    *k = (int)(tile / ntiles);
+    *tau = tile - (int64_t)*k * ntiles;
+  }
+}
+
 // look-back flag word: [epoch:24][status:2][value:38]
 constexpr uint64_t ST_AGG = 1, ST_INCL = 2;
 __device__ __forceinline__ uint64_t pack_state(uint32_t epoch, uint64_t st, uint64_t val) {
@@ -103,7 +116,7 @@ struct FiltSWAR {
       acc |= (v - 0x01010101u) & ~v;
     }
     if (!(acc & 0x80808080u)) return 0;
-    uint32_t mk = 0;
+    uint32_t mk = 0;  // per-word IMAD packing keeps part of this off the ALU pipe
 #pragma unroll
     for (int k = 0; k < 4; k++) mk |= zero_bytes4(x[k]) << (4 * k);
     return mk;

@@ -146,12 +146,14 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
       if (vq && P.out) {
         if (vq <= fuse_max) {
           const int64_t tile = t / NWARP;
-          const int k = (int)(tile / P.ntiles);
+          int k;
+          int64_t tau;
+          split_tile(tile, P.ntiles, &k, &tau);
           if (k != cur_k) {
             shift = P.pats[k].delta + P.off;
             cur_k = k;
           }
-          const int64_t pos0 = (tile % P.ntiles) * TILE - shift;
+          const int64_t pos0 = tau * TILE - shift;
           const uint16_t* L = P.lists + t * LIST_CAP;
           if (!P.unsorted_lists) {
             for (uint32_t e = 0; e < vq; e++)
@@ -229,12 +231,14 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
     const uint32_t c = cur.c;
     const int64_t o = cur.o;
     const int64_t tile = g / NWARP;
-    const int k = (int)(tile / P.ntiles);
+    int k;
+    int64_t tau;
+    split_tile(tile, P.ntiles, &k, &tau);
     if (k != cur_k) {
       shift = P.pats[k].delta + P.off;
       cur_k = k;
     }
-    const int64_t pos0 = (tile % P.ntiles) * TILE - shift;  // tile-relative offsets below
+    const int64_t pos0 = tau * TILE - shift;  // tile-relative offsets below
     if (o < P.cap) {
       if (c <= LIST_CAP) {
         uint32_t v = lane < (int)c ? (cur.lv & 0xFFFFu) : 0xFFFFFFFFu;

@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
         for (;;) {
           tk = atomicAdd(&P.ticket[P.ticket_slot], 1ULL);
           if ((int64_t)tk >= P.group_tiles) break;
-          kg = (int)((int64_t)tk / P.ntiles);
+          int64_t tau_unused;
+          split_tile((int64_t)tk, P.ntiles, &kg, &tau_unused);
           k = P.plist ? P.plist[kg] : kg;  // this launch's family group -> batch index
           if (!P.need || P.need[k]) break;
           // covered by the batch pass: jump the counter to the next pattern's tiles
