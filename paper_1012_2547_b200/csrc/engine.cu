@@ -147,6 +147,7 @@ struct mb_ctx {
   int64_t mp_tab_cap = 0;
   uint32_t* need = nullptr;    // per-pattern scan flags of a batch pass
   int64_t need_cap = 0;
+  double scratch_ok = 0;       // batch scratch bytes known to fit (skips the free-memory query)
   BatchPass pass;  // ad-hoc batches: planned per call
   int64_t mp_batches = 0;
   uint32_t epoch = 0;
@@ -910,13 +911,16 @@ static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int 
                      const uint32_t* d_tab) {
   CUDA_TRY(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
   const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 338.0;
-  double budget = 1.0 * (1ULL << 30);  // batches needing <= 1 GiB of scratch skip the memory query
+  // batches needing <= 1 GiB of scratch, or no more than a previous call
+  // already got, skip the memory query (cudaMemGetInfo costs up to ms)
+  double budget = std::max(1.0 * (1ULL << 30), c->scratch_ok);
   if (const char* env = getenv("MB_SCRATCH_BUDGET")) {
     budget = atof(env);  // tests force sub-batching
   } else if (per_pattern * K > budget) {
     size_t free_b = 0, total_b = 0;
     CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
     budget = std::max(budget, std::min<double>((double)free_b / 3.0, 16.0 * (1ULL << 30)));
+    c->scratch_ok = std::max(c->scratch_ok, std::min(budget, per_pattern * K));
   }
   int kc = (int)std::max<double>(1.0, std::min<double>((double)K, budget / per_pattern));
   if (kc < K && kc >= MP_CHUNK) kc -= kc % MP_CHUNK;  // keep the pass tables' chunks aligned to sub-batches

@@ -9,6 +9,11 @@ namespace mb {
 // ticket order taken at CTA start (no prefetch), so each chunk only waits on
 // chunks already running -- the decoupled look-back never stalls on a queued
 // predecessor.
+#ifndef MB_FUSE_MAX
+#define MB_FUSE_MAX 16
+#endif
+constexpr int FUSE_MAX = MB_FUSE_MAX;  // sorted lists; unsorted ones at most 8 (the sort network's width)
+
 // 8-input sorting network (19 compare-exchanges)
 __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
   const uint32_t lo = min(a, b), hi = max(a, b);
@@ -122,10 +127,11 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   const int64_t seg_per_pat = P.ntiles * NWARP;
   // Sorted sparse segments (<= LIST_CAP uint16 offsets) are expanded right here;
   // dense or unsorted (MP) segments are queued for expand_kernel with their offset.
-  // sorted lists are expanded here whole; unsorted (batch-pass) lists up to 8
-  // entries are sorted in registers (a 19-comparator network) and expanded
-  // here too, longer ones go to expand_kernel's warp sort
-  const uint32_t fuse_max = !P.out ? 0u : P.unsorted_lists ? 8u : (uint32_t)LIST_CAP;
+  // lists of up to FUSE_MAX entries are expanded right here by their thread
+  // (unsorted batch-pass lists sorted in registers by a 19-comparator
+  // network); longer ones go to expand_kernel, whose warp per segment writes
+  // them coalesced (a thread looping over 32 scattered stores is slower)
+  const uint32_t fuse_max = !P.out ? 0u : P.unsorted_lists ? (uint32_t)min(FUSE_MAX, 8) : (uint32_t)FUSE_MAX;
   int cur_k = -1;
   int64_t shift = 0;
   // pattern of this thread's first segment and the segment's rank within it
