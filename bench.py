@@ -31,6 +31,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+SPIN_CYCLES = 400_000  # ~0.2 ms at 1.965 GHz: covers the host enqueue of one search / batch
+
 METRIC = "text GB/s scanned (all matches emitted) vs m and σ; % of HBM roofline"
 CFG4_LENGTHS = (2, 8, 32, 128, 1024)
 PEAK_FALLBACK = 6650.0  # B200_PROFILING.md fallback, GB/s
@@ -299,6 +301,7 @@ def run_ours(args, rank, world, local_rank):
         for i, (pl, v) in enumerate(zip(plans, views)):
             if ev is not None and flush is not None:
                 flush.zero_()
+                torch.cuda._sleep(SPIN_CYCLES)  # GPU busy while the host enqueues the search
             if ev is not None:
                 ev[i][0].record(stream)
             engine.find_into(pl, v, out, cnt[i : i + 1], stream)
@@ -480,11 +483,12 @@ def run_batched_sweep(args, rank, world, local_rank):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for e0, e1 in evs:
             flush.zero_()
+            torch.cuda._sleep(SPIN_CYCLES)  # GPU busy while the host enqueues the batch: device time only
             e0.record(stream)
             engine.find_batch_into(plans, d, out, offs, stream)
             e1.record(stream)
         torch.cuda.synchronize()
-        ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+        ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
         b = len(pats) * t.size
         fams = sorted({pl.info().family for pl in plans.plans})
         rows.append({"sigma": sigma, "m": m, "patterns": len(pats), "ms": round(ms, 4),
@@ -498,7 +502,9 @@ def run_batched_sweep(args, rank, world, local_rank):
             "warmup": max(args.warmup, 3), "ms_per_step": round(tot_ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{args.workload}: batched, 500 patterns per launch (CSR)",
-                       "l2": "L2 flushed (256 MiB write) before every timed launch; value aggregated K*n/t"},
+                       "l2": "L2 flushed (256 MiB write) before every timed launch; value aggregated K*n/t",
+                       "timing": "per cell: median of the steps' CUDA-event times; a spin kernel keeps the "
+                                 "GPU busy while each launch is enqueued, so host enqueue time is excluded"},
             "cells": rows, "gpu_launches": engine.launch_count() - launches0}), flush=True)
 
 

@@ -823,10 +823,22 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       M.nents = bp->chunks[ci].nent;
       M.kbase = k0;
       M.ticket = c->ticket + TICKET_MP0 + (ci - chunk0);
-      const size_t smem = (size_t)SM_STAGES + (size_t)STAGES * M.stage_bytes + 8192 + 4 * bs_words +
-                          (size_t)4 * ent_words * M.nents;
+      auto smem_for = [&](int ns) {
+        return (size_t)SM_STAGES + (size_t)ns * M.stage_bytes + 8192 + 4 * bs_words + (size_t)4 * ent_words * M.nents;
+      };
+      // 3 stages, or for the aligned pass 2 where that keeps two CTAs per SM
+      // (big tables / halos; measured 55 -> 40 us on config 3, m = 16).  The
+      // byte-offset pass is bound by its smem bloom lookups: a second CTA
+      // does not help it and the shallower ring hurts (sigma = 2: +18%).
+      M.nstages = STAGES;
+      size_t smem = smem_for(STAGES);
       int per_sm = 0;
       CUDA_TRY(occupancy(fn, NT + 32, smem, &per_sm));
+      if (bp->kind == 1 && per_sm < 2 && STAGES > 2) {
+        int per_sm2 = 0;
+        CUDA_TRY(occupancy(fn, NT + 32, smem_for(2), &per_sm2));
+        if (per_sm2 > per_sm) M.nstages = 2, smem = smem_for(2), per_sm = per_sm2;
+      }
       if (per_sm < 1) return fail(MB_ECUDA, "batched pass kernel does not fit on an SM");
       const int grid = (int)std::min<int64_t>(M.ntiles_text, (int64_t)c->nsm * per_sm);
       if (bp->kind == 1)

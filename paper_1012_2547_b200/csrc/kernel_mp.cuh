@@ -37,9 +37,11 @@ __device__ __forceinline__ void mp_record(const MPParams& P, int k, int64_t b) {
 // TMA producer of the batched passes: text tiles (+ halo) into the ring.
 __device__ __forceinline__ void mp_produce(const MPParams& P, StageHdr* hdr, uint64_t* full, uint64_t* empty,
                                            uint8_t* stages) {
-  for (int it = 0;; it++) {
-    const int s = it % STAGES;
-    if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
+  const int NS = P.nstages;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int it = 0;; it++, s = (s + 1 == NS) ? (ph ^= 1u, 0) : s + 1) {
+    if (it >= NS) mbar_wait(&empty[s], ph ^ 1u);
     const unsigned long long tk = atomicAdd(P.ticket, 1ULL);
     if ((int64_t)tk >= P.ntiles_text) {
       hdr[s].tk = -1;
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
   uint8_t* stages = smem + SM_STAGES;
-  uint32_t* bloom = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes);
+  uint32_t* bloom = reinterpret_cast<uint32_t*>(stages + P.nstages * P.stage_bytes);
   uint32_t* bstart = bloom + 2048;
   uint2* ents = reinterpret_cast<uint2*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
   for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents[i];
   if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) {
+    for (int s = 0; s < P.nstages; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWARP);
     }
@@ -87,9 +89,11 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   }
 
   const int c0 = warp * SEG;
-  for (int it = 0;; it++) {
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+  const int NS = P.nstages;
+  int s = 0;
+  uint32_t ph = 0;
+  for (;; s = (s + 1 == NS) ? (ph ^= 1u, 0) : s + 1) {
+    mbar_wait(&full[s], ph);
     const int64_t tau = hdr[s].tk;
     if (tau < 0) break;
     const int64_t B0 = tau * TILE;
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
   uint8_t* stages = smem + SM_STAGES;
-  uint32_t* bloom = reinterpret_cast<uint32_t*>(stages + STAGES * P.stage_bytes);
+  uint32_t* bloom = reinterpret_cast<uint32_t*>(stages + P.nstages * P.stage_bytes);
   uint32_t* bstart = bloom + 2048;
   uint4* ents = reinterpret_cast<uint4*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
   for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
   for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents4[i];
   if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) {
+    for (int s = 0; s < P.nstages; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWARP);
     }
@@ -172,9 +176,11 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
   }
   constexpr uint32_t QMASK = Q >= 4 ? 0xFFFFFFFFu : ((1u << (8 * Q)) - 1u);
   const int c0 = warp * SEG;
-  for (int it = 0;; it++) {
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+  const int NS = P.nstages;
+  int s = 0;
+  uint32_t ph = 0;
+  for (;; s = (s + 1 == NS) ? (ph ^= 1u, 0) : s + 1) {
+    mbar_wait(&full[s], ph);
     const int64_t tau = hdr[s].tk;
     if (tau < 0) break;
     const int64_t B0 = tau * TILE;

@@ -105,6 +105,7 @@ struct MPParams {
   int64_t ntiles_text;  // tiles over the text (ticket range)
   int64_t ntiles;       // tiles per pattern in the segment layout (= ScanParams.ntiles)
   int pre, post, stage_bytes;
+  int nstages;             // TMA ring depth (2..STAGES), as for ScanParams
   unsigned long long* ticket;
   const uint32_t* bloom;   // 65536 bits over gram * 0x9E3779B1 >> 16
   const uint32_t* bstart;  // (1 << B) + 1 bucket starts
