@@ -80,6 +80,20 @@ __device__ __forceinline__ void split_tile(int64_t tile, int64_t ntiles, int* k,
   }
 }
 
+// End of a search's last kernel: the last CTA to finish zeroes every ticket
+// (including this counter), so the next search needs no memset.  Call from
+// all threads of every CTA.
+__device__ __forceinline__ void reset_tickets_if_last(unsigned long long* ticket, int ntickets, int done_slot) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ticket[done_slot], 1ULL) == (unsigned long long)(gridDim.x - 1)) {
+      __threadfence();
+      for (int i = 0; i < ntickets; i++) ticket[i] = 0ULL;
+    }
+  }
+}
+
 // look-back flag word: [epoch:24][status:2][value:38]
 constexpr uint64_t ST_AGG = 1, ST_INCL = 2;
 __device__ __forceinline__ uint64_t pack_state(uint32_t epoch, uint64_t st, uint64_t val) {

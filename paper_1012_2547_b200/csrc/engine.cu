@@ -271,7 +271,8 @@ int mb_ctx_create(int device, mb_ctx** out) {
   mb_ctx* c = new mb_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMalloc(&c->ticket, 16 * sizeof(unsigned long long)) != cudaSuccess) {
+  if (cudaMalloc(&c->ticket, NTICKETS * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemset(c->ticket, 0, NTICKETS * sizeof(unsigned long long)) != cudaSuccess) {
     delete c;
     return fail(MB_ENOMEM, "ticket alloc");
   }
@@ -379,6 +380,11 @@ static int stage_end(mb_ctx* c, cudaStream_t st) {
   CUDA_TRY(cudaEventRecord(s.ev, st));
   s.pending = true;
   return MB_OK;
+}
+
+// After a failed search the last kernel may not have zeroed the tickets.
+static void tickets_recover(mb_ctx* c, cudaStream_t st) {
+  cudaMemsetAsync(c->ticket, 0, NTICKETS * sizeof(unsigned long long), st);
 }
 
 // grow-only device scratch
@@ -752,6 +758,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // programmatic dependent launches: offsets/expand CTAs are scheduled as the
     // previous grid drains and wait in-kernel (griddepcontrol.wait) for its
     // results -- the launch gap and the scan's tail overlap
+    P.last = (d_out && cap > 0) ? 0 : 1;  // the search's last kernel zeroes the tickets
     if (scan_per == 32)
       CUDA_TRY(launch_pdl(offsets_kernel<32>, (int)nchunks, NT, st, P));
     else if (scan_per == 16)
@@ -762,6 +769,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     CUDA_TRY(cudaGetLastError());
     if (d_out && cap > 0) {
       const int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS, (int64_t)c->nsm * 16);
+      P.last = 1;
       CUDA_TRY(launch_pdl(expand_kernel, (int)eg, EXP_WARPS * 32, st, P));
       g_launches++;
       CUDA_TRY(cudaGetLastError());
@@ -796,7 +804,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     for (int k = 0; k < K; k++) any_out |= bp->need[kbase + k] != 0;
     if (any_out) CUDA_TRY(cudaMemsetAsync(M.overflow, 1, 1, st));
     M.need = c->need;
-    CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 16 * sizeof(unsigned long long), st));
+    CUDA_TRY(cudaMemsetAsync(c->ticket, 0, NTICKETS * sizeof(unsigned long long), st));
     const void* fn = bp->kind == 1 ? (const void*)mp_scan_kernel
                      : bp->q == 8  ? (const void*)mpb_scan_kernel<8>
                      : bp->q == 4  ? (const void*)mpb_scan_kernel<4>
@@ -862,7 +870,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     mp_used = true;
     c->mp_batches++;
   }
-  if (!mp_used) CUDA_TRY(cudaMemsetAsync(c->ticket, 0, 16 * sizeof(unsigned long long), st));
+  // tickets are zero here: ctx creation, or the previous search's last kernel reset them
   // group patterns by family key (stable); a single group needs no index list
   std::vector<int> keys;
   std::vector<std::vector<int32_t>> groups;
@@ -911,6 +919,7 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
   if (rc) return rc;
   if ((rc = stage_begin(c))) return rc;
   rc = run_search(c, dd, &p->dview, 1, d_text, n, d_out, cap, d_count, st);
+  if (rc) tickets_recover(c, st);
   const int rc2 = stage_end(c, st);
   return rc ? rc : rc2;
 }
@@ -970,6 +979,7 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
     if ((rc = stage_upload(c, c->mp_tab, c->pass.img.data(), sizeof(uint32_t) * c->pass.img.size(), st))) return rc;
   }
   rc = run_batch(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets, st, &c->pass, c->mp_tab);
+  if (rc) tickets_recover(c, st);
   const int rc2 = stage_end(c, st);
   return rc ? rc : rc2;
 }
@@ -1029,6 +1039,7 @@ int mb_find_batch_prepared(mb_ctx* c, const mb_batch* b, const uint8_t* d_text, 
   if (rc) return rc;
   rc = run_batch(c, b->d_pats, b->h_pats.data(), b->K, d_text, n, d_out, cap, d_offsets, (cudaStream_t)stream,
                  &b->pass, b->d_mp);
+  if (rc) tickets_recover(c, (cudaStream_t)stream);
   const int rc2 = stage_end(c, (cudaStream_t)stream);
   return rc ? rc : rc2;
 }

@@ -143,9 +143,9 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
 #pragma unroll
   for (int h = 0; h < PER / 2; h++) s_cnt[h * NT + tid] = v2[h];
   // nothing to emit and no pattern ends in this thread's range: done
-  if (tsum == 0 && rem + PER < seg_per_pat) return;
+  const bool idle = tsum == 0 && rem + PER < seg_per_pat;
 #pragma unroll 1
-  for (int q = 0; q < PER; q++) {
+  for (int q = 0; q < (idle ? 0 : PER); q++) {
     const int64_t t = base + (int64_t)tid * PER + q;
     const uint32_t vq = (s_cnt[(q >> 1) * NT + tid] >> (16 * (q & 1))) & 0xFFFFu;
     if (t < nseg) {
@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     run += vq;
     if (++rem == seg_per_pat) rem = 0, kq++;
   }
+  if (P.last) reset_tickets_if_last(P.ticket, NTICKETS, TICKET_DONE);
 }
 
 // ------------------------------------------------ kernel 3: expansion
@@ -221,12 +222,15 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
   const int64_t nq = (int64_t)P.ticket[TICKET_DENSE];
   const int64_t stride = (int64_t)gridDim.x * EXP_WARPS;
   int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp;
-  if (qi >= nq) return;
-  ExpSeg cur = exp_load(P, P.seglist[qi], lane);
-  int64_t g_nxt = qi + stride < nq ? P.seglist[qi + stride] : -1;
+  ExpSeg cur;
+  int64_t g_nxt = -1;
+  if (qi < nq) {
+    cur = exp_load(P, P.seglist[qi], lane);
+    g_nxt = qi + stride < nq ? P.seglist[qi + stride] : -1;
+  }
   int cur_k = -1;
   int64_t shift = 0;
-  while (true) {
+  while (qi < nq) {
     ExpSeg nxt;
     int64_t g_nn = -1;
     if (g_nxt >= 0) {  // prefetch: issued before the current segment's work
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
     cur = nxt;
     g_nxt = g_nn;
   }
+  if (P.last) reset_tickets_if_last(P.ticket, NTICKETS, TICKET_DONE);
 }
 
 

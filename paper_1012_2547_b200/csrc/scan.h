@@ -47,6 +47,8 @@ constexpr int TICKET_OFFSETS = 7; // ticket slot of offsets_kernel (slots 0..6: 
 constexpr int MAX_GROUPS = 7;
 constexpr int TICKET_MP0 = 8;     // MP chunk tickets use slots 8..14 (ticket array has 16)
 constexpr int TICKET_DENSE = 15;  // number of segments queued for expand_kernel
+constexpr int TICKET_DONE = 16;   // CTAs of a search's last kernel that finished (it zeroes slots 0..16)
+constexpr int NTICKETS = 17;
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 
 struct StageHdr {
@@ -95,6 +97,7 @@ struct ScanParams {
   int unsorted_lists;       // lists were filled in arbitrary order (MP path): sort on expand
   const unsigned int* run_if;  // count kernels exit at once unless *run_if != 0 (batch-pass fallback)
   const unsigned int* need;    // per batch pattern: 0 = the batch pass covered it (skip its tiles), else scan
+  int last;                    // this launch ends the search: its last CTA zeroes the tickets for the next one
 };
 
 // Batched multi-pattern single pass (K5 "MP"): every anchor gram of every
