@@ -55,5 +55,22 @@ pats = [t[i : i + 24] for i in rng.integers(0, 4 * TILE - 24, 40)] + [rb(256, 9)
 res = search_many(pats, t)
 for p, r in zip(pats, res):
     assert r == oracle.search(p, t).tolist()
+# batched passes: K5 (aligned words), K5b (byte offsets, q = 2 / 4 / 8) with
+# dense patterns left to their scans, anchor words 2 / 3, sampled in a batch
+for sigma, lo, hi in ((256, 8, 40), (16, 2, 3), (64, 4, 6), (4, 8, 30), (32, 300, 1200)):
+    t = rb(sigma, 3 * TILE + 321)
+    ms = rng.integers(lo, hi + 1, 64)
+    pats = [t[i : i + m] for i, m in zip(rng.integers(0, len(t) - hi, 64), ms)] + [b"ab" * 2, t[:lo]]
+    for obj in (None, "prepared"):
+        plans = [engine.Plan(p) for p in pats]
+        pos, offs = engine.find_batch(engine.Batch(plans) if obj else plans, t)
+        pos = pos.cpu().numpy()
+        for k, p in enumerate(pats):
+            assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(p, t)), (sigma, k)
+for nw in (2, 3):
+    t = rb(2, 2 * TILE + 77)
+    p = t[1000:1040]
+    got = engine.find(engine.Plan(p, anchor_words=nw), t).cpu().numpy()
+    assert np.array_equal(got, oracle.search(p, t)), nw
 torch.cuda.synchronize()
 print("sanitize cases ok")
