@@ -107,7 +107,8 @@ int mb_find_batch(mb_ctx* ctx, const mb_plan* const* plans, int K, const uint8_t
                   int64_t* d_out, int64_t cap, int64_t* d_offsets, void* stream);
 
 /* Prepared batch (compile once, search many texts): holds the device params of
- * K plans and the K5 multi-pattern tables.  The plans must outlive the batch. */
+ * K plans and the tables of its batched pass (K5 aligned-word or K5b
+ * byte-offset, chosen at creation).  The plans must outlive the batch. */
 typedef struct mb_batch mb_batch;
 int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out);
 void mb_batch_destroy(mb_batch* batch);
@@ -126,7 +127,7 @@ int mb_search_batch_host(mb_ctx* ctx, const uint8_t* const* h_patterns, const in
 /* ---- K0: device byte histogram (Text.alphabet_size, core.py:42-44) ---- */
 int mb_histogram(mb_ctx* ctx, const uint8_t* d_text, int64_t n, int64_t* d_hist256, void* stream);
 
-/* Batched searches on this context that took the K5 multi-pattern single pass. */
+/* Batched searches on this context that took a batched single pass (K5 / K5b). */
 int64_t mb_ctx_mp_batches(const mb_ctx* ctx);
 
 /* Number of this library's kernels launched so far in this process. */
