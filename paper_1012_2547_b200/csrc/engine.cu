@@ -562,7 +562,7 @@ static void pass_chunk(int kc, int ent_words, const Ent& ent_of, std::vector<uin
 
 static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, BatchPass* bp) {
   *bp = BatchPass();
-  if (K < 8 || K > MP_CHUNK * MAX_GROUPS) return;
+  if (K < 8 || K > MP_CHUNK * MAX_MP_CHUNKS) return;
   double hist[256] = {0}, tot = 0;
   int64_t minm = INT64_MAX;
   for (int k = 0; k < K; k++) {
@@ -759,6 +759,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // previous grid drains and wait in-kernel (griddepcontrol.wait) for its
     // results -- the launch gap and the scan's tail overlap
     P.last = (d_out && cap > 0) ? 0 : 1;  // the search's last kernel zeroes the tickets
+    P.offs_resident = nchunks <= (int64_t)c->nsm * 2 ? 1 : 0;  // __launch_bounds__(NT, 2)
     if (scan_per == 32)
       CUDA_TRY(launch_pdl(offsets_kernel<32>, (int)nchunks, NT, st, P));
     else if (scan_per == 16)

@@ -37,7 +37,9 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   __shared__ int64_t s_chunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_wait();  // counts / lists / bitmaps of the count kernel(s)
-  if (tid == 0) s_chunk = (int64_t)atomicAdd(&P.ticket[TICKET_OFFSETS], 1ULL);
+  // chunk id: CTA index when the whole grid is co-resident (any order is
+  // then safe for the look-back), else a ticket in CTA start order
+  if (tid == 0) s_chunk = P.offs_resident ? (int64_t)blockIdx.x : (int64_t)atomicAdd(&P.ticket[TICKET_OFFSETS], 1ULL);
   __syncthreads();
   const int64_t ch = s_chunk;
   const int64_t nseg = P.total_tiles * NWARP;

@@ -43,12 +43,14 @@ constexpr int SEG = TILE / NWARP; // positions per consumer-warp segment
 constexpr int SEG_WORDS = SEG / 32;
 constexpr int STAGES = MB_STAGES;  // TMA ring depth (max; scan_kernel may run with 2, see ScanParams.nstages)
 constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offsets
-constexpr int TICKET_OFFSETS = 7; // ticket slot of offsets_kernel (slots 0..6: family groups)
-constexpr int MAX_GROUPS = 7;
-constexpr int TICKET_MP0 = 8;     // MP chunk tickets use slots 8..14 (ticket array has 16)
-constexpr int TICKET_DENSE = 15;  // number of segments queued for expand_kernel
-constexpr int TICKET_DONE = 16;   // CTAs of a search's last kernel that finished (it zeroes slots 0..16)
-constexpr int NTICKETS = 17;
+// ticket counters (one uint64 each, zeroed between searches):
+constexpr int MAX_GROUPS = 12;      // family groups of one batch: slots 0..11 (10 family keys exist)
+constexpr int TICKET_OFFSETS = 12;  // offsets_kernel chunks (when the grid is not co-resident)
+constexpr int MAX_MP_CHUNKS = 7;    // batch-pass table chunks (MP_CHUNK patterns each): slots 13..19
+constexpr int TICKET_MP0 = 13;
+constexpr int TICKET_DENSE = 20;    // number of segments queued for expand_kernel
+constexpr int TICKET_DONE = 21;     // CTAs of a search's last kernel that finished (it zeroes all slots)
+constexpr int NTICKETS = 22;
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 
 struct StageHdr {
@@ -98,6 +100,7 @@ struct ScanParams {
   const unsigned int* run_if;  // count kernels exit at once unless *run_if != 0 (batch-pass fallback)
   const unsigned int* need;    // per batch pattern: 0 = the batch pass covered it (skip its tiles), else scan
   int last;                    // this launch ends the search: its last CTA zeroes the tickets for the next one
+  int offs_resident;           // offsets_kernel grid fits on the GPU at once: chunk = blockIdx.x
 };
 
 // Batched multi-pattern single pass (K5 "MP"): every anchor gram of every

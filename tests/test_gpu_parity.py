@@ -290,6 +290,28 @@ def test_mpb_byte_offset_pass(cuda, sigma, lo, hi):
             assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(p, t)), (k, p)
 
 
+def test_batch_with_every_family_group(cuda):
+    """One batch spanning all ten family keys (SWAR m=1/2/3, WIN4, ALIGNED
+    1/2/3 words, sampled, shift-or 32/64): one count launch per group."""
+    rng = np.random.default_rng(404)
+    n = 2 * TILE + 999
+    t = rand_bytes(rng, 256, n)
+    tb = rand_bytes(rng, 2, 4096)
+    t = t[:9000] + tb + t[9000 + len(tb):]
+    specs = [(t[100:101], "auto", 0), (t[200:202], "auto", 0), (t[300:303], "auto", 0), (t[400:405], "auto", 0),
+             (t[500:524], "auto", 1), (tb[10:50], "auto", 2), (tb[100:160], "auto", 3),
+             (t[700:1300], "auto", 0), (t[2000:2020], "shiftor", 0), (t[3000:3050], "shiftor", 0)]
+    plans = [engine.Plan(p, fam, anchor_words=nw) for p, fam, nw in specs]
+    keys = {(pl.info().family, pl.m if pl.info().family == "swar" else pl.info().words,
+             pl.m <= 32 if pl.info().family == "shiftor" else None) for pl in plans}
+    assert len(keys) == 10, keys
+    for obj in (plans, plans * 3):
+        pos, offs = engine.find_batch(obj, t)
+        pos = pos.cpu().numpy()
+        for k, pl in enumerate(obj):
+            assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(pl.pattern, t)), (k, pl.m)
+
+
 def test_mpb_overflow_falls_back(cuda):
     # selective-looking short patterns, but one of them repeats > LIST_CAP times in a segment
     rng = np.random.default_rng(77)
