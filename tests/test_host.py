@@ -202,6 +202,63 @@ def _shard_worker(rank, world, port, text, pats, q):
     dist.destroy_process_group()
 
 
+def _shard_batch_worker(rank, world, port, text, pats, q):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_1012_2547_b200 import shard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def batch(ps, t):  # the oracle stands in for engine.find_batch on this CPU test
+        res = [oracle.search(p, t) for p in ps]
+        offs = np.concatenate([[0], np.cumsum([r.size for r in res])])
+        return np.concatenate(res) if res else np.zeros(0, np.int64), offs
+
+    pos, offs = shard.sharded_search_batch(pats, text, batch)
+    # text striping: every rank's slice of one pattern gathered into the global list
+    p = pats[0]
+    lo, hi, rhi = shard.shard_bounds(len(text), len(p), world, rank)
+    local, _, _ = shard.sharded_search(p, text[lo:rhi], len(text), lambda a, b: oracle.search(a, b))
+    full = shard.gather_positions(torch.from_numpy(np.asarray(local, dtype=np.int64)))
+    q.put((rank, pos.tolist(), offs.tolist(), full.tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_batch_and_gather_gloo(world):
+    """pattern-sharded batches (text replicated) gather into the
+    batch CSR, and text-striped positions gather into the global list."""
+    import multiprocessing as mp
+    import socket
+
+    import oracle
+
+    rng = np.random.default_rng(10 + world)
+    text = rng.integers(0, 4, 6000, dtype=np.uint8).tobytes()
+    pats = [text[i : i + m] for i, m in zip(rng.integers(0, 5900, 7), (2, 3, 5, 8, 13, 40, 90))]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_batch_worker, args=(r, world, port, text, pats, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    want = [oracle.search(p, text).tolist() for p in pats]
+    for rank, pos, offs, full in outs:
+        for k in range(len(pats)):
+            assert pos[offs[k] : offs[k + 1]] == want[k], (rank, k)
+        assert full == want[0]
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_search_gloo(world):
     import multiprocessing as mp
