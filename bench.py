@@ -137,7 +137,10 @@ def build_workload(args, rank, world):
         n = args.n or (16 << 30)
         n = (n // inputs.STRIPE) * inputs.STRIPE if n >= inputs.STRIPE else n
         halo = 1023 if rank < world - 1 else 0
-        host = torch.empty(n + halo, dtype=torch.uint8, pin_memory=True)
+        try:
+            host = torch.empty(n + halo, dtype=torch.uint8, pin_memory=True)
+        except RuntimeError:  # pinned host memory exhausted (many ranks on one node): pageable
+            host = torch.empty(n + halo, dtype=torch.uint8)
         h = host.numpy()
         stripe0 = rank * max(n // inputs.STRIPE, 1)
         _cfg4_stripes(h[:n], stripe0, n)
