@@ -312,6 +312,25 @@ def test_batch_with_every_family_group(cuda):
             assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(pl.pattern, t)), (k, pl.m)
 
 
+@pytest.mark.parametrize("n", [0, 1, 5, 100, 3000])
+def test_batched_passes_tiny_texts(cuda, n):
+    """Batched passes (and their fallbacks) on texts shorter than many of the
+    patterns, down to the empty text."""
+    rng = np.random.default_rng(n + 17)
+    for sigma in (4, 64, 256):
+        t = rand_bytes(rng, sigma, n)
+        pats = [rand_bytes(rng, sigma, int(m)) for m in rng.integers(1, 40, 30)]
+        pats += [t[i : i + 3] for i in range(0, max(n - 3, 0), max(n // 7, 1))][:10]
+        pats = [p for p in pats if p]
+        for obj in (None, "prepared"):
+            plans = [engine.Plan(p) for p in pats]
+            pos, offs = engine.find_batch(engine.Batch(plans) if obj else plans, t)
+            pos = pos.cpu().numpy()
+            for k, p in enumerate(pats):
+                want = oracle.search(p, t) if len(p) <= n else np.empty(0, np.int64)
+                assert np.array_equal(pos[offs[k] : offs[k + 1]], want), (sigma, k, len(p), n)
+
+
 def test_mpb_overflow_falls_back(cuda):
     # selective-looking short patterns, but one of them repeats > LIST_CAP times in a segment
     rng = np.random.default_rng(77)
