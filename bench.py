@@ -39,6 +39,30 @@ PEAK_FALLBACK = 6650.0  # B200_PROFILING.md fallback, GB/s
 BACKEND = os.environ.get("MB_BENCH_BACKEND", "nccl")  # gloo only for multi-rank tests on one GPU
 
 
+FLUSH_DESC = ("L2 flushed before every timed launch: 256 MiB write (evicts the text), then a 256 MiB read of a "
+              "second buffer (evicts the write's dirty lines, so their write-back is not charged to the search)")
+
+
+class L2Flush:
+    """Evict the 126 MB L2 between timed launches of L2-sized inputs.  A write
+    alone leaves L2 full of dirty lines whose write-back then lands inside the
+    next timed launch (measured: +14 us on a 256 MiB scan, tools/flush_modes.py);
+    reading a clean buffer afterwards leaves only clean lines."""
+
+    def __init__(self, dev):
+        import torch
+
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        self.r = torch.zeros(32 << 20, dtype=torch.int64, device=dev)
+        self.sink = torch.empty((), dtype=torch.int64, device=dev)
+
+    def __call__(self):
+        import torch
+
+        self.w.zero_()
+        torch.sum(self.r, dim=0, out=self.sink)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -295,15 +319,15 @@ def run_ours(args, rank, world, local_rank):
     cnt = torch.zeros(len(plans), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
     K = len(plans)
-    # texts up to 4x the 126 MB L2 are flushed out of L2 (256 MiB write, outside
+    # texts up to 4x the 126 MB L2 are flushed out of L2 (L2Flush, outside
     # the per-launch events) before every timed launch; ms_per_step is then the
     # sum of the launches' event durations
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if n + halo <= (512 << 20) else None
+    flush = L2Flush(dev) if n + halo <= (512 << 20) else None
 
     def step(ev=None):
         for i, (pl, v) in enumerate(zip(plans, views)):
             if ev is not None and flush is not None:
-                flush.zero_()
+                flush()
                 torch.cuda._sleep(SPIN_CYCLES)  # GPU busy while the host enqueues the search
             if ev is not None:
                 ev[i][0].record(stream)
@@ -422,7 +446,7 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl["desc"], "text_bytes_per_gpu": int(n), "patterns_m": [len(p) for p in pats],
                        "l2": "inputs larger than L2 (text > 4x 126 MB), no flush needed" if flush is None
-                       else "L2 flushed (256 MiB write) before every timed launch; ms = sum of launch events", "parallelism": f"dp{world} (text stripes, count all_gather)"},
+                       else FLUSH_DESC + "; ms = sum of launch events", "parallelism": f"dp{world} (text stripes, count all_gather)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "kernel": "scan_kernel (full-scan families, per-pattern launch incl. offsets+expand)",
@@ -460,7 +484,7 @@ def run_batched_sweep(args, rank, world, local_rank):
         t = inputs.config3()
         for m in (4, 16, 64, 256, 1024):
             cells.append((95, m, t, inputs.config3_patterns(t, m)))
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    flush = L2Flush(dev)
     rows, tot_b, tot_ms, launches0 = [], 0, 0.0, engine.launch_count()
     dtexts = {}
     for sigma, m, t, pats in cells:
@@ -485,7 +509,7 @@ def run_batched_sweep(args, rank, world, local_rank):
         # starts with the text in HBM, as a one-off search would
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for e0, e1 in evs:
-            flush.zero_()
+            flush()
             torch.cuda._sleep(SPIN_CYCLES)  # GPU busy while the host enqueues the batch: device time only
             e0.record(stream)
             engine.find_batch_into(plans, d, out, offs, stream)
@@ -505,7 +529,7 @@ def run_batched_sweep(args, rank, world, local_rank):
             "warmup": max(args.warmup, 3), "ms_per_step": round(tot_ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{args.workload}: batched, 500 patterns per launch (CSR)",
-                       "l2": "L2 flushed (256 MiB write) before every timed launch; value aggregated K*n/t",
+                       "l2": FLUSH_DESC + "; value aggregated K*n/t",
                        "timing": "per cell: median of the steps' CUDA-event times; a spin kernel keeps the "
                                  "GPU busy while each launch is enqueued, so host enqueue time is excluded"},
             "cells": rows, "gpu_launches": engine.launch_count() - launches0}), flush=True)

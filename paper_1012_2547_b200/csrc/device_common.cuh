@@ -24,6 +24,27 @@ namespace mb {
   } while (0)
 #endif
 
+// Kernel-phase timestamps for the trace build (make trace -> libmatchb200_trace.so,
+// tools/trace_phases.py): slot i keeps the min (even) / max (odd) %globaltimer
+// any CTA recorded there.  Compiled out of the product library.
+#ifdef MB_TRACE
+__device__ unsigned long long g_trace[32];
+__device__ __forceinline__ void trace_mark(int slot) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (slot & 1) atomicMax(&g_trace[slot], t); else atomicMin(&g_trace[slot], t);
+  }
+}
+#define MB_TRACE_MARK(slot) trace_mark(slot)
+#define MB_TRACE_SYNC_MARK(slot) (__syncthreads(), trace_mark(slot))
+#else
+#define MB_TRACE_MARK(slot) \
+  do {                      \
+  } while (0)
+#define MB_TRACE_SYNC_MARK(slot) MB_TRACE_MARK(slot)
+#endif
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -80,16 +101,19 @@ __device__ __forceinline__ void split_tile(int64_t tile, int64_t ntiles, int* k,
   }
 }
 
-// End of a search's last kernel: the last CTA to finish zeroes every ticket
-// (including this counter), so the next search needs no memset.  Call from
-// all threads of every CTA.
-__device__ __forceinline__ void reset_tickets_if_last(unsigned long long* ticket, int ntickets, int done_slot) {
+// End of offsets_kernel: the last CTA to finish zeroes every ticket but
+// keep_slot (this search's expand-queue count, read by expand_kernel; the next
+// search, of the other epoch parity, zeroes it), so no search needs a memset.
+// Call from all threads of every CTA.
+__device__ __forceinline__ void reset_tickets_if_last(unsigned long long* ticket, int ntickets, int done_slot,
+                                                      int keep_slot) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&ticket[done_slot], 1ULL) == (unsigned long long)(gridDim.x - 1)) {
       __threadfence();
-      for (int i = 0; i < ntickets; i++) ticket[i] = 0ULL;
+      for (int i = 0; i < ntickets; i++)
+        if (i != keep_slot) ticket[i] = 0ULL;
     }
   }
 }

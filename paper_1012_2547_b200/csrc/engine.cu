@@ -261,6 +261,19 @@ int mb_plan_gram_hash(const mb_plan* p, int q, uint32_t* o) {
   return MB_OK;
 }
 
+// Every kernel of a search prefers the maximum shared-memory carveout: the
+// count kernels need it, and an SM switching carveouts between two kernels
+// must drain first (a visible launch gap before each scan otherwise).
+static void prefer_max_smem() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const void* fns[] = {(const void*)offsets_kernel<8>, (const void*)offsets_kernel<16>,
+                         (const void*)offsets_kernel<32>, (const void*)expand_kernel, (const void*)fill_kernel};
+    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaGetLastError();
+  });
+}
+
 int mb_ctx_create(int device, mb_ctx** out) {
   if (!out) return fail(MB_EINVAL, "null out");
   *out = nullptr;
@@ -268,6 +281,7 @@ int mb_ctx_create(int device, mb_ctx** out) {
   CUDA_TRY(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(MB_EINVAL, "bad device index");
   CUDA_TRY(cudaSetDevice(device));
+  prefer_max_smem();
   mb_ctx* c = new mb_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
@@ -738,6 +752,8 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   if (nchunks > c->state_cap || c->epoch >= (1u << 24) - 4) {
     if ((rc = grow(&c->state, &c->state_cap, nchunks, "look-back state"))) return rc;
     CUDA_TRY(cudaMemsetAsync(c->state, 0, sizeof(uint64_t) * c->state_cap, st));
+    // the epoch parity picks the expand-queue slot: restart it with clean tickets
+    CUDA_TRY(cudaMemsetAsync(c->ticket, 0, NTICKETS * sizeof(unsigned long long), st));
     c->epoch = 0;
   }
   P.counts = c->counts;
@@ -758,7 +774,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // programmatic dependent launches: offsets/expand CTAs are scheduled as the
     // previous grid drains and wait in-kernel (griddepcontrol.wait) for its
     // results -- the launch gap and the scan's tail overlap
-    P.last = (d_out && cap > 0) ? 0 : 1;  // the search's last kernel zeroes the tickets
+    P.dense_slot = (P.epoch & 1) ? TICKET_DENSE_ODD : TICKET_DENSE;
     P.offs_resident = nchunks <= (int64_t)c->nsm * 2 ? 1 : 0;  // __launch_bounds__(NT, 2)
     if (scan_per == 32)
       CUDA_TRY(launch_pdl(offsets_kernel<32>, (int)nchunks, NT, st, P));
@@ -769,8 +785,11 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     if (d_out && cap > 0) {
-      const int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS, (int64_t)c->nsm * 16);
-      P.last = 1;
+      // one resident wave at most: the CTAs are scheduled while offsets_kernel
+      // runs (it triggers its dependents at entry) and loop over the queue
+      int exp_per_sm = 0;
+      CUDA_TRY(occupancy((const void*)expand_kernel, EXP_WARPS * 32, 0, &exp_per_sm));
+      const int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS, (int64_t)c->nsm * std::max(exp_per_sm, 1));
       CUDA_TRY(launch_pdl(expand_kernel, (int)eg, EXP_WARPS * 32, st, P));
       g_launches++;
       CUDA_TRY(cudaGetLastError());
@@ -1140,3 +1159,20 @@ int mb_search_host(mb_ctx* c, const uint8_t* h_pattern, int64_t m, const uint8_t
 }
 
 }  // extern "C"
+
+// Trace build only (make trace): copy out the kernel-phase timestamps
+// (device_common.cuh MB_TRACE_MARK) and optionally re-arm them.
+extern "C" int mb_debug_trace(uint64_t* out, int reset) {
+#ifdef MB_TRACE
+  if (out) CUDA_TRY(cudaMemcpyFromSymbol(out, g_trace, sizeof(uint64_t) * 32));
+  if (reset) {
+    uint64_t init[32];
+    for (int i = 0; i < 32; i++) init[i] = (i & 1) ? 0ULL : ~0ULL;
+    CUDA_TRY(cudaMemcpyToSymbol(g_trace, init, sizeof(init)));
+  }
+  return MB_OK;
+#else
+  (void)out, (void)reset;
+  return fail(MB_EINVAL, "not a trace build");
+#endif
+}

@@ -36,7 +36,11 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   __shared__ int64_t s_excl;
   __shared__ int64_t s_chunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  pdl_wait();  // counts / lists / bitmaps of the count kernel(s)
+  MB_TRACE_MARK(2);
+  pdl_trigger();  // expand_kernel's CTAs get resident now and wait for this grid in pdl_wait
+  pdl_wait();     // counts / lists / bitmaps of the count kernel(s)
+  MB_TRACE_MARK(4);
+  MB_TRACE_MARK(5);
   // chunk id: CTA index when the whole grid is co-resident (any order is
   // then safe for the look-back), else a ticket in CTA start order
   if (tid == 0) s_chunk = P.offs_resident ? (int64_t)blockIdx.x : (int64_t)atomicAdd(&P.ticket[TICKET_OFFSETS], 1ULL);
@@ -120,6 +124,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     __syncthreads();  // s_first / s_part are rewritten next round
   }
   __syncthreads();
+  MB_TRACE_MARK(7);
   if (tid == 0) {
     if (ch > 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_INCL, (uint64_t)(s_excl + chunk_total)));
     s_excl += P.out_base ? *P.out_base : 0;
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
           }
         } else {
           P.toff[t] = run;
-          const unsigned long long slot = atomicAdd(&P.ticket[TICKET_DENSE], 1ULL);
+          const unsigned long long slot = atomicAdd(&P.ticket[P.dense_slot], 1ULL);
           P.seglist[slot] = t;
         }
       }
@@ -189,7 +194,8 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     run += vq;
     if (++rem == seg_per_pat) rem = 0, kq++;
   }
-  if (P.last) reset_tickets_if_last(P.ticket, NTICKETS, TICKET_DONE);
+  MB_TRACE_SYNC_MARK(9);
+  reset_tickets_if_last(P.ticket, NTICKETS, TICKET_DONE, P.dense_slot);
 }
 
 // ------------------------------------------------ kernel 3: expansion
@@ -199,7 +205,10 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
 // current segment is written.  Unsorted (MP) lists get a 32-lane bitonic
 // sort; dense segments are staged in smem as uint16 offsets, then streamed out
 // with coalesced 256-byte stores.
-constexpr int EXP_WARPS = 4;
+#ifndef MB_EXP_WARPS
+#define MB_EXP_WARPS 8
+#endif
+constexpr int EXP_WARPS = MB_EXP_WARPS;
 
 struct ExpSeg {  // one queued segment as a lane holds it
   int64_t g, o;
@@ -220,8 +229,10 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint16_t s_run[EXP_WARPS][SEG];  // dense segments: staged offsets per warp
   uint16_t* const sb = s_run[warp];
+  MB_TRACE_MARK(10);
   pdl_wait();  // queue and offsets of offsets_kernel
-  const int64_t nq = (int64_t)P.ticket[TICKET_DENSE];
+  MB_TRACE_MARK(12);
+  const int64_t nq = (int64_t)P.ticket[P.dense_slot];
   const int64_t stride = (int64_t)gridDim.x * EXP_WARPS;
   int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp;
   ExpSeg cur;
@@ -307,7 +318,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
     cur = nxt;
     g_nxt = g_nn;
   }
-  if (P.last) reset_tickets_if_last(P.ticket, NTICKETS, TICKET_DONE);
+  MB_TRACE_SYNC_MARK(13);
 }
 
 

@@ -18,6 +18,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + SM_EMPTY);
   uint8_t* stages = smem + SM_STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  MB_TRACE_MARK(0);
+  pdl_trigger();  // the offsets kernel may be scheduled as SMs drain (it waits for this grid)
   if (P.run_if && *P.run_if == 0u) return;  // conditional fallback launch (MP did not overflow)
   const int NS = P.nstages;
   uint32_t* bm = reinterpret_cast<uint32_t*>(stages + NS * P.stage_bytes) + warp * SEG_WORDS;
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
       mbar_arrive(&empty[s]);
     }
   }
+  MB_TRACE_MARK(1);
 }
 
 

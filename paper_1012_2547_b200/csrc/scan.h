@@ -48,9 +48,10 @@ constexpr int MAX_GROUPS = 12;      // family groups of one batch: slots 0..11 (
 constexpr int TICKET_OFFSETS = 12;  // offsets_kernel chunks (when the grid is not co-resident)
 constexpr int MAX_MP_CHUNKS = 7;    // batch-pass table chunks (MP_CHUNK patterns each): slots 13..19
 constexpr int TICKET_MP0 = 13;
-constexpr int TICKET_DENSE = 20;    // number of segments queued for expand_kernel
-constexpr int TICKET_DONE = 21;     // CTAs of a search's last kernel that finished (it zeroes all slots)
-constexpr int NTICKETS = 22;
+constexpr int TICKET_DENSE = 20;    // segments queued for expand_kernel (even epochs; odd: TICKET_DENSE_ODD)
+constexpr int TICKET_DONE = 21;     // offsets_kernel CTAs that finished (the last one zeroes the slots)
+constexpr int TICKET_DENSE_ODD = 22;
+constexpr int NTICKETS = 23;
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 
 struct StageHdr {
@@ -89,7 +90,7 @@ struct ScanParams {
   uint16_t* lists;      // per segment LIST_CAP tile-relative offsets
   uint32_t* bitmaps;    // per segment SEG_WORDS words (dense segments only)
   int64_t* toff;        // per segment exclusive output offset (queued segments only)
-  int64_t* seglist;     // segments queued for expand_kernel (count in ticket[TICKET_DENSE])
+  int64_t* seglist;     // segments queued for expand_kernel (count in ticket[dense_slot])
   uint64_t* state;      // look-back flags of offsets_kernel (per chunk)
   uint32_t epoch;
   int64_t* out;         // positions (may be null: count only)
@@ -99,7 +100,9 @@ struct ScanParams {
   int unsorted_lists;       // lists were filled in arbitrary order (MP path): sort on expand
   const unsigned int* run_if;  // count kernels exit at once unless *run_if != 0 (batch-pass fallback)
   const unsigned int* need;    // per batch pattern: 0 = the batch pass covered it (skip its tiles), else scan
-  int last;                    // this launch ends the search: its last CTA zeroes the tickets for the next one
+  int dense_slot;              // ticket slot counting this search's expand queue (alternates by epoch parity:
+                               // offsets_kernel's last CTA zeroes every slot but this one, so the
+                               // expand grid needs no atomics; the next search zeroes it)
   int offs_resident;           // offsets_kernel grid fits on the GPU at once: chunk = blockIdx.x
 };
 
