@@ -124,6 +124,42 @@ __device__ __forceinline__ uint64_t pack_state(uint32_t epoch, uint64_t st, uint
   return ((uint64_t)epoch << 40) | (st << 38) | (val & ((1ULL << 38) - 1));
 }
 
+// barrier over the NT consumer threads of a warp-specialised CTA (the producer
+// warp has returned); id 1 (id 0 is __syncthreads)
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory"); }
+
+// Decoupled look-back by one warp: publish `agg` for item idx, then sum the
+// predecessors' published values 32 at a time back to the nearest inclusive
+// one; publish the inclusive prefix and return the exclusive one (all lanes).
+// Items must be numbered in start order of their (running) producers.
+__device__ __forceinline__ int64_t warp_lookback(uint64_t* state, int64_t idx, uint64_t agg, uint32_t epoch,
+                                                 int lane) {
+  if (lane == 0) st_relaxed(&state[idx], pack_state(epoch, idx == 0 ? ST_INCL : ST_AGG, agg));
+  int64_t excl = 0;
+  for (int64_t j = idx - 1; j >= 0; j -= 32) {
+    const int64_t q = j - lane;
+    uint64_t sv = 0;
+    bool incl = false;
+    if (q >= 0) {
+      while (true) {
+        sv = ld_relaxed(&state[q]);
+        if ((uint32_t)(sv >> 40) == epoch && ((sv >> 38) & 3)) break;
+        __nanosleep(20);
+      }
+      incl = ((sv >> 38) & 3) == ST_INCL;
+    }
+    const uint32_t bi = __ballot_sync(0xffffffffu, incl);
+    const int first = bi ? __ffs(bi) - 1 : 32;  // nearest predecessor holding an inclusive prefix
+    unsigned long long v = (q >= 0 && lane <= first) ? (sv & ((1ULL << 38) - 1)) : 0ULL;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    excl += (int64_t)v;
+    if (bi) break;
+  }
+  if (lane == 0 && idx > 0) st_relaxed(&state[idx], pack_state(epoch, ST_INCL, (uint64_t)excl + agg));
+  return excl;
+}
+
 // ----------------------------------------------------------- SWAR primitives
 // exact per-byte zero flags (0x80 in each zero byte) -> 4-bit mask
 __device__ __forceinline__ uint32_t zero_bytes4(uint32_t x) {

@@ -418,11 +418,28 @@ static int grow(T** p, int64_t* cap, int64_t need, const char* what) {
 
 struct SampledTag {};
 
+// raise a kernel's dynamic smem limit once (227 KiB per CTA minus its static smem)
+static cudaError_t allow_max_smem(const void* fn) {
+  static std::mutex mu;
+  static std::vector<const void*> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (std::find(done.begin(), done.end(), fn) != done.end()) return cudaSuccess;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess) done.push_back(fn);
+  return e;
+}
+
 // Launch the count-producing kernel of one family group: patterns
 // plist[0..gk) of the batch (indices into P.pats), ticket counter `slot`.
+// *fused (optional, in/out): run the whole search as one single-wave
+// scan_kernel<F, true> if every tile gets its own resident CTA; cleared when
+// that does not apply (then the count kernel is launched as usual).
 template <class F>
 static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int32_t* h_idx, const int32_t* d_idx,
-                        int gk, int slot, cudaStream_t st) {
+                        int gk, int slot, cudaStream_t st, bool* fused = nullptr) {
   int pre = 0, post = 0, maxL = 0;
   int64_t maxm = 1;
   bool any_periodic = false;
@@ -456,32 +473,44 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
     const int64_t wunits = (P.ntiles * NWARP + SMP_SEGS - 1) / SMP_SEGS;
     const int64_t units = ((wunits + SMP_WARPS - 1) / SMP_WARPS) * gk;
     const int64_t grid_s = std::min<int64_t>(units, (int64_t)c->nsm * per_sm_s);
+    if (fused) *fused = false;
     sampled_kernel<<<(int)grid_s, SMP_NT, smem_s, st>>>(P);
   } else {
     auto smem_for = [&](int ns) {
       return (size_t)SM_STAGES + (size_t)ns * P.stage_bytes + NWARP * SEG_WORDS * 4 +
              (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * 256 * 8 : 0);
     };
-    static std::once_flag attr_once;
-    cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [&] {
-      attr_err = cudaFuncSetAttribute(scan_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    });
-    CUDA_TRY(attr_err);
+    if (fused && *fused) {
+      // one stage: each CTA stages exactly one tile
+      P.nstages = 1;
+      const size_t smem1 = smem_for(1);
+      const void* fn = (const void*)scan_kernel<F, true>;
+      CUDA_TRY(allow_max_smem(fn));
+      int per_sm1 = 0;
+      CUDA_TRY(occupancy(fn, NT + 32, smem1, &per_sm1));
+      if (per_sm1 >= 1 && P.group_tiles <= (int64_t)c->nsm * per_sm1) {
+        scan_kernel<F, true><<<(int)P.group_tiles, NT + 32, smem1, st>>>(P);
+        g_launches++;
+        CUDA_TRY(cudaGetLastError());
+        return MB_OK;
+      }
+      *fused = false;
+    }
+    CUDA_TRY(allow_max_smem((const void*)scan_kernel<F, false>));
     // 3 stages, unless that leaves one CTA per SM where 2 stages fit two
     // (large halos: long periodic patterns keep 2 x 17 warps per SM busy)
     P.nstages = STAGES;
     size_t smem = smem_for(STAGES);
     int per_sm = 0;
-    CUDA_TRY(occupancy((const void*)scan_kernel<F>, NT + 32, smem, &per_sm));
+    CUDA_TRY(occupancy((const void*)scan_kernel<F, false>, NT + 32, smem, &per_sm));
     if (per_sm < 2 && STAGES > 2) {
       int per_sm2 = 0;
-      CUDA_TRY(occupancy((const void*)scan_kernel<F>, NT + 32, smem_for(2), &per_sm2));
+      CUDA_TRY(occupancy((const void*)scan_kernel<F, false>, NT + 32, smem_for(2), &per_sm2));
       if (per_sm2 > per_sm) P.nstages = 2, smem = smem_for(2), per_sm = per_sm2;
     }
     if (per_sm < 1) return fail(MB_ECUDA, "scan kernel does not fit on an SM");
     const int64_t grid = std::min<int64_t>(P.group_tiles, (int64_t)c->nsm * per_sm);
-    scan_kernel<F><<<(int)grid, NT + 32, smem, st>>>(P);
+    scan_kernel<F, false><<<(int)grid, NT + 32, smem, st>>>(P);
   }
   g_launches++;
   CUDA_TRY(cudaGetLastError());
@@ -497,24 +526,24 @@ static int family_key(const PatDev& d) {
 }
 
 static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, const int32_t* h_idx,
-                         const int32_t* d_idx, int gk, int slot, cudaStream_t st) {
+                         const int32_t* d_idx, int gk, int slot, cudaStream_t st, bool* fused = nullptr) {
   const PatDev& d = h_pats[h_idx[0]];
   switch (d.family) {
     case MB_FAM_SWAR:
-      if (d.m == 1) return launch_group<FiltSWAR<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
-      if (d.m == 2) return launch_group<FiltSWAR<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
-      return launch_group<FiltSWAR<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
-    case MB_FAM_WIN4: return launch_group<FiltWIN4>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+      if (d.m == 1) return launch_group<FiltSWAR<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      if (d.m == 2) return launch_group<FiltSWAR<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      return launch_group<FiltSWAR<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+    case MB_FAM_WIN4: return launch_group<FiltWIN4>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     case MB_FAM_ALIGNED:
-      if (d.nw == 3) return launch_group<FiltALIGNED<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
-      if (d.nw == 2) return launch_group<FiltALIGNED<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
-      return launch_group<FiltALIGNED<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
-    case MB_FAM_SAMPLED: return launch_group<SampledTag>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+      if (d.nw == 3) return launch_group<FiltALIGNED<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      if (d.nw == 2) return launch_group<FiltALIGNED<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      return launch_group<FiltALIGNED<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+    case MB_FAM_SAMPLED: return launch_group<SampledTag>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     case MB_FAM_SHIFTOR: {
       int64_t maxm = 0;
       for (int i = 0; i < gk; i++) maxm = std::max<int64_t>(maxm, h_pats[h_idx[i]].m);
-      if (maxm <= 32) return launch_group<FiltSO<32>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
-      return launch_group<FiltSO<64>>(c, P, h_pats, h_idx, d_idx, gk, slot, st);
+      if (maxm <= 32) return launch_group<FiltSO<32>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      return launch_group<FiltSO<64>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     }
   }
   return fail(MB_EINVAL, "unknown kernel family");
@@ -749,8 +778,10 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * SEG_WORDS, "bitmaps"))) return rc;
   if ((rc = grow(&c->toff, &c->toff_cap, T, "tile offsets"))) return rc;
   if ((rc = grow(&c->seglist, &c->seglist_cap, T, "expand queue"))) return rc;
-  if (nchunks > c->state_cap || c->epoch >= (1u << 24) - 4) {
-    if ((rc = grow(&c->state, &c->state_cap, nchunks, "look-back state"))) return rc;
+  // look-back flags: per offsets chunk, or per tile of a fused single-wave search
+  const int64_t nstate = std::max<int64_t>(nchunks, K == 1 ? std::min<int64_t>(P.total_tiles, 4 * (int64_t)c->nsm) : 0);
+  if (nstate > c->state_cap || c->epoch >= (1u << 24) - 4) {
+    if ((rc = grow(&c->state, &c->state_cap, nstate, "look-back state"))) return rc;
     CUDA_TRY(cudaMemsetAsync(c->state, 0, sizeof(uint64_t) * c->state_cap, st));
     // the epoch parity picks the expand-queue slot: restart it with clean tickets
     CUDA_TRY(cudaMemsetAsync(c->ticket, 0, NTICKETS * sizeof(unsigned long long), st));
@@ -768,8 +799,10 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.offsets_plus1 = offsets_plus1;
   P.out_base = out_base;
 
+  // one epoch per search: look-back flags of older searches never match, and
+  // its parity picks the expand-queue ticket slot (consecutive searches alternate)
+  P.epoch = ++c->epoch;
   auto finish = [&](bool unsorted) -> int {
-    P.epoch = ++c->epoch;
     P.unsorted_lists = unsorted ? 1 : 0;
     // programmatic dependent launches: offsets/expand CTAs are scheduled as the
     // previous grid drains and wait in-kernel (griddepcontrol.wait) for its
@@ -891,6 +924,14 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     c->mp_batches++;
   }
   // tickets are zero here: ctx creation, or the previous search's last kernel reset them
+  if (K == 1 && !mp_used) {
+    // one pattern: the whole search as one single-wave launch when every tile
+    // fits a resident CTA (texts up to ~9 MiB), else the count kernel + finish
+    bool fused = true;
+    const int32_t idx0 = 0;
+    if ((rc = launch_family(c, P, h_pats, &idx0, nullptr, 1, 0, st, &fused))) return rc;
+    return fused ? MB_OK : finish(false);
+  }
   // group patterns by family key (stable); a single group needs no index list
   std::vector<int> keys;
   std::vector<std::vector<int32_t>> groups;

@@ -5,12 +5,61 @@
 namespace mb {
 
 // ---------------------------------------------------------------- kernel 1: scan
+// FUSED (single-wave search of one pattern, grid = tiles, all resident): every
+// CTA takes ONE tile; its consumer warps keep their segment's match bits in
+// registers, the CTA's count goes through a warp look-back over the tiles (in
+// ticket order) and the positions are written straight to the output -- the
+// whole search is this one launch (fused_emit).
+__device__ __forceinline__ void fused_emit(const ScanParams& P, int64_t tk, uint32_t cnt, uint32_t ex, uint32_t w0,
+                                           uint32_t w1, int64_t pos0, int warp, int lane) {
+  __shared__ uint32_t s_wc[NWARP];
+  __shared__ int64_t s_base;
+  if (tk < 0) {  // no tile (cannot happen with grid = tiles): still count this CTA for the reset
+    if (warp == 0 && lane == 0 && atomicAdd(&P.ticket[TICKET_DONE], 1ULL) == (unsigned long long)(gridDim.x - 1))
+      for (int i = 0; i < NTICKETS; i++) P.ticket[i] = 0ULL;
+    return;
+  }
+  if (lane == 0) s_wc[warp] = cnt;
+  consumer_sync();
+  uint32_t tot = 0, before = 0;
+#pragma unroll
+  for (int w = 0; w < NWARP; w++) {
+    const uint32_t x = s_wc[w];
+    tot += x;
+    before += w < warp ? x : 0u;
+  }
+  if (warp == 0) {
+    int64_t excl = warp_lookback(P.state, tk, tot, P.epoch, lane);
+    if (lane == 0) {
+      excl += P.out_base ? *P.out_base : 0;
+      s_base = excl;
+      if (tk == P.ntiles - 1) P.offsets_plus1[0] = excl + tot;
+    }
+  }
+  consumer_sync();
+  if (P.out) {
+    int64_t o = s_base + before + ex;
+    const int64_t p = pos0 + 64 * lane;
+    uint64_t bits = ((uint64_t)w1 << 32) | w0;
+    while (bits) {
+      const int i = __ffsll((long long)bits) - 1;
+      bits &= bits - 1;
+      if (o < P.cap) P.out[o] = p + i;
+      o++;
+    }
+  }
+  // every CTA took its ticket before its tile arrived: the last one to get
+  // here zeroes all slots (tile tickets, this counter, both expand slots)
+  if (warp == 0 && lane == 0 && atomicAdd(&P.ticket[TICKET_DONE], 1ULL) == (unsigned long long)(gridDim.x - 1))
+    for (int i = 0; i < NTICKETS; i++) P.ticket[i] = 0ULL;
+}
+
 // Warp-specialised: warp NWARP is the TMA producer (ticket -> bulk copies of
 // the tile+halo and of the pattern into a free stage), warps 0..NWARP-1 are
 // consumers that each own one SEG-position segment of every tile.  Stages are
 // handed over through full/empty mbarriers; there is no block-wide barrier in
 // the loop, so warps drift independently within the ring.
-template <class Filt>
+template <class Filt, bool FUSED>
 __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
   StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
@@ -78,6 +127,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
         mbar_expect_tx(&full[s], tb + pb);
         bulk_g2s(st, pd->bytes, pb, &full[s]);
         if (tb) bulk_g2s(st + P.pat_cap + (cs - start), P.text + cs, tb, &full[s]);
+        if (FUSED) break;  // one tile per CTA (the consumers stop after it)
         if (++s == NS) s = 0, ph ^= 1u;
       }
     }
@@ -91,6 +141,8 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   int64_t blo = 0, bhi = -1;
   int s = 0;
   uint32_t ph = 0;
+  uint32_t f_w0 = 0, f_w1 = 0, f_ex = 0, f_cnt = 0;  // FUSED: the one tile's results
+  int64_t f_tk = -1, f_pos0 = 0;
   for (;; s = (s + 1 == NS) ? (ph ^= 1u, 0) : s + 1) {
     mbar_wait(&full[s], ph);
     const int64_t tk = hdr[s].tk;
@@ -282,26 +334,33 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
         if (lane >= d) inc += o;
       }
       cnt = __shfl_sync(0xffffffffu, inc, 31);
-      const int64_t g = tk * NWARP + warp;
-      if (cnt <= LIST_CAP) {
-        uint32_t j = inc - c2;
-        uint16_t* L = P.lists + g * LIST_CAP;
-        uint64_t bits = ((uint64_t)w1 << 32) | w0;
-        while (bits) {
-          const int i = __ffsll((long long)bits) - 1;
-          bits &= bits - 1;
-          L[j++] = (uint16_t)(c0 + 64 * lane + i);
-        }
+      if constexpr (FUSED) {
+        f_w0 = w0, f_w1 = w1, f_ex = inc - c2;
       } else {
-        reinterpret_cast<uint2*>(P.bitmaps + g * SEG_WORDS)[lane] = make_uint2(w0, w1);
+        const int64_t g = tk * NWARP + warp;
+        if (cnt <= LIST_CAP) {
+          uint32_t j = inc - c2;
+          uint16_t* L = P.lists + g * LIST_CAP;
+          uint64_t bits = ((uint64_t)w1 << 32) | w0;
+          while (bits) {
+            const int i = __ffsll((long long)bits) - 1;
+            bits &= bits - 1;
+            L[j++] = (uint16_t)(c0 + 64 * lane + i);
+          }
+        } else {
+          reinterpret_cast<uint2*>(P.bitmaps + g * SEG_WORDS)[lane] = make_uint2(w0, w1);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
+    if constexpr (FUSED) f_cnt = cnt, f_tk = tk, f_pos0 = B0 + c0 - P.off - pd.delta;
     if (lane == 0) {
-      P.counts[tk * NWARP + warp] = (uint16_t)cnt;
+      if constexpr (!FUSED) P.counts[tk * NWARP + warp] = (uint16_t)cnt;
       mbar_arrive(&empty[s]);
     }
+    if constexpr (FUSED) break;
   }
+  if constexpr (FUSED) fused_emit(P, f_tk, f_cnt, f_ex, f_w0, f_w1, f_pos0, warp, lane);
   MB_TRACE_MARK(1);
 }
 

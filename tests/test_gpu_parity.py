@@ -17,7 +17,8 @@ from cases import KNOWN, fuzz_cases, rand_bytes
 from paper_1012_2547_b200 import engine
 
 pytestmark = pytest.mark.gpu
-TILE = 16384
+TILE = 16384  # boundary spacing of the plants (the engine's tiles are 32 KiB: 2 of these)
+ENGINE_TILE = 32768
 SEG = 2048
 
 
@@ -168,6 +169,56 @@ def test_shiftor_edges(cuda, m):
         for off in (3, 9):
             got = engine.find(engine.Plan(p, "shiftor"), base[off:n]).cpu().numpy()
             assert np.array_equal(got, oracle.search(p, bytes(t)[off:n])), (m, sigma, off)
+
+
+@pytest.mark.parametrize("tiles", [1, 2, 150, 295, 296, 297, 300, 450])
+def test_single_wave_fused_boundary(cuda, tiles):
+    """Texts of up to one resident wave of tiles run as ONE fused launch (scan,
+    look-back over tiles, positions written directly); one tile more takes the
+    scan / offsets / expand pipeline.  Both must agree with the oracle, for
+    sparse, dense (sigma = 2, m = 3), periodic and long patterns, and for the
+    last alignment of the text."""
+    rng = np.random.default_rng(4000 + tiles)
+    n = tiles * ENGINE_TILE - 37
+    t = bytearray(rand_bytes(rng, 2, n))
+    pats = [bytes(t[5:8]), bytes(t[n - 40 : n - 20]), b"\x00\x01" * 40, bytes(t[n - 300 :])]
+    for p in pats:
+        check(p, bytes(t))
+    p = bytes(t[1000:1003])
+    want = oracle.search(p, bytes(t))
+    plan = engine.Plan(p)
+    d = torch.from_numpy(np.frombuffer(bytes(t), dtype=np.uint8).copy()).cuda()
+    out = torch.empty(want.size + 1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    l0 = engine.launch_count()
+    engine.find_into(plan, d, out, cnt)
+    launches = engine.launch_count() - l0
+    assert int(cnt.item()) == want.size
+    assert np.array_equal(out[: want.size].cpu().numpy(), want)
+    # one wave: >= 2 resident CTAs per SM x 148 SMs, at most 3 (544-thread CTAs)
+    if tiles <= 296:
+        assert launches == 1, launches
+    elif tiles > 3 * 148:
+        assert launches == 3, launches
+    else:
+        assert launches in (1, 3), launches
+
+
+def test_single_wave_dense_and_capacity(cuda):
+    """Fused single-wave search with every position a match (sigma = 1), count
+    only, and a capacity cut in the middle of a tile."""
+    t = b"a" * (4 << 20)
+    for m in (1, 2, 9, 64, 700):
+        check(b"a" * m, t)
+    plan = engine.Plan(b"aaa")
+    d = torch.from_numpy(np.frombuffer(t, dtype=np.uint8).copy()).cuda()
+    assert engine.count(plan, d) == len(t) - 2
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = torch.full((50000,), -1, dtype=torch.int64, device="cuda")
+    engine.find_into(plan, d, out, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == len(t) - 2
+    assert np.array_equal(out.cpu().numpy(), np.arange(50000))
 
 
 def test_count_only_and_overflow(cuda):
