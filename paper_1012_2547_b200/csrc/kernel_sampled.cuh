@@ -41,13 +41,39 @@ __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& 
     const int64_t sv = x - j;           // virtual start
     const int64_t bit = sv + pd.delta;  // = x - j + S - 1, inside [x, x + S)
     if (bit < ulo || bit >= uhi || bit < blo || bit > bhi) continue;
-    const uint8_t* tp = P.text + sv;
     MB_CHECK(sv >= P.off && sv + pd.m <= P.off + P.n);
-    bool ok = true;
-    for (int c = 0; c < pd.m && ok; c++) ok = __ldg(tp + c) == spat[c];
-    if (ok) found[nf++] = (uint32_t)(bit - ulo);
+    found[nf++] = (uint32_t)(bit - ulo);  // gram match: verified by the whole warp (sampled_verify)
   }
   return nf;
+}
+
+// Warp-cooperative verification of the lanes' gram matches: one candidate at
+// a time, lane l comparing text bytes l, l + 32, ... (independent coalesced
+// loads; a lane looping over m bytes alone would take ~100 cycles per byte).
+// Failed candidates are dropped from their lane's found[] (order kept).
+__device__ __forceinline__ int sampled_verify(const ScanParams& P, const PatDev& pd, const uint8_t* spat,
+                                              int64_t ulo, uint32_t* found, int nf, int lane) {
+  uint32_t pend = __ballot_sync(0xffffffffu, nf != 0);
+  uint32_t keep = 0;  // this lane's surviving entries (bit f)
+  while (pend) {
+    const int src = __ffs(pend) - 1;
+    pend &= pend - 1;
+    const int ns = __shfl_sync(0xffffffffu, nf, src);
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+      if (f >= ns) break;
+      const uint32_t rel = __shfl_sync(0xffffffffu, found[f], src);
+      const uint8_t* tp = P.text + (ulo + rel - pd.delta);
+      bool bad = false;
+      for (int c = lane; c < pd.m; c += 32) bad |= __ldg(tp + c) != spat[c];
+      if (!__any_sync(0xffffffffu, bad) && lane == src) keep |= 1u << f;
+    }
+  }
+  int n2 = 0;
+#pragma unroll
+  for (int f = 0; f < 4; f++)
+    if ((keep >> f) & 1u) found[n2++] = found[f];
+  return n2;
 }
 
 #ifndef MB_SMP_MINB
@@ -127,6 +153,7 @@ __global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const Scan
           const uint32_t w[8] = {g[r].x, g[r].y, g[r].z, g[r].w, g2[r].x, g2[r].y, g2[r].z, g2[r].w};
           nf = sampled_probe(P, pd, bloom, bstart, bent, spat, w, x, ulo, uhi, blo, bhi, found);
         }
+        nf = sampled_verify(P, pd, spat, ulo, found, nf, lane);
         // ascending: lanes own disjoint increasing bit ranges; bucket entries are in ascending start order
         const uint32_t any = __ballot_sync(0xffffffffu, nf != 0);
         if (any) {
