@@ -79,6 +79,11 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_acquire(const unsigned long long* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -101,9 +106,9 @@ __device__ __forceinline__ void split_tile(int64_t tile, int64_t ntiles, int* k,
   }
 }
 
-// End of offsets_kernel: the last CTA to finish zeroes every ticket but
-// keep_slot (this search's expand-queue count, read by expand_kernel; the next
-// search, of the other epoch parity, zeroes it), so no search needs a memset.
+// End of a search's last kernel (offsets_kernel of a count-only search): the
+// last CTA to finish zeroes every ticket but keep_slot (-1: none), so the next
+// search needs no memset.  (expand_kernel zeroes them at its start instead.)
 // Call from all threads of every CTA.
 __device__ __forceinline__ void reset_tickets_if_last(unsigned long long* ticket, int ntickets, int done_slot,
                                                       int keep_slot) {

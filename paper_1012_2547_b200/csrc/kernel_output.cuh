@@ -38,16 +38,25 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   MB_TRACE_MARK(2);
   pdl_trigger();  // expand_kernel's CTAs get resident now and wait for this grid in pdl_wait
-  pdl_wait();     // counts / lists / bitmaps of the count kernel(s)
-  MB_TRACE_MARK(4);
-  MB_TRACE_MARK(5);
   // chunk id: CTA index when the whole grid is co-resident (any order is
-  // then safe for the look-back), else a ticket in CTA start order
+  // then safe), else a ticket in CTA start order.  Everything that does not
+  // depend on the count kernel's results is set up before pdl_wait, while
+  // its tail drains: chunk id, this thread's first pattern and its shift.
   if (tid == 0) s_chunk = P.offs_resident ? (int64_t)blockIdx.x : (int64_t)atomicAdd(&P.ticket[TICKET_OFFSETS], 1ULL);
   __syncthreads();
   const int64_t ch = s_chunk;
   const int64_t nseg = P.total_tiles * NWARP;
   const int64_t base = ch * (int64_t)(NT * PER);
+  const int64_t seg_per_pat = P.ntiles * NWARP;
+  // pattern of this thread's first segment and the segment's rank within it
+  // (one division per thread; the CSR end is written at rank seg_per_pat - 1)
+  int64_t kq = (base + (int64_t)tid * PER) / seg_per_pat;
+  int64_t rem = base + (int64_t)tid * PER - kq * seg_per_pat;
+  int cur_k = (int)kq;
+  int64_t shift = kq < P.K ? P.pats[kq].delta + P.off : 0;
+  pdl_wait();     // counts / lists / bitmaps of the count kernel(s)
+  MB_TRACE_MARK(4);
+  MB_TRACE_MARK(5);
   static_assert(PER % 8 == 0, "vector loads of 8 uint16 counts");
   // PER uint16 counts kept packed two per register (2 CTAs per SM fit)
   uint32_t v2[PER / 2];
@@ -66,6 +75,14 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
 #pragma unroll
   for (int h = 0; h < PER / 2; h++) tsum32 += (v2[h] & 0xFFFFu) + (v2[h] >> 16);
   const int64_t tsum = tsum32;
+  // the first 8 list entries of this thread's first non-empty segment are
+  // fetched now, so they arrive during the exclusive-offset computation
+  int fq = -1;
+#pragma unroll
+  for (int q = PER - 1; q >= 0; q--)
+    if ((v2[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) fq = q;
+  uint4 pre = make_uint4(0, 0, 0, 0);
+  if (fq >= 0 && P.out) pre = *reinterpret_cast<const uint4*>(P.lists + (base + (int64_t)tid * PER + fq) * LIST_CAP);
   int64_t inc = tsum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -79,17 +96,43 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     chunk_total += wsum[q];
     wbefore += q < warp ? wsum[q] : 0;
   }
-  // block-wide decoupled look-back: the whole CTA reads NT predecessors per
-  // round trip (a 16 GiB single-pattern search has 512 chunks: one round
-  // trip); the nearest inclusive predecessor and the sum up to it are found
-  // with warp ballots / shuffles and one word per warp in smem (no smem atomics)
   __shared__ int s_first[NWARP];
   __shared__ unsigned long long s_part[NWARP];
   if (tid == 0) {
     st_relaxed(&P.state[ch], pack_state(P.epoch, ch == 0 ? ST_INCL : ST_AGG, (uint64_t)chunk_total));
     s_excl = 0;
   }
+  MB_TRACE_MARK(24);
+  MB_TRACE_MARK(25);
   int64_t j = ch - 1;  // newest predecessor of this window
+  if (P.offs_resident) {
+    // every chunk is resident: one grid barrier once all chunk totals are
+    // published, then each CTA sums its predecessors' totals directly (no
+    // polling of not-yet-published flags by every thread of every CTA)
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&P.ticket[TICKET_OFFBAR], 1ULL);
+      while (ld_acquire(&P.ticket[TICKET_OFFBAR]) < (unsigned long long)gridDim.x) __nanosleep(32);
+    }
+    __syncthreads();
+    unsigned long long v = 0;
+    for (int64_t i = tid; i < ch; i += NT) v += ld_relaxed(&P.state[i]) & ((1ULL << 38) - 1);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+    if (lane == 0) s_part[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long sum = 0;
+#pragma unroll
+      for (int w = 0; w < NWARP; w++) sum += s_part[w];
+      s_excl = (int64_t)sum;
+    }
+    j = -1;
+  }
+  // otherwise block-wide decoupled look-back: the whole CTA reads NT
+  // predecessors per round trip; the nearest inclusive predecessor and the sum
+  // up to it are found with warp ballots / shuffles and one word per warp in
+  // smem (no smem atomics)
   while (j >= 0) {     // uniform across the CTA (j, first read after barriers)
     const int64_t idx = j - tid;
     uint64_t sv = 0;
@@ -126,12 +169,13 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   __syncthreads();
   MB_TRACE_MARK(7);
   if (tid == 0) {
-    if (ch > 0) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_INCL, (uint64_t)(s_excl + chunk_total)));
+    // look-back mode only: in barrier mode other CTAs may still be summing
+    // this chunk's published total
+    if (ch > 0 && !P.offs_resident) st_relaxed(&P.state[ch], pack_state(P.epoch, ST_INCL, (uint64_t)(s_excl + chunk_total)));
     s_excl += P.out_base ? *P.out_base : 0;
   }
   __syncthreads();
   int64_t run = s_excl + wbefore + inc - tsum;
-  const int64_t seg_per_pat = P.ntiles * NWARP;
   // Sorted sparse segments (<= LIST_CAP uint16 offsets) are expanded right here;
   // dense or unsorted (MP) segments are queued for expand_kernel with their offset.
   // lists of up to FUSE_MAX entries are expanded right here by their thread
@@ -139,12 +183,6 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   // network); longer ones go to expand_kernel, whose warp per segment writes
   // them coalesced (a thread looping over 32 scattered stores is slower)
   const uint32_t fuse_max = !P.out ? 0u : P.unsorted_lists ? (uint32_t)min(FUSE_MAX, 8) : (uint32_t)FUSE_MAX;
-  int cur_k = -1;
-  int64_t shift = 0;
-  // pattern of this thread's first segment and the segment's rank within it
-  // (one division per thread; the CSR end is written at rank seg_per_pat - 1)
-  int64_t kq = (base + (int64_t)tid * PER) / seg_per_pat;
-  int64_t rem = base + (int64_t)tid * PER - kq * seg_per_pat;
   // the counts go through shared memory (transposed: conflict-free) so the
   // output loop below is not unrolled and the kernel stays at 2 CTAs per SM
 #pragma unroll
@@ -169,10 +207,18 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
           const int64_t pos0 = tau * TILE - shift;
           const uint16_t* L = P.lists + t * LIST_CAP;
           if (!P.unsorted_lists) {
-            for (uint32_t e = 0; e < vq; e++)
-              if (run + e < P.cap) P.out[run + e] = pos0 + L[e];
+            for (uint32_t e = 0; e < vq; e++) {
+              uint32_t x;
+              if (q == fq && e < 8) {  // prefetched
+                const uint32_t w = (e >> 1) == 0 ? pre.x : (e >> 1) == 1 ? pre.y : (e >> 1) == 2 ? pre.z : pre.w;
+                x = (w >> (16 * (e & 1))) & 0xFFFFu;
+              } else {
+                x = L[e];
+              }
+              if (run + e < P.cap) P.out[run + e] = pos0 + x;
+            }
           } else {
-            const uint4 raw = *reinterpret_cast<const uint4*>(L);  // 8 slots (64-byte aligned list)
+            const uint4 raw = q == fq ? pre : *reinterpret_cast<const uint4*>(L);  // 8 slots (64-byte aligned list)
             uint32_t v[8] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16,
                              raw.z & 0xFFFFu, raw.z >> 16, raw.w & 0xFFFFu, raw.w >> 16};
 #pragma unroll
@@ -195,7 +241,8 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     if (++rem == seg_per_pat) rem = 0, kq++;
   }
   MB_TRACE_SYNC_MARK(9);
-  reset_tickets_if_last(P.ticket, NTICKETS, TICKET_DONE, P.dense_slot);
+  // ticket reset for the next search: expand_kernel does it when it follows
+  if (!P.out || P.cap <= 0) reset_tickets_if_last(P.ticket, NTICKETS, TICKET_DONE, -1);
 }
 
 // ------------------------------------------------ kernel 3: expansion
@@ -232,6 +279,10 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
   MB_TRACE_MARK(10);
   pdl_wait();  // queue and offsets of offsets_kernel
   MB_TRACE_MARK(12);
+  // the count and offsets grids are complete: zero every ticket but this
+  // search's queue count (read below; the next search, of the other epoch
+  // parity, zeroes it), so the next search needs no memset
+  if (blockIdx.x == 0 && threadIdx.x < NTICKETS && threadIdx.x != P.dense_slot) P.ticket[threadIdx.x] = 0ULL;
   const int64_t nq = (int64_t)P.ticket[P.dense_slot];
   const int64_t stride = (int64_t)gridDim.x * EXP_WARPS;
   int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp;

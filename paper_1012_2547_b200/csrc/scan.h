@@ -51,7 +51,8 @@ constexpr int TICKET_MP0 = 13;
 constexpr int TICKET_DENSE = 20;    // segments queued for expand_kernel (even epochs; odd: TICKET_DENSE_ODD)
 constexpr int TICKET_DONE = 21;     // offsets_kernel CTAs that finished (the last one zeroes the slots)
 constexpr int TICKET_DENSE_ODD = 22;
-constexpr int NTICKETS = 23;
+constexpr int TICKET_OFFBAR = 23;   // offsets_kernel grid barrier (co-resident grid)
+constexpr int NTICKETS = 24;
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 
 struct StageHdr {
@@ -101,8 +102,8 @@ struct ScanParams {
   const unsigned int* run_if;  // count kernels exit at once unless *run_if != 0 (batch-pass fallback)
   const unsigned int* need;    // per batch pattern: 0 = the batch pass covered it (skip its tiles), else scan
   int dense_slot;              // ticket slot counting this search's expand queue (alternates by epoch parity:
-                               // offsets_kernel's last CTA zeroes every slot but this one, so the
-                               // expand grid needs no atomics; the next search zeroes it)
+                               // expand_kernel zeroes every slot but this one once the offsets grid is
+                               // complete; the next search, of the other parity, zeroes it)
   int offs_resident;           // offsets_kernel grid fits on the GPU at once: chunk = blockIdx.x
 };
 

@@ -84,7 +84,9 @@ def test_config5_full(cuda):
     for p in inputs.config5_patterns():
         got = engine.find(engine.Plan(p), d).cpu().numpy()
         want = oracle.search(p, t, "SO", threads=THREADS)  # BF is O(n*m) on a^m
-        assert np.array_equal(got, want), (len(p), p[-1:])
+        assert np.array_equal(got, want), (len(p), p[-1:], got.size, want.size,
+                                           sorted(set(want.tolist()) - set(got.tolist()))[:5],
+                                           sorted(set(got.tolist()) - set(want.tolist()))[:5])
         props(got, p, t)
 
 

@@ -108,6 +108,57 @@ float run_region_rot(int64_t* d, size_t n, int grid, int block, int rmul) {
   return nseg * (2048 - 5) * 8.0 * 10 / (ms * 1e-3) / 1e9;
 }
 
+// region-per-warp through TMA bulk stores: the warp fills a 16 KB smem buffer
+// (double-buffered) and one lane issues cp.async.bulk.global.shared for the
+// 16-B aligned body; head/tail elements are plain stores
+__global__ void __launch_bounds__(128) k_region_tma(int64_t* __restrict__ out, size_t nseg, int64_t base, int off) {
+  extern __shared__ __align__(128) int64_t sbuf[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t w0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const int len = 2048 - 5;
+  int buf = 0;
+  for (size_t g = w0; g < nseg; g += nw, buf ^= 1) {
+    int64_t* d = out + g * 2048 + off;
+    const int64_t v0 = base + (int64_t)(g * 2048);
+    const int head = (int)(((uintptr_t)d >> 3) & 1);
+    const int body = (len - head) & ~1;
+    int64_t* sb = sbuf + (warp * 2 + buf) * 2048;
+    // the bulk copy that read this buffer two iterations ago must be done
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    for (int i = lane; i < body; i += 32) sb[i] = v0 + head + i;
+    if (lane == 0 && head) d[0] = v0;
+    if (lane == 0 && head + body < len) d[len - 1] = v0 + len - 1;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d + head),
+                   "r"((uint32_t)__cvta_generic_to_shared(sb)), "r"((uint32_t)(body * 8))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+float run_region_tma(int64_t* d, size_t n, int grid, int off) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const size_t nseg = n / 2048 - 1;
+  const size_t smem = 4 * 2 * 2048 * 8;
+  cudaFuncSetAttribute(k_region_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_region_tma<<<grid, 128, smem>>>(d, nseg, 7, off);
+  cudaEventRecord(a);
+  for (int r = 0; r < 10; r++) k_region_tma<<<grid, 128, smem>>>(d, nseg, r, off);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("  (tma err: %s)\n", cudaGetErrorString(cudaGetLastError()));
+  return nseg * (2048 - 5) * 8.0 * 10 / (ms * 1e-3) / 1e9;
+}
+
 // region-per-CTA of S consecutive 16 KB runs: the whole block writes S*2048
 // int64 at a time (a CTA expanding S consecutive dense segments)
 template <int S>
@@ -206,11 +257,10 @@ int main() {
            run_region_v<5, 2, false>(d, n, g, 256), run_region_v<0, 2, false>(d, n, g, 256),
            run_region_v<5, 2, true>(d, n, g, 256), run_region_v<5, 1, true>(d, n, g, 256));
   }
-  for (int mult : {4, 8, 16}) {
+  for (int mult : {1, 2, 3}) {
     const int g = nsm * mult;
-    printf("region-per-warp x128 grid %5d rotated: mul 0 %7.0f | 32 %7.0f | 416 %7.0f | 1000 %7.0f | 1237 %7.0f GB/s\n", g,
-           run_region_rot(d, n, g, 128, 0), run_region_rot(d, n, g, 128, 32), run_region_rot(d, n, g, 128, 416),
-           run_region_rot(d, n, g, 128, 1000), run_region_rot(d, n, g, 128, 1237));
+    printf("region-per-warp TMA bulk store grid %5d x 128: off5 %7.0f | off0 %7.0f GB/s\n", g,
+           run_region_tma(d, n, g, 5), run_region_tma(d, n, g, 0));
   }
   cudaFree(d);
   return 0;

@@ -14,7 +14,8 @@ NAMES = {0: "scan entry (first CTA)", 1: "scan exit (last CTA)", 2: "offsets ent
          9: "offsets exit (last)", 10: "expand entry (first)", 12: "expand after pdl_wait (first)",
          13: "expand exit (last)", 14: "fused: scan done (first)", 15: "fused: scan done (last)",
          16: "fused: barrier 1 passed (first)", 17: "fused: barrier 1 passed (last)",
-         19: "fused: offsets done (last)", 20: "fused: barrier 2 passed (first)", 21: "fused: exit (last)"}
+         19: "fused: offsets done (last)", 24: "offsets aggregate published (first)",
+         25: "offsets aggregate published (last)", 20: "fused: barrier 2 passed (first)", 21: "fused: exit (last)"}
 
 n = int(sys.argv[1])
 sigma = int(sys.argv[2]) if len(sys.argv) > 2 else 256
