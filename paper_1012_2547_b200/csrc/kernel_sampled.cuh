@@ -47,33 +47,26 @@ __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& 
   return nf;
 }
 
-// Warp-cooperative verification of the lanes' gram matches: one candidate at
-// a time, lane l comparing text bytes l, l + 32, ... (independent coalesced
-// loads; a lane looping over m bytes alone would take ~100 cycles per byte).
-// Failed candidates are dropped from their lane's found[] (order kept).
-__device__ __forceinline__ int sampled_verify(const ScanParams& P, const PatDev& pd, const uint8_t* spat,
-                                              int64_t ulo, uint32_t* found, int nf, int lane) {
-  uint32_t pend = __ballot_sync(0xffffffffu, nf != 0);
-  uint32_t keep = 0;  // this lane's surviving entries (bit f)
-  while (pend) {
-    const int src = __ffs(pend) - 1;
-    pend &= pend - 1;
-    const int ns = __shfl_sync(0xffffffffu, nf, src);
-#pragma unroll
-    for (int f = 0; f < 4; f++) {
-      if (f >= ns) break;
-      const uint32_t rel = __shfl_sync(0xffffffffu, found[f], src);
-      const uint8_t* tp = P.text + (ulo + rel - pd.delta);
-      bool bad = false;
-      for (int c = lane; c < pd.m; c += 32) bad |= __ldg(tp + c) != spat[c];
-      if (!__any_sync(0xffffffffu, bad) && lane == src) keep |= 1u << f;
-    }
+// Warp-cooperative verification of the gram matches appended to a warp's list
+// wl[from, n) (ascending): one candidate at a time, lane l comparing text
+// bytes l, l + 32, ... (independent coalesced loads; one lane looping over m
+// bytes alone took ~100 cycles per byte, 63 us for a 1024-byte occurrence).
+// Failures are dropped in place (order kept); returns the new list length.
+// Run outside the sample loop, so that loop's registers do not carry it.
+__device__ __forceinline__ uint32_t sampled_verify(const ScanParams& P, const PatDev& pd, const uint8_t* spat,
+                                                   int64_t ulo, uint32_t* wl, uint32_t from, uint32_t n, int lane) {
+  uint32_t keep = from;
+  for (uint32_t e = from; e < n; e++) {
+    const uint32_t rel = wl[e];
+    const uint8_t* tp = P.text + (ulo + rel - pd.delta);
+    bool bad = false;
+    for (int c = lane; c < pd.m; c += 32) bad |= __ldg(tp + c) != spat[c];
+    const bool ok = !__any_sync(0xffffffffu, bad);
+    if (ok && lane == 0) wl[keep] = rel;  // keep <= e: in place
+    keep += ok ? 1u : 0u;
+    __syncwarp();
   }
-  int n2 = 0;
-#pragma unroll
-  for (int f = 0; f < 4; f++)
-    if ((keep >> f) & 1u) found[n2++] = found[f];
-  return n2;
+  return keep;
 }
 
 #ifndef MB_SMP_MINB
@@ -130,8 +123,12 @@ __global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const Scan
     const int64_t tlimit = P.off + P.n;  // virtual end of the text
     const int64_t i0 = ulo / S, i1 = (uhi - 1) / S;
     uint32_t* wl = lists + warp * SMP_LIST;
-    uint32_t nmatch = 0;
+    uint32_t nmatch = 0, nver = 0;  // wl[0, nver) verified, wl[nver, nmatch) gram matches
     for (int64_t ib = i0; ib <= i1; ib += 32 * SMP_ILP) {
+      if (nmatch + 4 * 32 * SMP_ILP > SMP_LIST) {  // room for this batch's gram matches (<= 4 per sample)
+        __syncwarp();
+        nmatch = nver = sampled_verify(P, pd, spat, ulo, wl, nver, nmatch, lane);
+      }
       uint4 g[SMP_ILP], g2[SMP_ILP];
 #pragma unroll
       for (int r = 0; r < SMP_ILP; r++) {  // issue every load of the batch first
@@ -153,7 +150,6 @@ __global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const Scan
           const uint32_t w[8] = {g[r].x, g[r].y, g[r].z, g[r].w, g2[r].x, g2[r].y, g2[r].z, g2[r].w};
           nf = sampled_probe(P, pd, bloom, bstart, bent, spat, w, x, ulo, uhi, blo, bhi, found);
         }
-        nf = sampled_verify(P, pd, spat, ulo, found, nf, lane);
         // ascending: lanes own disjoint increasing bit ranges; bucket entries are in ascending start order
         const uint32_t any = __ballot_sync(0xffffffffu, nf != 0);
         if (any) {
@@ -171,7 +167,9 @@ __global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const Scan
         }
       }
     }
-    if (nmatch > SMP_LIST) __trap();  // impossible for the plans that choose K3 (see plan.cpp)
+    __syncwarp();
+    if (nmatch > nver) nmatch = sampled_verify(P, pd, spat, ulo, wl, nver, nmatch, lane);
+    if (nmatch > SMP_LIST) __trap();  // impossible: verified before the list could overflow
     __syncwarp();
     // per-segment counts and uint16 tile-relative lists, as scan_kernel writes them
     for (int sl = lane; sl < nsegs; sl += 32) {
