@@ -140,6 +140,8 @@ struct mb_ctx {
   int64_t toff_cap = 0;
   int64_t* seglist = nullptr;
   int64_t seglist_cap = 0;
+  int64_t* qpos = nullptr;
+  int64_t qpos_cap = 0;
   int32_t* plist = nullptr;
   int64_t plist_cap = 0;
   std::vector<int32_t> h_plist;
@@ -302,6 +304,7 @@ void mb_ctx_destroy(mb_ctx* c) {
   cudaFree(c->bitmaps);
   cudaFree(c->toff);
   cudaFree(c->seglist);
+  cudaFree(c->qpos);
   cudaFree(c->plist);
   cudaFree(c->mp_tab);
   cudaFree(c->need);
@@ -778,6 +781,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   if ((rc = grow(&c->bitmaps, &c->bitmaps_cap, T * SEG_WORDS, "bitmaps"))) return rc;
   if ((rc = grow(&c->toff, &c->toff_cap, T, "tile offsets"))) return rc;
   if ((rc = grow(&c->seglist, &c->seglist_cap, T, "expand queue"))) return rc;
+  if ((rc = grow(&c->qpos, &c->qpos_cap, T, "expand queue positions"))) return rc;
   // look-back flags: per offsets chunk, or per tile of a fused single-wave search
   const int64_t nstate = std::max<int64_t>(nchunks, K == 1 ? std::min<int64_t>(P.total_tiles, 4 * (int64_t)c->nsm) : 0);
   if (nstate > c->state_cap || c->epoch >= (1u << 24) - 4) {
@@ -792,6 +796,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.bitmaps = c->bitmaps;
   P.toff = c->toff;
   P.seglist = c->seglist;
+  P.qpos = c->qpos;
   P.state = c->state;
   P.ticket = c->ticket;
   P.out = d_out;
@@ -986,13 +991,13 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
 }
 
 // Run a batch whose params are on the device as sub-batches under the scratch
-// budget (~338 B per 2 KiB segment per pattern: counts, list, bitmap, offset,
+// budget (~346 B per 2 KiB segment per pattern: counts, list, bitmap, offset, position,
 // queue; a third of free memory, <= 16 GiB), chained through d_offsets.
 static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text, int64_t n,
                      int64_t* d_out, int64_t cap, int64_t* d_offsets, cudaStream_t st, const BatchPass* bp,
                      const uint32_t* d_tab) {
   CUDA_TRY(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
-  const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 338.0;
+  const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 346.0;
   // batches needing <= 1 GiB of scratch, or no more than a previous call
   // already got, skip the memory query (cudaMemGetInfo costs up to ms)
   double budget = std::max(1.0 * (1ULL << 30), c->scratch_ok);

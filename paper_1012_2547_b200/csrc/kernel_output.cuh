@@ -195,16 +195,12 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     const uint32_t vq = (s_cnt[(q >> 1) * NT + tid] >> (16 * (q & 1))) & 0xFFFFu;
     if (t < nseg) {
       if (vq && P.out) {
+        if (kq != cur_k) {  // (kq, rem) = (pattern, rank) of segment t
+          shift = P.pats[kq].delta + P.off;
+          cur_k = (int)kq;
+        }
         if (vq <= fuse_max) {
-          const int64_t tile = t / NWARP;
-          int k;
-          int64_t tau;
-          split_tile(tile, P.ntiles, &k, &tau);
-          if (k != cur_k) {
-            shift = P.pats[k].delta + P.off;
-            cur_k = k;
-          }
-          const int64_t pos0 = tau * TILE - shift;
+          const int64_t pos0 = (rem / NWARP) * TILE - shift;  // position of tile offset 0
           const uint16_t* L = P.lists + t * LIST_CAP;
           if (!P.unsorted_lists) {
             for (uint32_t e = 0; e < vq; e++) {
@@ -230,9 +226,11 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
               if ((uint32_t)e < vq && run + e < P.cap) P.out[run + e] = pos0 + v[e];
           }
         } else {
-          P.toff[t] = run;
+          // queue entry: segment | count << 48, output offset, position of bit 0
           const unsigned long long slot = atomicAdd(&P.ticket[P.dense_slot], 1ULL);
-          P.seglist[slot] = t;
+          P.seglist[slot] = t | ((int64_t)vq << 48);
+          P.toff[slot] = run;
+          P.qpos[slot] = rem * SEG - shift;
         }
       }
       if (rem == seg_per_pat - 1) P.offsets_plus1[kq] = run + vq;
@@ -247,30 +245,42 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
 
 // ------------------------------------------------ kernel 3: expansion
 // The segments offsets_kernel queued (dense, or MP's unsorted lists), a warp
-// per segment, software-pipelined: the queue entry two steps ahead and the
-// count / offset / list / bitmap words one step ahead are in flight while the
-// current segment is written.  Unsorted (MP) lists get a 32-lane bitonic
-// sort; dense segments are staged in smem as uint16 offsets, then streamed out
-// with coalesced 256-byte stores.
+// per queue entry, software-pipelined: the entry two steps ahead and the list
+// / bitmap words one step ahead are in flight while the current segment is
+// written.  An entry carries everything but the match bits (segment | count,
+// output offset, position of bit 0), so no pattern lookup or division sits on
+// the path.  Unsorted (MP) lists get a 32-lane bitonic sort; dense segments
+// are staged in smem as uint16 offsets (set bits extracted one by one, or, at
+// >= 50% density, by an unrolled predicated pass over all 64 bits of a lane),
+// then streamed out with coalesced 256-byte stores.
 #ifndef MB_EXP_WARPS
 #define MB_EXP_WARPS 8
 #endif
 constexpr int EXP_WARPS = MB_EXP_WARPS;
 
 struct ExpSeg {  // one queued segment as a lane holds it
-  int64_t g, o;
+  int64_t g, o, sp;
   uint32_t c, lv, xa, xb;
 };
-__device__ __forceinline__ ExpSeg exp_load(const ScanParams& P, int64_t g, int lane) {
+__device__ __forceinline__ void exp_head(const ScanParams& P, int64_t qi, int64_t* ent, int64_t* o, int64_t* sp) {
+  *ent = P.seglist[qi];
+  *o = P.toff[qi];
+  *sp = P.qpos[qi];
+}
+__device__ __forceinline__ ExpSeg exp_load(const ScanParams& P, int64_t ent, int64_t o, int64_t sp, int lane) {
   ExpSeg e;
-  e.g = g;
-  e.c = P.counts[g];
-  e.o = P.toff[g];
-  e.lv = P.lists[g * LIST_CAP + lane];  // meaningful when c <= LIST_CAP
-  e.xa = P.bitmaps[g * SEG_WORDS + lane];  // meaningful when c > LIST_CAP
-  e.xb = P.bitmaps[g * SEG_WORDS + 32 + lane];
+  e.g = ent & ((1LL << 48) - 1);
+  e.c = (uint32_t)(ent >> 48);
+  e.o = o;
+  e.sp = sp;
+  e.lv = P.lists[e.g * LIST_CAP + lane];  // meaningful when c <= LIST_CAP
+  e.xa = P.bitmaps[e.g * SEG_WORDS + lane];  // meaningful when c > LIST_CAP
+  e.xb = P.bitmaps[e.g * SEG_WORDS + 32 + lane];
   return e;
 }
+// smem run index of entry e: XOR-swizzled by its 32-entry block, so all-ones
+// words (lane l writing entries 64 l + k) do not pile onto two banks
+__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 5) & 31u); }
 
 __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -287,34 +297,28 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
   const int64_t stride = (int64_t)gridDim.x * EXP_WARPS;
   int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp;
   ExpSeg cur;
-  int64_t g_nxt = -1;
+  int64_t h_ent = 0, h_o = 0, h_sp = 0;  // entry qi + stride
+  bool have_nxt = false;
   if (qi < nq) {
-    cur = exp_load(P, P.seglist[qi], lane);
-    g_nxt = qi + stride < nq ? P.seglist[qi + stride] : -1;
+    int64_t ent, o, sp;
+    exp_head(P, qi, &ent, &o, &sp);
+    cur = exp_load(P, ent, o, sp, lane);
+    if (qi + stride < nq) exp_head(P, qi + stride, &h_ent, &h_o, &h_sp), have_nxt = true;
   }
-  int cur_k = -1;
-  int64_t shift = 0;
   while (qi < nq) {
     ExpSeg nxt;
-    int64_t g_nn = -1;
-    if (g_nxt >= 0) {  // prefetch: issued before the current segment's work
-      nxt = exp_load(P, g_nxt, lane);
-      if (qi + 2 * stride < nq) g_nn = P.seglist[qi + 2 * stride];
+    int64_t n_ent = 0, n_o = 0, n_sp = 0;
+    bool have_nn = false;
+    if (have_nxt) {  // prefetch: issued before the current segment's work
+      nxt = exp_load(P, h_ent, h_o, h_sp, lane);
+      if (qi + 2 * stride < nq) exp_head(P, qi + 2 * stride, &n_ent, &n_o, &n_sp), have_nn = true;
     }
-    const int64_t g = cur.g;
     const uint32_t c = cur.c;
     const int64_t o = cur.o;
-    const int64_t tile = g / NWARP;
-    int k;
-    int64_t tau;
-    split_tile(tile, P.ntiles, &k, &tau);
-    if (k != cur_k) {
-      shift = P.pats[k].delta + P.off;
-      cur_k = k;
-    }
-    const int64_t pos0 = tau * TILE - shift;  // tile-relative offsets below
     if (o < P.cap) {
       if (c <= LIST_CAP) {
+        // lists hold tile-relative offsets: position = tile origin + entry
+        const int64_t pos0 = cur.sp - (cur.g & (NWARP - 1)) * SEG;
         uint32_t v = lane < (int)c ? (cur.lv & 0xFFFFu) : 0xFFFFFFFFu;
         if (P.unsorted_lists) {  // MP fills list slots atomically: warp bitonic sort of <= 32 offsets
 #pragma unroll
@@ -330,10 +334,8 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
         if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + v;
       } else {
         // dense: exclusive popcount prefix of the 64 words (2 per lane); each
-        // lane extracts its words' set bits into the warp's smem run (index
-        // XOR-swizzled by its 32-entry block so all-ones words do not pile onto
-        // two banks); the warp then streams the c positions out coalesced
-        const int64_t segpos = pos0 + (g % NWARP) * SEG;
+        // lane writes its words' set bits into the warp's smem run; the warp
+        // then streams the c positions out coalesced
         const uint32_t pa = __popc(cur.xa), pb = __popc(cur.xb);
         uint32_t ia = pa, ib = pb;
 #pragma unroll
@@ -343,31 +345,43 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
           if (lane >= d) ia += va, ib += vb;
         }
         const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31);
-        uint32_t x = cur.xa, e = ia - pa;
-        while (x) {
-          const uint32_t b = __ffs(x) - 1;
-          x &= x - 1;
-          sb[e ^ ((e >> 5) & 31u)] = (uint16_t)(32u * lane + b);
-          e++;
-        }
-        x = cur.xb, e = ta + ib - pb;
-        while (x) {
-          const uint32_t b = __ffs(x) - 1;
-          x &= x - 1;
-          sb[e ^ ((e >> 5) & 31u)] = (uint16_t)(32u * (32 + lane) + b);
-          e++;
+        uint32_t ea = ia - pa, eb = ta + ib - pb;
+        const uint32_t ba = 32u * lane, bb = 32u * (32 + lane);
+        if (c >= SEG / 2) {  // >= 50% set: every bit position once, predicated
+#pragma unroll
+          for (int b = 0; b < 32; b++) {
+            if ((cur.xa >> b) & 1u) sb[swz(ea)] = (uint16_t)(ba + b), ea++;
+            if ((cur.xb >> b) & 1u) sb[swz(eb)] = (uint16_t)(bb + b), eb++;
+          }
+        } else {
+          uint32_t x = cur.xa;
+          while (x) {
+            const uint32_t b = __ffs(x) - 1;
+            x &= x - 1;
+            sb[swz(ea++)] = (uint16_t)(ba + b);
+          }
+          x = cur.xb;
+          while (x) {
+            const uint32_t b = __ffs(x) - 1;
+            x &= x - 1;
+            sb[swz(eb++)] = (uint16_t)(bb + b);
+          }
         }
         __syncwarp();
         const uint32_t lim = (uint32_t)(P.cap - o < (int64_t)c ? P.cap - o : (int64_t)c);
-        int64_t* const dst = P.out + o;
-        for (uint32_t i = lane; i < lim; i += 32) dst[i] = segpos + sb[i ^ ((i >> 5) & 31u)];
+        int64_t* d = P.out + o + lane;
+        const int64_t sp = cur.sp;
+        uint32_t i = lane;
+#pragma unroll 4
+        for (uint32_t blk = 0; i < lim; blk++, i += 32, d += 32) *d = sp + sb[i ^ (blk & 31u)];
         __syncwarp();  // the next segment overwrites sb
       }
     }
-    if (g_nxt < 0) break;
+    if (!have_nxt) break;
     qi += stride;
     cur = nxt;
-    g_nxt = g_nn;
+    have_nxt = have_nn;
+    h_ent = n_ent, h_o = n_o, h_sp = n_sp;
   }
   MB_TRACE_SYNC_MARK(13);
 }

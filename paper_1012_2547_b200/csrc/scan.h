@@ -90,8 +90,9 @@ struct ScanParams {
   uint16_t* counts;     // per segment (tile * NWARP + warp); <= SEG
   uint16_t* lists;      // per segment LIST_CAP tile-relative offsets
   uint32_t* bitmaps;    // per segment SEG_WORDS words (dense segments only)
-  int64_t* toff;        // per segment exclusive output offset (queued segments only)
-  int64_t* seglist;     // segments queued for expand_kernel (count in ticket[dense_slot])
+  int64_t* seglist;     // expand queue (length in ticket[dense_slot]): segment | count << 48
+  int64_t* toff;        // per queue entry: exclusive output offset
+  int64_t* qpos;        // per queue entry: position of the segment's bit 0
   uint64_t* state;      // look-back flags of offsets_kernel (per chunk)
   uint32_t epoch;
   int64_t* out;         // positions (may be null: count only)
