@@ -122,6 +122,8 @@ struct BatchPass {
   std::vector<Chunk> chunks;  // one per MP_CHUNK patterns
   int pre = 0, post = 0;                        // staged margins the verification needs
   std::vector<uint32_t> need;                   // per pattern: 0 = in the pass, 1 = per-pattern scan
+  std::vector<int32_t> rep;                     // per pattern: first identical pattern of the batch (itself if none)
+  int ndup = 0;                                 // patterns with rep[k] != k (searched once, through their rep)
   int64_t words() const { return (int64_t)img.size(); }
 };
 
@@ -142,6 +144,8 @@ struct mb_ctx {
   int64_t seglist_cap = 0;
   int64_t* qpos = nullptr;
   int64_t qpos_cap = 0;
+  int32_t* rep = nullptr;  // batch pattern representatives (duplicates)
+  int64_t rep_cap = 0;
   int32_t* plist = nullptr;
   int64_t plist_cap = 0;
   std::vector<int32_t> h_plist;
@@ -305,6 +309,7 @@ void mb_ctx_destroy(mb_ctx* c) {
   cudaFree(c->toff);
   cudaFree(c->seglist);
   cudaFree(c->qpos);
+  cudaFree(c->rep);
   cudaFree(c->plist);
   cudaFree(c->mp_tab);
   cudaFree(c->need);
@@ -608,7 +613,20 @@ static void pass_chunk(int kc, int ent_words, const Ent& ent_of, std::vector<uin
 
 static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, BatchPass* bp) {
   *bp = BatchPass();
-  if (K < 8 || K > MP_CHUNK * MAX_MP_CHUNKS) return;
+  // identical patterns are searched once: rep[k] = first k' with the same bytes
+  bp->rep.resize(K);
+  {
+    std::unordered_map<std::string, int> first;
+    first.reserve((size_t)K * 2);
+    for (int k = 0; k < K; k++) {
+      const auto& pb = plans[k]->h.pat;
+      auto ins = first.emplace(std::string(reinterpret_cast<const char*>(pb.data()), pb.size()), k);
+      bp->rep[k] = ins.first->second;
+      bp->ndup += ins.first->second != k;
+    }
+  }
+  const std::vector<int32_t>& rep = bp->rep;
+  if (K - bp->ndup < 8 || K > MP_CHUNK * MAX_MP_CHUNKS) return;
   double hist[256] = {0}, tot = 0;
   int64_t minm = INT64_MAX;
   for (int k = 0; k < K; k++) {
@@ -629,6 +647,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     double rate = 0;
     bool all_sampled = true;
     for (int k = 0; k < K; k++) {
+      if (rep[k] != k) continue;
       all_sampled &= h_pats[k].family == MB_FAM_SAMPLED;
       for (int j = 0; j < 4; j++) {
         uint8_t g[4];
@@ -636,7 +655,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
         rate += gp(g, 4);
       }
     }
-    if (rate <= 0.05 && (!all_sampled || K >= 64)) {
+    if (rate <= 0.05 && (!all_sampled || K - bp->ndup >= 64)) {
       bp->kind = 1;
       bp->need.assign(K, 0u);
       int64_t pre = 0, post = 0;
@@ -651,6 +670,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
         int B = 0, ne = 0;
         pass_chunk(std::min(MP_CHUNK, K - k0), 2,
                    [&](int i, int j, uint32_t* h, uint32_t* w) {
+                     if (rep[k0 + i] != k0 + i) return false;  // searched through its representative
                      w[0] = h_pats[k0 + i].mpG[j];
                      w[1] = ((uint32_t)i << 16) | (uint32_t)(h_pats[k0 + i].mpa + j);
                      *h = w[0] * 0x9E3779B1u;  // the aligned pass hashes the word alone
@@ -671,6 +691,10 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
   for (int k = 0; k < K; k++) {
     const auto& pb = plans[k]->h.pat;
     const int64_t m = (int64_t)pb.size();
+    if (rep[k] != k) {  // searched through its representative: no entry, no scan
+      need[k] = 0u;
+      continue;
+    }
     if (m < 2 || h_pats[k].family == MB_FAM_SAMPLED) continue;  // K3 reads ~1/S of the text on its own
     const double per_seg = 2048.0 * gp(pb.data(), (int)std::min<int64_t>(m, 32));
     if (per_seg > (plans[k]->h.period < m ? 2.0 : 8.0)) continue;
@@ -678,13 +702,13 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     n_in++;
     qm = std::min(qm, m);
   }
-  if (n_in < 8 || 2 * n_in < K) return;
+  if (n_in < 8 || 2 * n_in < K - bp->ndup) return;
   const int q = qm >= 8 ? 8 : qm >= 4 ? 4 : (int)qm;
   std::vector<int32_t> anchor(K, 0);
   std::unordered_map<uint64_t, int> used;  // gram value -> patterns already anchored on it
   double pooled = 0;
   for (int k = 0; k < K; k++) {
-    if (need[k]) continue;
+    if (need[k] || rep[k] != k) continue;
     const auto& pb = plans[k]->h.pat;
     const int64_t m = (int64_t)pb.size();
     // rarest window, spread over distinct gram values (a value shared by many
@@ -710,7 +734,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
   bp->need = need;
   int64_t pre = 0, post = 0;
   for (int k = 0; k < K; k++) {
-    if (need[k]) continue;
+    if (need[k] || rep[k] != k) continue;
     pre = std::max<int64_t>(pre, anchor[k]);
     post = std::max<int64_t>(post, h_pats[k].m - anchor[k] + 8);
   }
@@ -721,7 +745,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     int B = 0, ne = 0;
     pass_chunk(std::min(MP_CHUNK, K - k0), 4,
                [&](int i, int j, uint32_t* h, uint32_t* w) {
-                 if (j || need[k0 + i]) return false;  // one gram per pattern in the pass
+                 if (j || need[k0 + i] || rep[k0 + i] != k0 + i) return false;  // one gram per pattern in the pass
                  const auto& pb = plans[k0 + i]->h.pat;
                  uint8_t g[8] = {0};
                  memcpy(g, pb.data() + anchor[k0 + i], q);
@@ -740,10 +764,16 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
 // selective batch of anchor-filter patterns, one MP pass over the text), then
 // one offsets and one expand launch over all K patterns' segments, so the
 // output is CSR in the caller's pattern order whatever the family mix.
+// h_rep / h_need (batches, host, this batch's indices; null = identity / scan
+// all): representative of each pattern (identical patterns are searched once:
+// offsets/expand read the representative's segments for the duplicate's CSR
+// range) and per-pattern scan flags (0: covered by the batch pass or by its
+// representative -- the count kernels skip its tiles).
 static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
                       int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st,
                       const int64_t* out_base = nullptr, const BatchPass* bp = nullptr,
-                      const uint32_t* d_tab = nullptr, int chunk0 = 0) {
+                      const uint32_t* d_tab = nullptr, int chunk0 = 0, const int32_t* h_rep = nullptr,
+                      const uint32_t* h_need = nullptr) {
   ScanParams P;
   memset(&P, 0, sizeof(P));
   const uintptr_t addr = (uintptr_t)d_text;
@@ -797,6 +827,11 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.toff = c->toff;
   P.seglist = c->seglist;
   P.qpos = c->qpos;
+  if (h_rep) {
+    if ((rc = grow(&c->rep, &c->rep_cap, K, "pattern representatives"))) return rc;
+    if ((rc = stage_upload(c, c->rep, h_rep, sizeof(int32_t) * K, st))) return rc;
+    P.rep = c->rep;
+  }
   P.state = c->state;
   P.ticket = c->ticket;
   P.out = d_out;
@@ -856,10 +891,9 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // per-pattern scan flags: patterns left out of the pass start at 1 (and so
     // does the any-flag that gates the per-pattern scan launches)
     if ((rc = grow(&c->need, &c->need_cap, K, "pass flags"))) return rc;
-    const int kbase = chunk0 * MP_CHUNK;
-    if ((rc = stage_upload(c, c->need, bp->need.data() + kbase, sizeof(uint32_t) * K, st))) return rc;
+    if ((rc = stage_upload(c, c->need, h_need, sizeof(uint32_t) * K, st))) return rc;
     bool any_out = false;
-    for (int k = 0; k < K; k++) any_out |= bp->need[kbase + k] != 0;
+    for (int k = 0; k < K; k++) any_out |= h_need[k] != 0;
     if (any_out) CUDA_TRY(cudaMemsetAsync(M.overflow, 1, 1, st));
     M.need = c->need;
     CUDA_TRY(cudaMemsetAsync(c->ticket, 0, NTICKETS * sizeof(unsigned long long), st));
@@ -927,6 +961,10 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     P.need = c->need;
     mp_used = true;
     c->mp_batches++;
+  } else if (h_need) {  // no pass: duplicates' tiles are skipped
+    if ((rc = grow(&c->need, &c->need_cap, K, "scan flags"))) return rc;
+    if ((rc = stage_upload(c, c->need, h_need, sizeof(uint32_t) * K, st))) return rc;
+    P.need = c->need;
   }
   // tickets are zero here: ctx creation, or the previous search's last kernel reset them
   if (K == 1 && !mp_used) {
@@ -1011,12 +1049,28 @@ static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int 
   }
   int kc = (int)std::max<double>(1.0, std::min<double>((double)K, budget / per_pattern));
   if (kc < K && kc >= MP_CHUNK) kc -= kc % MP_CHUNK;  // keep the pass tables' chunks aligned to sub-batches
+  std::vector<int32_t> lrep;
+  std::vector<uint32_t> lneed;
   for (int k0 = 0; k0 < K; k0 += kc) {
     const int kk = std::min(kc, K - k0);
     // the pass runs on sub-batches made of whole table chunks
     const bool whole = bp && bp->kind && (k0 % MP_CHUNK) == 0 && (kk % MP_CHUNK == 0 || k0 + kk == K);
+    // representatives inside this sub-batch; a duplicate whose representative
+    // is in another sub-batch is scanned here (it has no pass-table entry)
+    const bool dups = bp && bp->ndup > 0 && (int)bp->rep.size() == K;
+    if (dups || whole) {
+      lrep.resize(kk);
+      lneed.resize(kk);
+      for (int i = 0; i < kk; i++) {
+        const int r = dups ? bp->rep[k0 + i] : k0 + i;
+        lrep[i] = r >= k0 ? r - k0 : i;
+        const bool orphan = r != k0 + i && r < k0;
+        lneed[i] = whole ? (orphan ? 1u : bp->need[k0 + i]) : (lrep[i] == i ? 1u : 0u);
+      }
+    }
     int rc = run_search(c, d_pats + k0, h_pats + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st,
-                        k0 ? d_offsets + k0 : nullptr, whole ? bp : nullptr, whole ? d_tab : nullptr, k0 / MP_CHUNK);
+                        k0 ? d_offsets + k0 : nullptr, whole ? bp : nullptr, whole ? d_tab : nullptr, k0 / MP_CHUNK,
+                        dups ? lrep.data() : nullptr, (dups || whole) ? lneed.data() : nullptr);
     if (rc) return rc;
   }
   return MB_OK;

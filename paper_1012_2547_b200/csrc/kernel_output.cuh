@@ -54,6 +54,16 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   int64_t rem = base + (int64_t)tid * PER - kq * seg_per_pat;
   int cur_k = (int)kq;
   int64_t shift = kq < P.K ? P.pats[kq].delta + P.off : 0;
+  // representatives (duplicate patterns read their representative's
+  // segments): segment rank r of pattern k lives at rep[k] * seg_per_pat + r.
+  // A thread's PER <= 32 segments span at most patterns kq and kq + 1
+  // (seg_per_pat >= 16)
+  int64_t rb0 = kq * seg_per_pat, rb1 = (kq + 1) * seg_per_pat;  // data bases of kq, kq + 1
+  if (P.rep) {
+    if (kq < P.K) rb0 = (int64_t)P.rep[kq] * seg_per_pat;
+    if (kq + 1 < P.K) rb1 = (int64_t)P.rep[kq + 1] * seg_per_pat;
+  }
+  int64_t rbase = rb0;  // data base of cur_k
   pdl_wait();     // counts / lists / bitmaps of the count kernel(s)
   MB_TRACE_MARK(4);
   MB_TRACE_MARK(5);
@@ -61,10 +71,18 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   // PER uint16 counts kept packed two per register (2 CTAs per SM fit)
   uint32_t v2[PER / 2];
   uint32_t tsum32 = 0;
-  const uint4* cv = reinterpret_cast<const uint4*>(P.counts + base + (int64_t)tid * PER);
+  // data index of this thread's segment q (8-count groups never straddle a
+  // pattern: seg_per_pat is a multiple of 16)
+  auto dseg = [&](int q) -> int64_t {
+    const int64_t r = rem + q;
+    return r < seg_per_pat ? rb0 + r : rb1 + (r - seg_per_pat);
+  };
 #pragma unroll
   for (int q8 = 0; q8 < PER / 8; q8++) {
-    const uint4 x = cv[q8];  // counts are allocated to a whole number of chunks
+    // counts are allocated to a whole number of chunks; past the last pattern
+    // the slots are read unmapped and zeroed below
+    const int64_t t0 = base + (int64_t)tid * PER + 8 * q8;
+    const uint4 x = *reinterpret_cast<const uint4*>(P.counts + (t0 < nseg ? dseg(8 * q8) : t0));
     v2[4 * q8] = x.x, v2[4 * q8 + 1] = x.y, v2[4 * q8 + 2] = x.z, v2[4 * q8 + 3] = x.w;
   }
   if (base + (int64_t)NT * PER > nseg) {  // last chunk: zero the slots past the last segment
@@ -82,7 +100,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   for (int q = PER - 1; q >= 0; q--)
     if ((v2[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) fq = q;
   uint4 pre = make_uint4(0, 0, 0, 0);
-  if (fq >= 0 && P.out) pre = *reinterpret_cast<const uint4*>(P.lists + (base + (int64_t)tid * PER + fq) * LIST_CAP);
+  if (fq >= 0 && P.out) pre = *reinterpret_cast<const uint4*>(P.lists + dseg(fq) * LIST_CAP);
   int64_t inc = tsum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -198,10 +216,12 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
         if (kq != cur_k) {  // (kq, rem) = (pattern, rank) of segment t
           shift = P.pats[kq].delta + P.off;
           cur_k = (int)kq;
+          rbase = rb1;  // a thread's range reaches at most pattern kq + 1
         }
+        const int64_t ds = rbase + rem;  // data segment (the representative's when a duplicate)
         if (vq <= fuse_max) {
           const int64_t pos0 = (rem / NWARP) * TILE - shift;  // position of tile offset 0
-          const uint16_t* L = P.lists + t * LIST_CAP;
+          const uint16_t* L = P.lists + ds * LIST_CAP;
           if (!P.unsorted_lists) {
             for (uint32_t e = 0; e < vq; e++) {
               uint32_t x;
@@ -228,7 +248,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
         } else {
           // queue entry: segment | count << 48, output offset, position of bit 0
           const unsigned long long slot = atomicAdd(&P.ticket[P.dense_slot], 1ULL);
-          P.seglist[slot] = t | ((int64_t)vq << 48);
+          P.seglist[slot] = ds | ((int64_t)vq << 48);
           P.toff[slot] = run;
           P.qpos[slot] = rem * SEG - shift;
         }

@@ -93,6 +93,7 @@ struct ScanParams {
   int64_t* seglist;     // expand queue (length in ticket[dense_slot]): segment | count << 48
   int64_t* toff;        // per queue entry: exclusive output offset
   int64_t* qpos;        // per queue entry: position of the segment's bit 0
+  const int32_t* rep;   // batch pattern -> representative whose segments hold its matches (null: itself)
   uint64_t* state;      // look-back flags of offsets_kernel (per chunk)
   uint32_t epoch;
   int64_t* out;         // positions (may be null: count only)

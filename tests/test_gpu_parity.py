@@ -466,3 +466,22 @@ def test_batch_sub_batching_chains_csr(cuda, monkeypatch):
     assert mb.search_many(pats, t) == want
     monkeypatch.setenv("MB_SCRATCH_BUDGET", str(1))  # one pattern per sub-batch
     assert mb.search_many(pats, t) == want
+
+
+@pytest.mark.parametrize("sigma,m", [(2, 2), (2, 8), (4, 4), (64, 16), (4, 300)])
+def test_batch_duplicate_patterns(cuda, sigma, m, monkeypatch):
+    """Identical patterns of a batch are searched once and their CSR ranges
+    filled from the representative's segments: every copy must still get the
+    complete list, through the batch passes, the per-pattern scans and chained
+    sub-batches (where a copy's representative may sit in an earlier one)."""
+    rng = np.random.default_rng(7000 + sigma + m)
+    t = rand_bytes(rng, sigma, 300_000)
+    base = [t[i : i + m] for i in rng.integers(0, len(t) - m, 12)]
+    pats = [base[i] for i in rng.integers(0, len(base), 120)] + [b"\x00" * (m + 1), base[0]]
+    want = {p: oracle.search(p, t).tolist() for p in set(pats)}
+    res = mb.search_many(pats, t)
+    assert [len(r) for r in res] == [len(want[p]) for p in pats]
+    assert all(r == want[p] for r, p in zip(res, pats))
+    monkeypatch.setenv("MB_SCRATCH_BUDGET", str(3_000_000))  # sub-batches of a few patterns
+    res = mb.search_many(pats, t)
+    assert all(r == want[p] for r, p in zip(res, pats))
