@@ -574,6 +574,11 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
 // patterns: bloom (64 Kbit), bucket starts, entries.
 
 static inline uint32_t pass_hash(uint32_t lo, uint32_t hi) { return lo * 0x9E3779B1u ^ hi * 0x85EBCA77u; }
+// q = 16: hash of the 4 gram words, and the fingerprint of words 2-3 kept in the entry
+static inline uint32_t pass_hash16(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
+  return w0 * 0x9E3779B1u ^ w1 * 0x85EBCA77u ^ w2 * 0xC2B2AE3Du ^ w3 * 0x27D4EB2Fu;
+}
+static inline uint32_t pass_fp16(uint32_t w2, uint32_t w3) { return w2 ^ (w3 * 0x9E3779B1u); }
 
 template <class Ent>
 static void pass_chunk(int kc, int ent_words, const Ent& ent_of, std::vector<uint32_t>& img, int* Bout, int* nout) {
@@ -703,9 +708,23 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     qm = std::min(qm, m);
   }
   if (n_in < 8 || 2 * n_in < K - bp->ndup) return;
-  const int q = qm >= 8 ? 8 : qm >= 4 ? 4 : (int)qm;
+  int q = qm >= 8 ? 8 : qm >= 4 ? 4 : (int)qm;
+  if (q == 8 && qm >= 16) {
+    // 8-byte grams of small alphabets hit at most text positions (sigma = 2:
+    // 8 bits each, 500 patterns cover all 256 values): 16-byte grams when the
+    // 8-byte pool would hit more than 0.05 times per position
+    double pool8 = 0;
+    for (int k = 0; k < K; k++)
+      if (!need[k] && rep[k] == k) {
+        double best = 1;
+        const auto& pb = plans[k]->h.pat;
+        for (int64_t a = 0; a + 8 <= (int64_t)pb.size(); a++) best = std::min(best, gp(pb.data() + a, 8));
+        pool8 += best;
+      }
+    if (pool8 > 0.05) q = 16;
+  }
   std::vector<int32_t> anchor(K, 0);
-  std::unordered_map<uint64_t, int> used;  // gram value -> patterns already anchored on it
+  std::unordered_map<std::string, int> used;  // gram value -> patterns already anchored on it
   double pooled = 0;
   for (int k = 0; k < K; k++) {
     if (need[k] || rep[k] != k) continue;
@@ -715,10 +734,9 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     // patterns makes every text hit on it walk all of them)
     int best = 0;
     double bcost = 1e300, bpr = 0;
-    uint64_t bval = 0;
+    std::string bval;
     for (int64_t a = 0; a + q <= m; a++) {
-      uint64_t v = 0;
-      memcpy(&v, pb.data() + a, q);
+      const std::string v(reinterpret_cast<const char*>(pb.data() + a), q);
       const double r = gp(pb.data() + a, q);
       auto it = used.find(v);
       const double cost = r * (1 + (it == used.end() ? 0 : it->second));
@@ -739,7 +757,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     post = std::max<int64_t>(post, h_pats[k].m - anchor[k] + 8);
   }
   bp->pre = (int)((pre + 15) & ~15LL);
-  bp->post = (int)((std::max<int64_t>(post, 24) + 15) & ~15LL) + 16;
+  bp->post = (int)((std::max<int64_t>(post, q == 16 ? 36 : 24) + 15) & ~15LL) + 16;
   for (int k0 = 0; k0 < K; k0 += MP_CHUNK) {
     const int64_t off = (int64_t)bp->img.size();
     int B = 0, ne = 0;
@@ -747,12 +765,15 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
                [&](int i, int j, uint32_t* h, uint32_t* w) {
                  if (j || need[k0 + i] || rep[k0 + i] != k0 + i) return false;  // one gram per pattern in the pass
                  const auto& pb = plans[k0 + i]->h.pat;
-                 uint8_t g[8] = {0};
+                 uint8_t g[16] = {0};
                  memcpy(g, pb.data() + anchor[k0 + i], q);
-                 memcpy(&w[0], g, 4);
-                 memcpy(&w[1], g + 4, 4);
+                 uint32_t gw[4];
+                 memcpy(gw, g, 16);
+                 w[0] = gw[0];
+                 w[1] = gw[1];
                  w[2] = ((uint32_t)i << 16) | (uint32_t)anchor[k0 + i];
-                 *h = pass_hash(w[0], w[1]);
+                 w[3] = q == 16 ? pass_fp16(gw[2], gw[3]) : 0u;
+                 *h = q == 16 ? pass_hash16(gw[0], gw[1], gw[2], gw[3]) : pass_hash(w[0], w[1]);
                  return true;
                },
                bp->img, &B, &ne);
@@ -898,6 +919,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     M.need = c->need;
     CUDA_TRY(cudaMemsetAsync(c->ticket, 0, NTICKETS * sizeof(unsigned long long), st));
     const void* fn = bp->kind == 1 ? (const void*)mp_scan_kernel
+                     : bp->q == 16 ? (const void*)mpb_scan_kernel<16>
                      : bp->q == 8  ? (const void*)mpb_scan_kernel<8>
                      : bp->q == 4  ? (const void*)mpb_scan_kernel<4>
                      : bp->q == 3  ? (const void*)mpb_scan_kernel<3>
@@ -943,6 +965,8 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       const int grid = (int)std::min<int64_t>(M.ntiles_text, (int64_t)c->nsm * per_sm);
       if (bp->kind == 1)
         mp_scan_kernel<<<grid, NT + 32, smem, st>>>(M);
+      else if (bp->q == 16)
+        mpb_scan_kernel<16><<<grid, NT + 32, smem, st>>>(M);
       else if (bp->q == 8)
         mpb_scan_kernel<8><<<grid, NT + 32, smem, st>>>(M);
       else if (bp->q == 4)

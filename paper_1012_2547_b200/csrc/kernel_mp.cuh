@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
 // offset a_k; q in {2, 3, 4, 8} for the whole batch) and every text position's
 // q-byte window is hashed once: bloom bit in smem, then a bucket of
 // {gram, pattern, a_k} entries, the full pattern verified in the staged tile,
-// the occurrence recorded as in the aligned pass.  Q = q.
+// the occurrence recorded as in the aligned pass.  Q = q.  Q = 16 (small
+// alphabets: sigma = 2 has 8 bits per 8-byte gram): the entry keeps gram words
+// 0-1 and a fingerprint of words 2-3, the hash covers all four.
 template <int Q>
 __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -188,29 +190,40 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
 #pragma unroll 1
     for (int r = 0; r < SEG / 512; r++) {
       const int c = c0 + r * 512 + lane * 16;
-      MB_CHECK(S + c + 24 <= stages + (s + 1) * P.stage_bytes);
+      MB_CHECK(S + c + 36 <= stages + (s + 1) * P.stage_bytes);
       const uint4 X = *reinterpret_cast<const uint4*>(S + c);
-      const uint2 Y = *reinterpret_cast<const uint2*>(S + c + 16);
-      const uint32_t w[6] = {X.x, X.y, X.z, X.w, Y.x, Y.y};
+      const uint4 Y = *reinterpret_cast<const uint4*>(S + c + 16);  // words 4-5 (Q = 16: 4-7, 8)
+      const uint32_t Z = Q == 16 ? *reinterpret_cast<const uint32_t*>(S + c + 32) : 0u;
+      const uint32_t w[9] = {X.x, X.y, X.z, X.w, Y.x, Y.y, Y.z, Y.w, Z};
       uint32_t hits = 0;
+      auto gram = [&](int p, uint32_t* lo, uint32_t* hi, uint32_t* fp) -> uint32_t {  // hash of window p
+        const int i = p >> 2, sh = 8 * (p & 3);
+        *lo = __funnelshift_r(w[i], w[i + 1], sh) & QMASK;
+        *hi = Q >= 8 ? __funnelshift_r(w[i + 1], w[i + 2], sh) : 0u;
+        if (Q == 16) {
+          const uint32_t w2 = __funnelshift_r(w[i + 2], w[i + 3], sh), w3 = __funnelshift_r(w[i + 3], w[i + 4], sh);
+          *fp = w2 ^ (w3 * 0x9E3779B1u);
+          return *lo * 0x9E3779B1u ^ *hi * 0x85EBCA77u ^ w2 * 0xC2B2AE3Du ^ w3 * 0x27D4EB2Fu;
+        }
+        *fp = 0u;
+        return *lo * 0x9E3779B1u ^ *hi * 0x85EBCA77u;
+      };
 #pragma unroll
       for (int p = 0; p < 16; p++) {
-        const uint32_t lo = __funnelshift_r(w[p >> 2], w[(p >> 2) + 1], 8 * (p & 3)) & QMASK;
-        const uint32_t hi = Q == 8 ? __funnelshift_r(w[(p >> 2) + 1], w[(p >> 2) + 2], 8 * (p & 3)) : 0u;
-        const uint32_t h = lo * 0x9E3779B1u ^ hi * 0x85EBCA77u;
+        uint32_t lo, hi, fp;
+        const uint32_t h = gram(p, &lo, &hi, &fp);
         hits |= ((bloom[h >> 21] >> ((h >> 16) & 31)) & 1u) << p;
       }
       while (hits) {  // bucket walk + verification
         const int p = __ffs(hits) - 1;
         hits &= hits - 1;
-        const uint32_t lo = __funnelshift_r(w[p >> 2], w[(p >> 2) + 1], 8 * (p & 3)) & QMASK;
-        const uint32_t hi = Q == 8 ? __funnelshift_r(w[(p >> 2) + 1], w[(p >> 2) + 2], 8 * (p & 3)) : 0u;
-        const uint32_t h = lo * 0x9E3779B1u ^ hi * 0x85EBCA77u;
+        uint32_t lo, hi, fp;
+        const uint32_t h = gram(p, &lo, &hi, &fp);
         const uint32_t bk = h >> (32 - P.B);
         const int64_t x = B0 + c + p;  // virtual position of the window
         for (uint32_t e = bstart[bk]; e < bstart[bk + 1]; e++) {
           const uint4 en = ents[e];
-          if (en.x != lo || en.y != hi) continue;
+          if (en.x != lo || en.y != hi || en.w != fp) continue;
           const int kl = (int)(en.z >> 16);
           const int a = (int)(en.z & 0xFFFFu);
           const int64_t sv = x - a;  // virtual start

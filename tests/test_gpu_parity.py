@@ -317,7 +317,8 @@ def test_mp_mixed_family_batch(cuda):
             assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(p, t)), (k, len(p))
 
 
-@pytest.mark.parametrize("sigma,lo,hi", [(16, 2, 3), (64, 4, 6), (256, 2, 9), (4, 8, 20), (8, 5, 40), (32, 3, 300)])
+@pytest.mark.parametrize("sigma,lo,hi", [(16, 2, 3), (64, 4, 6), (256, 2, 9), (4, 8, 20), (8, 5, 40), (32, 3, 300),
+                                         (2, 16, 64), (2, 20, 300)])
 def test_mpb_byte_offset_pass(cuda, sigma, lo, hi):
     """K5b byte-offset pass (short patterns / small alphabets): planted edges,
     duplicates, patterns longer than the text; ad-hoc and prepared batches."""

@@ -55,12 +55,14 @@ pats = [t[i : i + 24] for i in rng.integers(0, 4 * TILE - 24, 40)] + [rb(256, 9)
 res = search_many(pats, t)
 for p, r in zip(pats, res):
     assert r == oracle.search(p, t).tolist()
-# batched passes: K5 (aligned words), K5b (byte offsets, q = 2 / 4 / 8) with
-# dense patterns left to their scans, anchor words 2 / 3, sampled in a batch
-for sigma, lo, hi in ((256, 8, 40), (16, 2, 3), (64, 4, 6), (4, 8, 30), (32, 300, 1200)):
+# batched passes: K5 (aligned words), K5b (byte offsets, q = 2 / 4 / 8 / 16) with
+# dense patterns left to their scans, anchor words 2 / 3, sampled in a batch,
+# duplicate patterns
+for sigma, lo, hi in ((256, 8, 40), (16, 2, 3), (64, 4, 6), (4, 8, 30), (32, 300, 1200), (2, 16, 300)):
     t = rb(sigma, 3 * TILE + 321)
     ms = rng.integers(lo, hi + 1, 64)
     pats = [t[i : i + m] for i, m in zip(rng.integers(0, len(t) - hi, 64), ms)] + [b"ab" * 2, t[:lo]]
+    pats += pats[:5]
     for obj in (None, "prepared"):
         plans = [engine.Plan(p) for p in pats]
         pos, offs = engine.find_batch(engine.Batch(plans) if obj else plans, t)
