@@ -913,9 +913,6 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // does the any-flag that gates the per-pattern scan launches)
     if ((rc = grow(&c->need, &c->need_cap, K, "pass flags"))) return rc;
     if ((rc = stage_upload(c, c->need, h_need, sizeof(uint32_t) * K, st))) return rc;
-    bool any_out = false;
-    for (int k = 0; k < K; k++) any_out |= h_need[k] != 0;
-    if (any_out) CUDA_TRY(cudaMemsetAsync(M.overflow, 1, 1, st));
     M.need = c->need;
     CUDA_TRY(cudaMemsetAsync(c->ticket, 0, NTICKETS * sizeof(unsigned long long), st));
     const void* fn = bp->kind == 1 ? (const void*)mp_scan_kernel
@@ -985,10 +982,6 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     P.need = c->need;
     mp_used = true;
     c->mp_batches++;
-  } else if (h_need) {  // no pass: duplicates' tiles are skipped
-    if ((rc = grow(&c->need, &c->need_cap, K, "scan flags"))) return rc;
-    if ((rc = stage_upload(c, c->need, h_need, sizeof(uint32_t) * K, st))) return rc;
-    P.need = c->need;
   }
   // tickets are zero here: ctx creation, or the previous search's last kernel reset them
   if (K == 1 && !mp_used) {
@@ -999,33 +992,50 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     if ((rc = launch_family(c, P, h_pats, &idx0, nullptr, 1, 0, st, &fused))) return rc;
     return fused ? MB_OK : finish(false);
   }
-  // group patterns by family key (stable); a single group needs no index list
+  // count kernels, one launch per family key (stable groups): the patterns
+  // that need a scan (all; or those the batch pass left out, and the
+  // representatives of duplicates) unconditionally; with a batch pass, its
+  // own patterns once more behind the overflow flag -- those launches exit at
+  // once unless a pass segment overflowed, and then scan only the patterns
+  // whose flag the pass set
+  const uint32_t* run_if_pass = P.run_if;
   std::vector<int> keys;
   std::vector<std::vector<int32_t>> groups;
-  for (int k = 0; k < K; k++) {
-    const int key = family_key(h_pats[k]);
+  std::vector<char> gated;
+  auto add = [&](int k, bool gate) {
+    const int key = family_key(h_pats[k]) * 2 + (gate ? 1 : 0);
     size_t g = 0;
     while (g < keys.size() && keys[g] != key) g++;
     if (g == keys.size()) {
       keys.push_back(key);
       groups.emplace_back();
+      gated.push_back(gate ? 1 : 0);
     }
     groups[g].push_back(k);
-  }
+  };
+  int nlisted = 0;
+  for (int k = 0; k < K; k++)
+    if (!h_need || h_need[k]) add(k, false), nlisted++;
+  if (mp_used)
+    for (int k = 0; k < K; k++)
+      if (!h_need[k] && (!h_rep || h_rep[k] == k)) add(k, true), nlisted++;
   if ((int)groups.size() > MAX_GROUPS) return fail(MB_EINVAL, "too many kernel families in one batch");
-  if (groups.size() == 1) {
-    if ((rc = launch_family(c, P, h_pats, groups[0].data(), nullptr, K, 0, st))) return rc;
-  } else {
-    if ((rc = grow(&c->plist, &c->plist_cap, K, "family index lists"))) return rc;
+  const bool identity = groups.size() == 1 && nlisted == K;  // all patterns in order: no index list needed
+  if (!identity && nlisted) {
+    if ((rc = grow(&c->plist, &c->plist_cap, nlisted, "family index lists"))) return rc;
     c->h_plist.clear();
     for (auto& g : groups) c->h_plist.insert(c->h_plist.end(), g.begin(), g.end());
-    if ((rc = stage_upload(c, c->plist, c->h_plist.data(), sizeof(int32_t) * K, st))) return rc;
-    int base = 0;
-    for (size_t g = 0; g < groups.size(); g++) {
-      if ((rc = launch_family(c, P, h_pats, groups[g].data(), c->plist + base, (int)groups[g].size(), (int)g, st)))
-        return rc;
-      base += (int)groups[g].size();
-    }
+    if ((rc = stage_upload(c, c->plist, c->h_plist.data(), sizeof(int32_t) * nlisted, st))) return rc;
+  }
+  int base = 0;
+  for (size_t g = 0; g < groups.size(); g++) {
+    ScanParams Pg = P;
+    Pg.run_if = gated[g] ? run_if_pass : nullptr;
+    Pg.need = gated[g] ? P.need : nullptr;
+    if ((rc = launch_family(c, Pg, h_pats, groups[g].data(), identity ? nullptr : c->plist + base,
+                            (int)groups[g].size(), (int)g, st)))
+      return rc;
+    base += (int)groups[g].size();
   }
   return finish(mp_used);
 }

@@ -44,15 +44,16 @@ constexpr int SEG_WORDS = SEG / 32;
 constexpr int STAGES = MB_STAGES;  // TMA ring depth (max; scan_kernel may run with 2, see ScanParams.nstages)
 constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offsets
 // ticket counters (one uint64 each, zeroed between searches):
-constexpr int MAX_GROUPS = 12;      // family groups of one batch: slots 0..11 (10 family keys exist)
-constexpr int TICKET_OFFSETS = 12;  // offsets_kernel chunks (when the grid is not co-resident)
-constexpr int MAX_MP_CHUNKS = 7;    // batch-pass table chunks (MP_CHUNK patterns each): slots 13..19
-constexpr int TICKET_MP0 = 13;
-constexpr int TICKET_DENSE = 20;    // segments queued for expand_kernel (even epochs; odd: TICKET_DENSE_ODD)
-constexpr int TICKET_DONE = 21;     // offsets_kernel CTAs that finished (the last one zeroes the slots)
-constexpr int TICKET_DENSE_ODD = 22;
-constexpr int TICKET_OFFBAR = 23;   // offsets_kernel grid barrier (co-resident grid)
-constexpr int NTICKETS = 24;
+constexpr int MAX_GROUPS = 24;      // count-kernel launches of one batch: slots 0..23 (10 family keys,
+                                    // twice with a batch pass: scans + overflow fallback)
+constexpr int TICKET_OFFSETS = 24;  // offsets_kernel chunks (when the grid is not co-resident)
+constexpr int MAX_MP_CHUNKS = 7;    // batch-pass table chunks (MP_CHUNK patterns each): slots 25..31
+constexpr int TICKET_MP0 = 25;
+constexpr int TICKET_DENSE = 32;    // segments queued for expand_kernel (even epochs; odd: TICKET_DENSE_ODD)
+constexpr int TICKET_DONE = 33;     // offsets_kernel CTAs that finished (the last one zeroes the slots)
+constexpr int TICKET_DENSE_ODD = 34;
+constexpr int TICKET_OFFBAR = 35;   // offsets_kernel grid barrier (co-resident grid)
+constexpr int NTICKETS = 36;
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 
 struct StageHdr {
