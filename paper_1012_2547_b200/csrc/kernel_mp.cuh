@@ -34,6 +34,69 @@ __device__ __forceinline__ void mp_record(const MPParams& P, int k, int64_t b) {
   }
 }
 
+// Batched-pass verification of a gram hit: candidate start sv of batch-chunk
+// pattern kl against the staged tile.  The first min(m, 16) bytes are compared
+// word-wise by the lane; a short pattern is recorded right away, a longer
+// survivor is queued (up to 4 per lane and round, else verified word-wise by
+// the lane) for mp_verify_queued, where the whole warp compares it.
+struct MPCand {
+  int n;
+  int64_t sv[4];
+  int kl[4];
+};
+__device__ __forceinline__ bool mp_head_ok(const uint8_t* tp, const uint8_t* pp, int64_t m) {
+  const int hb = m < 16 ? (int)m : 16;
+  int k = 0;
+  for (; k + 4 <= hb; k += 4)
+    if (lds32u(tp + k) != __ldg(reinterpret_cast<const uint32_t*>(pp + k))) return false;
+  if (k < hb) {
+    const uint32_t mask = (1u << (8 * (hb - k))) - 1u;
+    if ((lds32u(tp + k) ^ __ldg(reinterpret_cast<const uint32_t*>(pp + k))) & mask) return false;
+  }
+  return true;
+}
+__device__ __forceinline__ bool mp_tail_ok(const uint8_t* tp, const uint8_t* pp, int64_t m, int k0, int step) {
+  bool bad = false;
+  for (int64_t k = k0; k < m; k += step) {
+    uint32_t diff = lds32u(tp + k) ^ __ldg(reinterpret_cast<const uint32_t*>(pp + k));
+    if (m - k < 4) diff &= (1u << (8 * (m - k))) - 1u;
+    bad |= diff != 0;
+  }
+  return !bad;
+}
+__device__ __forceinline__ void mp_candidate(const MPParams& P, MPCand& q, const uint8_t* tp, int64_t sv, int kl) {
+  const PatDev* pd = P.pats + P.kbase + kl;
+  const int64_t m = pd->m;
+  if (!mp_head_ok(tp, pd->bytes, m)) return;
+  if (m <= 16) {
+    mp_record(P, P.kbase + kl, sv + pd->delta);
+  } else if (q.n < 4) {
+    q.sv[q.n] = sv, q.kl[q.n] = kl, q.n++;
+  } else if (mp_tail_ok(tp, pd->bytes, m, 16, 4)) {
+    mp_record(P, P.kbase + kl, sv + pd->delta);
+  }
+}
+// the lanes' queued long candidates, one at a time by the whole warp (lane l
+// compares words 16 + 4 l, + 128, ...); call from all lanes
+__device__ __forceinline__ void mp_verify_queued(const MPParams& P, const MPCand& q, const uint8_t* S, int64_t B0,
+                                                 int lane) {
+  uint32_t pend = __ballot_sync(0xffffffffu, q.n > 0);
+  while (pend) {
+    const int src = __ffs(pend) - 1;
+    pend &= pend - 1;
+    const int ns = __shfl_sync(0xffffffffu, q.n, src);
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+      if (f >= ns) break;
+      const int64_t sv = __shfl_sync(0xffffffffu, (long long)q.sv[f], src);
+      const int kl = __shfl_sync(0xffffffffu, q.kl[f], src);
+      const PatDev* pd = P.pats + P.kbase + kl;
+      const bool ok = mp_tail_ok(S + (sv - B0), pd->bytes, pd->m, 16 + 4 * lane, 128);
+      if (__all_sync(0xffffffffu, ok) && lane == src) mp_record(P, P.kbase + kl, sv + pd->delta);
+    }
+  }
+}
+
 // TMA producer of the batched passes: text tiles (+ halo) into the ring.
 __device__ __forceinline__ void mp_produce(const MPParams& P, StageHdr* hdr, uint64_t* full, uint64_t* empty,
                                            uint8_t* stages) {
@@ -109,6 +172,8 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
         const uint32_t h = w[q] * 0x9E3779B1u;
         hits |= ((bloom[h >> 21] >> ((h >> 16) & 31)) & 1u) << q;
       }
+      MPCand cq;
+      cq.n = 0;
       while (hits) {  // rare: bucket walk + verification
         const int q = __ffs(hits) - 1;
         hits &= hits - 1;
@@ -123,18 +188,14 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
           const int aj = (int)(en.y & 0xFFFFu);
           const int64_t sv = x - aj;  // virtual start
           const int64_t spos = sv - P.off;
-          const PatDev* pd = P.pats + P.kbase + kl;
-          const int64_t m = pd->m;
+          const int64_t m = P.pats[P.kbase + kl].m;
           if (spos < 0 || spos + m > P.n) continue;
           const uint8_t* tp = S + (sv - B0);
-          MB_CHECK(tp >= stages + s * P.stage_bytes && tp + m <= stages + (s + 1) * P.stage_bytes);
-          const uint8_t* pp = pd->bytes;
-          bool ok = true;
-          for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);
-          if (!ok) continue;
-          mp_record(P, P.kbase + kl, sv + pd->delta);
+          MB_CHECK(tp >= stages + s * P.stage_bytes && tp + m + 4 <= stages + (s + 1) * P.stage_bytes);
+          mp_candidate(P, cq, tp, sv, kl);
         }
       }
+      mp_verify_queued(P, cq, S, B0, lane);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -196,6 +257,8 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
       const uint32_t Z = Q == 16 ? *reinterpret_cast<const uint32_t*>(S + c + 32) : 0u;
       const uint32_t w[9] = {X.x, X.y, X.z, X.w, Y.x, Y.y, Y.z, Y.w, Z};
       uint32_t hits = 0;
+      MPCand cq;
+      cq.n = 0;
       auto gram = [&](int p, uint32_t* lo, uint32_t* hi, uint32_t* fp) -> uint32_t {  // hash of window p
         const int i = p >> 2, sh = 8 * (p & 3);
         *lo = __funnelshift_r(w[i], w[i + 1], sh) & QMASK;
@@ -228,17 +291,14 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
           const int a = (int)(en.z & 0xFFFFu);
           const int64_t sv = x - a;  // virtual start
           const int64_t spos = sv - P.off;
-          const PatDev* pd = P.pats + P.kbase + kl;
-          const int64_t m = pd->m;
+          const int64_t m = P.pats[P.kbase + kl].m;
           if (spos < 0 || spos + m > P.n) continue;
           const uint8_t* tp = S + (sv - B0);
-          MB_CHECK(tp >= stages + s * P.stage_bytes && tp + m <= stages + (s + 1) * P.stage_bytes);
-          const uint8_t* pp = pd->bytes;
-          bool ok = true;
-          for (int64_t t = 0; t < m && ok; t++) ok = tp[t] == __ldg(pp + t);
-          if (ok) mp_record(P, P.kbase + kl, sv + pd->delta);
+          MB_CHECK(tp >= stages + s * P.stage_bytes && tp + m + 4 <= stages + (s + 1) * P.stage_bytes);
+          mp_candidate(P, cq, tp, sv, kl);
         }
       }
+      mp_verify_queued(P, cq, S, B0, lane);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
