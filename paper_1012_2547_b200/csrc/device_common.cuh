@@ -238,6 +238,9 @@ struct FiltALIGNED {
       for (int k = 0; k < 4; k++)
         hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
       if (!hit) return 0;
+      // c^m: the run test decides every start exactly (run1_lane_matches), so
+      // any hit just marks the lane's 16 positions
+      if (P.periodic && P.per == 1) return 0xFFFFu;
     }
     uint32_t mk = 0;
 #pragma unroll
@@ -375,6 +378,52 @@ __device__ __forceinline__ void or_bits(uint32_t* bm, int y, uint32_t bits) {
   }
 }
 
+// Run patterns c^m (period 1): the exact match bits of this lane's 64 starts
+// [64 l, 64 l + 64) of a segment, from its nz bitmap brk (bit y = start byte y
+// is not c, words 0 .. nwords-1 cover the segment and its m - 1 byte halo;
+// warp_run_nz without next-break arrays).  A start i survives iff no nz byte
+// lies in [i, i + m): inside the lane by a width-m sliding OR of its 64 bits
+// (m >= 64: nothing at or above i), past it by the first nz byte after the
+// lane -- a warp suffix-min of the lanes' first nz bytes, lane 31 taking the
+// first nz of the halo.  Replaces the next-break arrays and per-lane break
+// walk of the general periodic test.  Call from all lanes.
+__device__ __forceinline__ uint64_t run1_lane_matches(const uint32_t* brk, int nwords, int m, int lane) {
+  const uint64_t z = ((uint64_t)brk[2 * lane + 1] << 32) | brk[2 * lane];
+  int hfirst = 0x7fffffff;  // first nz of the halo words [SEG / 32, nwords)
+  for (int i = SEG / 32 + lane; i < nwords; i += 32)
+    if (brk[i]) {
+      hfirst = 32 * i + __ffs(brk[i]) - 1;
+      break;
+    }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) hfirst = min(hfirst, __shfl_xor_sync(0xffffffffu, hfirst, d));
+  const int first = z ? 64 * lane + __ffsll((long long)z) - 1 : 0x7fffffff;
+  int suf = first;  // inclusive suffix-min over lanes
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_down_sync(0xffffffffu, suf, d);
+    if (lane + d < 32) suf = min(suf, o);
+  }
+  int after = __shfl_down_sync(0xffffffffu, suf, 1);
+  if (lane == 31) after = 0x7fffffff;
+  after = min(after, hfirst);
+  // start i survives the bytes after the lane iff i <= after - 64 l - m
+  const int64_t T = (int64_t)after - 64 * lane - m;
+  const uint64_t w2 = T < 0 ? 0ull : T >= 63 ? ~0ull : ((2ull << T) - 1ull);
+  uint64_t w1;
+  if (m >= 64) {  // no nz byte at or above i inside the lane
+    const int hb = z ? 63 - __clzll((long long)z) : -1;
+    w1 = hb == 63 ? 0ull : ~0ull << (hb + 1);
+  } else {  // sliding OR of width m
+    uint64_t r = z;
+    int w = 1;
+    while (2 * w <= m) r |= r >> w, w *= 2;
+    if (w < m) r |= r >> (m - w);
+    w1 = ~r;
+  }
+  return w1 & w2;
+}
+
 // Run patterns c^m (period 1): nz bitmap of the bytes != c over Y positions
 // [0, 32 nwords) of a segment (Y0 + c0 = position 0).  The bulk [delta,
 // delta + SEG) is the segment's own staged bytes, read as the filter read
@@ -382,7 +431,7 @@ __device__ __forceinline__ void or_bits(uint32_t* bm, int y, uint32_t bits) {
 // clean chunk costs four compares; only the edge ranges go byte-exact through
 // a warp loop.  Then nbw = next nz at or after each word.
 __device__ __forceinline__ void warp_run_nz(const uint8_t* Yseg, const uint8_t* Sseg, int delta, uint32_t c4,
-                                            int nwords, uint32_t* brk, int32_t* nbw) {
+                                            int nwords, uint32_t* brk, int32_t* nbw, bool next = true) {
   const int lane = threadIdx.x & 31;
   for (int i = lane; i < nwords; i += 32) brk[i] = 0;
   __syncwarp();
@@ -407,7 +456,7 @@ __device__ __forceinline__ void warp_run_nz(const uint8_t* Yseg, const uint8_t* 
     or_bits(brk, y, nz);
   }
   __syncwarp();
-  warp_next_set(nwords, brk, nbw);
+  if (next) warp_next_set(nwords, brk, nbw);
 }
 
 

@@ -224,7 +224,17 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
       if (!always_exact<Filt>::value && !is_shiftor<Filt>::value && !pd.exact &&
           __any_sync(0xffffffffu, (w0 | w1) != 0)) {
         const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
-        if (pd.periodic) {
+        if (pd.periodic && pd.per == 1) {
+          // c^m: exact match bits from the staged bytes (device_common.cuh
+          // run1_lane_matches); the filter's candidates carry the text-edge
+          // validity, so the intersection is the answer
+          const int nwords = (SEG + (int)pd.m + 31) / 32;
+          MB_CHECK(Y0 + c0 >= sbeg && Y0 + c0 + 32 * nwords + 9 <= send);
+          warp_run_nz(Y0 + c0, S + c0, pd.delta, 0x01010101u * spat[0], nwords, brk, nbw, false);
+          const uint64_t mm = run1_lane_matches(brk, nwords, (int)pd.m, lane);
+          w0 &= (uint32_t)mm;
+          w1 &= (uint32_t)(mm >> 32);
+        } else if (pd.periodic) {
           // s matches <=> t[s..s+per) = p[0..per) and no break t[y] != t[y+per] for
           // y in [s, s+L).  A break y kills starts [y-L+1, y]: walk the few breaks
           // that reach this lane's 64 starts, mask them out in bulk.
