@@ -42,7 +42,7 @@ extern "C" {
 
 /* Kernel families. */
 #define MB_FAM_AUTO 0
-#define MB_FAM_SWAR 1    /* K1, m <= 3: SWAR xor/zero-byte packed compare, exact */
+#define MB_FAM_SWAR 1    /* K1, m <= 3 or 5..8: SWAR xor/zero-byte packed compare, exact */
 #define MB_FAM_WIN4 2    /* K1, 4 <= m <= 6: packed 32-bit window compare */
 #define MB_FAM_ALIGNED 3 /* K1/K3, m >= 7: aligned-word q-gram anchor + smem verify */
 #define MB_FAM_SHIFTOR 4 /* K2, m <= 64: per-thread bit-parallel shift-or */

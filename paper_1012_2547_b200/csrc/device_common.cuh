@@ -189,8 +189,8 @@ struct FiltSWAR {
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       uint32_t v = w[k] ^ P.G[0];
-      if (M >= 2) v |= shr8(w[k], w[k + 1], 1) ^ P.G[1];
-      if (M >= 3) v |= shr8(w[k], w[k + 1], 2) ^ P.G[2];
+#pragma unroll
+      for (int j = 1; j < M; j++) v |= shr8(w[k + (j >> 2)], w[k + (j >> 2) + 1], j & 3) ^ P.G[j];
       x[k] = v;
       acc |= (v - 0x01010101u) & ~v;
     }

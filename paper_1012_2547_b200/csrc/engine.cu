@@ -273,8 +273,8 @@ int mb_plan_gram_hash(const mb_plan* p, int q, uint32_t* o) {
 static void prefer_max_smem() {
   static std::once_flag once;
   std::call_once(once, [] {
-    const void* fns[] = {(const void*)offsets_kernel<8>, (const void*)offsets_kernel<16>,
-                         (const void*)offsets_kernel<32>, (const void*)expand_kernel, (const void*)fill_kernel};
+    const void* fns[] = {(const void*)offsets_kernel<8, NT>, (const void*)offsets_kernel<16, NT>,
+                         (const void*)offsets_kernel<64, NT / 2>, (const void*)expand_kernel, (const void*)fill_kernel};
     for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaGetLastError();
   });
@@ -538,9 +538,16 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
   const PatDev& d = h_pats[h_idx[0]];
   switch (d.family) {
     case MB_FAM_SWAR:
-      if (d.m == 1) return launch_group<FiltSWAR<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
-      if (d.m == 2) return launch_group<FiltSWAR<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
-      return launch_group<FiltSWAR<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      switch (d.m) {
+        case 1: return launch_group<FiltSWAR<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+        case 2: return launch_group<FiltSWAR<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+        case 3: return launch_group<FiltSWAR<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+        case 5: return launch_group<FiltSWAR<5>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+        case 6: return launch_group<FiltSWAR<6>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+        case 7: return launch_group<FiltSWAR<7>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+        case 8: return launch_group<FiltSWAR<8>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      }
+      return fail(MB_EINVAL, "SWAR family needs m in 1..3 or 5..8");
     case MB_FAM_WIN4: return launch_group<FiltWIN4>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     case MB_FAM_ALIGNED:
       if (d.nw == 3) return launch_group<FiltALIGNED<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
@@ -869,13 +876,15 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // previous grid drains and wait in-kernel (griddepcontrol.wait) for its
     // results -- the launch gap and the scan's tail overlap
     P.dense_slot = (P.epoch & 1) ? TICKET_DENSE_ODD : TICKET_DENSE;
-    P.offs_resident = nchunks <= (int64_t)c->nsm * 2 ? 1 : 0;  // __launch_bounds__(NT, 2)
+    // chunk = NT * scan_per counts; the largest chunks run as 256-thread CTAs
+    // x 64 counts (4 CTAs per SM, so 16 GiB's 512 chunks stay co-resident)
+    P.offs_resident = nchunks <= (int64_t)c->nsm * (scan_per == 32 ? 4 : 2) ? 1 : 0;  // __launch_bounds__
     if (scan_per == 32)
-      CUDA_TRY(launch_pdl(offsets_kernel<32>, (int)nchunks, NT, st, P));
+      CUDA_TRY(launch_pdl(offsets_kernel<64, NT / 2>, (int)nchunks, NT / 2, st, P));
     else if (scan_per == 16)
-      CUDA_TRY(launch_pdl(offsets_kernel<16>, (int)nchunks, NT, st, P));
+      CUDA_TRY(launch_pdl(offsets_kernel<16, NT>, (int)nchunks, NT, st, P));
     else
-      CUDA_TRY(launch_pdl(offsets_kernel<8>, (int)nchunks, NT, st, P));
+      CUDA_TRY(launch_pdl(offsets_kernel<8, NT>, (int)nchunks, NT, st, P));
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     if (d_out && cap > 0) {

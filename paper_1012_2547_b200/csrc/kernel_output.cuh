@@ -29,10 +29,14 @@ __device__ __forceinline__ void sort8(uint32_t* v) {
   cswap(v[1], v[2]); cswap(v[3], v[4]); cswap(v[5], v[6]);
 }
 
-template <int PER>  // counts per thread: chunk = NT * PER (host picks PER for >= 2 chunks per SM)
-__global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
-  __shared__ int64_t wsum[NWARP];
-  __shared__ uint32_t s_cnt[PER / 2 * NT];
+// PER counts per thread, OT threads per CTA: chunk = OT * PER (host picks the
+// largest chunk that still gives >= 2 chunks per SM; 16 GiB texts take
+// 256-thread CTAs x 64 counts so the 512 chunks stay co-resident at 4 CTAs/SM)
+template <int PER, int OT>
+__global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams P) {
+  constexpr int OW = OT / 32;  // warps of this CTA
+  __shared__ int64_t wsum[OW];
+  __shared__ uint32_t s_cnt[PER / 2 * OT];
   __shared__ int64_t s_excl;
   __shared__ int64_t s_chunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -46,7 +50,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   __syncthreads();
   const int64_t ch = s_chunk;
   const int64_t nseg = P.total_tiles * NWARP;
-  const int64_t base = ch * (int64_t)(NT * PER);
+  const int64_t base = ch * (int64_t)(OT * PER);
   const int64_t seg_per_pat = P.ntiles * NWARP;
   // pattern of this thread's first segment and the segment's rank within it
   // (one division per thread; the CSR end is written at rank seg_per_pat - 1)
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     const uint4 x = *reinterpret_cast<const uint4*>(P.counts + (t0 < nseg ? dseg(8 * q8) : t0));
     v2[4 * q8] = x.x, v2[4 * q8 + 1] = x.y, v2[4 * q8 + 2] = x.z, v2[4 * q8 + 3] = x.w;
   }
-  if (base + (int64_t)NT * PER > nseg) {  // last chunk: zero the slots past the last segment
+  if (base + (int64_t)OT * PER > nseg) {  // last chunk: zero the slots past the last segment
 #pragma unroll
     for (int q = 0; q < PER; q++)
       if (base + (int64_t)tid * PER + q >= nseg) v2[q >> 1] &= (q & 1) ? 0x0000FFFFu : 0xFFFF0000u;
@@ -101,6 +105,11 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     if ((v2[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) fq = q;
   uint4 pre = make_uint4(0, 0, 0, 0);
   if (fq >= 0 && P.out) pre = *reinterpret_cast<const uint4*>(P.lists + dseg(fq) * LIST_CAP);
+  // the counts go through shared memory (transposed: conflict-free) so the
+  // output loop below is not unrolled, and they stop occupying registers
+  // across the prefix computation (the 64-count variant would spill)
+#pragma unroll
+  for (int h = 0; h < PER / 2; h++) s_cnt[h * OT + tid] = v2[h];
   int64_t inc = tsum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -110,12 +119,12 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
   int64_t chunk_total = 0, wbefore = 0;
-  for (int q = 0; q < NWARP; q++) {
+  for (int q = 0; q < OW; q++) {
     chunk_total += wsum[q];
     wbefore += q < warp ? wsum[q] : 0;
   }
-  __shared__ int s_first[NWARP];
-  __shared__ unsigned long long s_part[NWARP];
+  __shared__ int s_first[OW];
+  __shared__ unsigned long long s_part[OW];
   if (tid == 0) {
     st_relaxed(&P.state[ch], pack_state(P.epoch, ch == 0 ? ST_INCL : ST_AGG, (uint64_t)chunk_total));
     s_excl = 0;
@@ -134,7 +143,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     }
     __syncthreads();
     unsigned long long v = 0;
-    for (int64_t i = tid; i < ch; i += NT) v += ld_relaxed(&P.state[i]) & ((1ULL << 38) - 1);
+    for (int64_t i = tid; i < ch; i += OT) v += ld_relaxed(&P.state[i]) & ((1ULL << 38) - 1);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
     if (lane == 0) s_part[warp] = v;
@@ -142,12 +151,12 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     if (tid == 0) {
       unsigned long long sum = 0;
 #pragma unroll
-      for (int w = 0; w < NWARP; w++) sum += s_part[w];
+      for (int w = 0; w < OW; w++) sum += s_part[w];
       s_excl = (int64_t)sum;
     }
     j = -1;
   }
-  // otherwise block-wide decoupled look-back: the whole CTA reads NT
+  // otherwise block-wide decoupled look-back: the whole CTA reads OT
   // predecessors per round trip; the nearest inclusive predecessor and the sum
   // up to it are found with warp ballots / shuffles and one word per warp in
   // smem (no smem atomics)
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     __syncthreads();
     int first = 0x7fffffff;  // nearest predecessor holding an inclusive prefix
 #pragma unroll
-    for (int w = 0; w < NWARP; w++) first = min(first, s_first[w]);
+    for (int w = 0; w < OW; w++) first = min(first, s_first[w]);
     unsigned long long v = (idx >= 0 && tid <= first) ? (sv & ((1ULL << 38) - 1)) : 0ULL;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
@@ -177,11 +186,11 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
     if (tid == 0) {
       unsigned long long sum = 0;
 #pragma unroll
-      for (int w = 0; w < NWARP; w++) sum += s_part[w];
+      for (int w = 0; w < OW; w++) sum += s_part[w];
       s_excl += (int64_t)sum;
     }
-    if (first != 0x7fffffff || j - NT < 0) break;
-    j -= NT;
+    if (first != 0x7fffffff || j - OT < 0) break;
+    j -= OT;
     __syncthreads();  // s_first / s_part are rewritten next round
   }
   __syncthreads();
@@ -201,16 +210,12 @@ __global__ void __launch_bounds__(NT, 2) offsets_kernel(const ScanParams P) {
   // network); longer ones go to expand_kernel, whose warp per segment writes
   // them coalesced (a thread looping over 32 scattered stores is slower)
   const uint32_t fuse_max = !P.out ? 0u : P.unsorted_lists ? (uint32_t)min(FUSE_MAX, 8) : (uint32_t)FUSE_MAX;
-  // the counts go through shared memory (transposed: conflict-free) so the
-  // output loop below is not unrolled and the kernel stays at 2 CTAs per SM
-#pragma unroll
-  for (int h = 0; h < PER / 2; h++) s_cnt[h * NT + tid] = v2[h];
   // nothing to emit and no pattern ends in this thread's range: done
   const bool idle = tsum == 0 && rem + PER < seg_per_pat;
 #pragma unroll 1
   for (int q = 0; q < (idle ? 0 : PER); q++) {
     const int64_t t = base + (int64_t)tid * PER + q;
-    const uint32_t vq = (s_cnt[(q >> 1) * NT + tid] >> (16 * (q & 1))) & 0xFFFFu;
+    const uint32_t vq = (s_cnt[(q >> 1) * OT + tid] >> (16 * (q & 1))) & 0xFFFFu;
     if (t < nseg) {
       if (vq && P.out) {
         if (kq != cur_k) {  // (kq, rem) = (pattern, rank) of segment t

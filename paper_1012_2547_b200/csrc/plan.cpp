@@ -68,6 +68,9 @@ constexpr double K2_MAX_ENTROPY = -1.0;
 
 // ALIGNED anchor-word thresholds (expected one-/two-word anchor hits per text
 // word above which one more word is added); tuned on config 2.
+#ifndef MB_SWAR_RATE
+#define MB_SWAR_RATE 2e-2  // anchor hits per text word above which 5 <= m <= 8 take exact SWAR
+#endif
 #ifndef MB_ALIGNED2_RATE
 #define MB_ALIGNED2_RATE 4e-3
 #endif
@@ -251,6 +254,20 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       ph->dev.B = tmp.dev.B;
     }
   }
+  // Small alphabets, 5 <= m <= 8: the anchor filters would flag a large share
+  // of the words (sigma = 2, m = 8: a quarter of them) and verify each
+  // candidate; exact SWAR compares of every byte of every alignment cost ~4
+  // operations per text byte instead (config 2 sigma = 2, m = 8).
+  if ((opts == nullptr || opts->family == MB_FAM_AUTO) && m >= 5 && m <= 8 &&
+      (fam == MB_FAM_WIN4 || fam == MB_FAM_ALIGNED)) {
+    double pr[256], r;
+    byte_probs(pat, m, hist, pr);
+    if (fam == MB_FAM_WIN4)
+      best_win4(pat, m, pr, &r);
+    else
+      best_aligned(pat, m, pr, 1, &r);
+    if (r > MB_SWAR_RATE) fam = MB_FAM_SWAR;
+  }
   if (auto_long && fam == MB_FAM_ALIGNED) {
     // ALIGNED tests 4 grams of one 7-byte window per word; WIN4 one gram at
     // every byte phase.  When the rare bytes of a pattern fit only one gram
@@ -273,7 +290,7 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
     *err = "sampled q-gram family does not apply to this pattern (m < 272, low entropy or periodic)";
     return MB_EINVAL;
   }
-  if ((fam == MB_FAM_SWAR && m > 3) || (fam == MB_FAM_WIN4 && m < 4) ||
+  if ((fam == MB_FAM_SWAR && (m == 4 || m > 8)) || (fam == MB_FAM_WIN4 && m < 4) ||
       (fam == MB_FAM_ALIGNED && m < 7) || (fam == MB_FAM_SHIFTOR && m > 64)) {
     *err = "requested kernel family does not apply at this pattern length";
     return MB_EINVAL;
@@ -296,7 +313,7 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
     case MB_FAM_SWAR:
       ph->anchor = 0;
       d.delta = 0;
-      for (int j = 0; j < 3; j++) d.G[j] = (j < m) ? 0x01010101u * pat[j] : 0u;
+      for (int j = 0; j < 8; j++) d.G[j] = (j < m) ? 0x01010101u * pat[j] : 0u;
       d.exact = 1;
       break;
     case MB_FAM_WIN4: {

@@ -115,7 +115,7 @@ def test_sigma1_and_zero_bytes(cuda):
         check(b"\x00" * m, b"\x00" * 3000 + b"\x01" + b"\x00" * 50)
 
 
-@pytest.mark.parametrize("family,lo,hi", [("win4", 4, 40), ("aligned", 7, 200), ("shiftor", 1, 64)])
+@pytest.mark.parametrize("family,lo,hi", [("win4", 4, 40), ("aligned", 7, 200), ("shiftor", 1, 64), ("swar", 5, 8)])
 def test_forced_families(cuda, family, lo, hi):
     for p, t in fuzz_cases(77, 150, lo, hi, n_max=3000):
         check(p, t, family)

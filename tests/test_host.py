@@ -133,6 +133,10 @@ def test_plan_info_families():
         assert engine.Plan(b"\x05" * (m - 1) + b"\x07").info().family == "win4", m
         assert engine.Plan(b"\x07" + b"\x05" * (m - 1)).info().family == "win4", m
     assert engine.Plan(b"a" * 100).info().periodic
+    # small alphabets, 5 <= m <= 8: exact SWAR instead of a busy anchor filter
+    for m in (5, 6, 7, 8):
+        assert engine.Plan(bytes(rng0.integers(0, 2, m, dtype=np.uint8))).info().family == "swar", m
+    assert engine.Plan(bytes(range(40, 48))).info().family == "aligned"
     assert not engine.Plan(b"a" * 99 + b"b").info().periodic
     with pytest.raises(ValueError):
         engine.Plan(b"x" * 8193)
