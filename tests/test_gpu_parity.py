@@ -425,6 +425,21 @@ def test_mp_overflow_falls_back(cuda):
         assert r == oracle.search(p, t).tolist()
 
 
+def test_mp_overflow_with_duplicates(cuda):
+    """Duplicates of patterns whose batch-pass segments overflow: the
+    representative falls back to its family scan and every copy still reads
+    the representative's (rescanned) segments."""
+    rng = np.random.default_rng(6)
+    unit = rand_bytes(rng, 256, 40)
+    t = rand_bytes(rng, 256, 50_000) + unit * 4000 + rand_bytes(rng, 256, 50_000)
+    dense = [unit[i:] + unit[:i] for i in range(8)]
+    sparse = [t[i : i + 24] for i in rng.integers(0, 50_000, 24)]
+    pats = dense + sparse + dense[::-1] + sparse[:5] + dense[:3]
+    res = mb.search_many(pats, t)
+    for p, r in zip(pats, res):
+        assert r == oracle.search(p, t).tolist()
+
+
 def test_compiled_searcher_shared_across_threads(cuda):
     """tests/test_registry.py:152-162 analog: one compiled run(hay) used from 4 threads."""
     from concurrent.futures import ThreadPoolExecutor
