@@ -5,10 +5,12 @@
 namespace mb {
 
 // ------------------------------------------------ kernel 2: segment offsets (scan)
-// Exclusive scan of per-segment counts in SCAN_CHUNK pieces; chunk order =
-// ticket order taken at CTA start (no prefetch), so each chunk only waits on
-// chunks already running -- the decoupled look-back never stalls on a queued
-// predecessor.
+// Exclusive scan of per-segment counts in OT * PER-count chunks, one per CTA.
+// Co-resident grids (every realistic single search, 16 GiB included): each
+// CTA publishes its chunk total, passes one grid barrier and sums its
+// predecessors' totals.  Otherwise chunk order = ticket order taken at CTA
+// start (no prefetch), so each chunk only waits on chunks already running --
+// the decoupled look-back never stalls on a queued predecessor.
 #ifndef MB_FUSE_MAX
 #define MB_FUSE_MAX 16
 #endif

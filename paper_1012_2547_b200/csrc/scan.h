@@ -1,6 +1,9 @@
 // scan.h -- launch parameters of the sm_100a search pipeline.
 //
-// A search (or a batch of K patterns over one text) is three kernels:
+// A search (or a batch of K patterns over one text) is three kernels -- or,
+// for one pattern over at most one resident wave of tiles (~9 MiB), one:
+// scan_kernel<Filter, FUSED> (a tile per CTA, match bits kept in registers,
+// warp look-back over the tiles, positions written directly).
 //
 //  1. count kernel -- scan_kernel<Filter> (persistent, dynamic tile tickets,
 //       no inter-CTA waits): TMA 1D bulk copy of tile + halo into a 2-3 stage
@@ -12,9 +15,11 @@
 //       tile-relative uint16 offsets, else the segment's 256-byte bitmap.
 //       Alternatives producing the same segment layout: sampled_kernel (K3,
 //       long patterns), mp_scan_kernel (K5, one pass for a whole batch).
-//  2. offsets_kernel -- exclusive scan of the segment counts (decoupled
-//       look-back over NT*PER-count chunks) -> CSR pattern ends; sparse
-//       sorted segments are expanded in place, the rest queued
+//  2. offsets_kernel -- exclusive scan of the segment counts (chunk totals +
+//       one grid barrier when co-resident, else decoupled look-back) -> CSR
+//       pattern ends; sparse sorted segments are expanded in place, the rest
+//       queued (duplicate patterns of a batch read their representative's
+//       segments)
 //  3. expand_kernel -- warp per queued segment: list / bitmap -> ascending
 //       int64 positions at out[offset ..]
 //
