@@ -89,7 +89,10 @@ int mb_plan_fwd_masks(const mb_plan* plan, uint64_t* h_out, int64_t words);
 int mb_plan_kmp(const mb_plan* plan, int64_t* h_out);
 int mb_plan_gram_hash(const mb_plan* plan, int q, uint32_t* h_out);
 
-/* ---- contexts: per-thread workspace (tile flags, tickets) bound to a device ---- */
+/* ---- contexts: per-thread workspace (tile flags, tickets) bound to a device.
+ * Searches on one context may be issued on different streams: a search on
+ * another stream than the previous one first waits for that one (the
+ * context's tickets and scratch are shared). ---- */
 int mb_ctx_create(int device, mb_ctx** out);
 void mb_ctx_destroy(mb_ctx* ctx);
 

@@ -130,6 +130,11 @@ struct BatchPass {
 struct mb_ctx {
   int device = 0;
   int nsm = 0;
+  // searches on one context share its tickets and scratch: a search on a
+  // different stream than the previous one waits for that one (done_ev)
+  cudaEvent_t done_ev = nullptr;
+  cudaStream_t last_st = nullptr;
+  bool have_last = false;
   uint64_t* state = nullptr;
   int64_t state_cap = 0;
   uint16_t* counts = nullptr;
@@ -319,6 +324,7 @@ void mb_ctx_destroy(mb_ctx* c) {
   cudaFree(c->d_out);
   cudaFree(c->d_offs);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->done_ev) cudaEventDestroy(c->done_ev);
   for (auto& s : c->stage) {
     if (s.ev) {
       cudaEventSynchronize(s.ev);
@@ -401,6 +407,20 @@ static int stage_end(mb_ctx* c, cudaStream_t st) {
   if (!s.ev) CUDA_TRY(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
   CUDA_TRY(cudaEventRecord(s.ev, st));
   s.pending = true;
+  return MB_OK;
+}
+
+// Stream ordering of the searches of one context (they share its tickets and
+// scratch): a search on another stream than the previous one waits for it.
+static int ctx_enter(mb_ctx* c, cudaStream_t st) {
+  if (c->have_last && c->last_st != st) CUDA_TRY(cudaStreamWaitEvent(st, c->done_ev, 0));
+  return MB_OK;
+}
+static int ctx_leave(mb_ctx* c, cudaStream_t st) {
+  if (!c->done_ev) CUDA_TRY(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(c->done_ev, st));
+  c->last_st = st;
+  c->have_last = true;
   return MB_OK;
 }
 
@@ -1064,11 +1084,13 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
   const PatDev* dd = nullptr;
   int rc = plan_device(p, &dd);
   if (rc) return rc;
+  if ((rc = ctx_enter(c, st))) return rc;
   if ((rc = stage_begin(c))) return rc;
   rc = run_search(c, dd, &p->dview, 1, d_text, n, d_out, cap, d_count, st);
   if (rc) tickets_recover(c, st);
   const int rc2 = stage_end(c, st);
-  return rc ? rc : rc2;
+  const int rc3 = ctx_leave(c, st);
+  return rc ? rc : rc2 ? rc2 : rc3;
 }
 
 // Run a batch whose params are on the device as sub-batches under the scratch
@@ -1134,6 +1156,7 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
   }
   int rc;
   if ((rc = grow(&c->d_pats, &c->pats_cap, K, "batch params"))) return rc;
+  if ((rc = ctx_enter(c, st))) return rc;
   if ((rc = stage_begin(c))) return rc;
   if ((rc = stage_upload(c, c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, st))) return rc;
   plan_pass(plans, c->h_pats.data(), K, &c->pass);
@@ -1144,7 +1167,8 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
   rc = run_batch(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets, st, &c->pass, c->mp_tab);
   if (rc) tickets_recover(c, st);
   const int rc2 = stage_end(c, st);
-  return rc ? rc : rc2;
+  const int rc3 = ctx_leave(c, st);
+  return rc ? rc : rc2 ? rc2 : rc3;
 }
 
 int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out) {
@@ -1198,13 +1222,15 @@ int mb_find_batch_prepared(mb_ctx* c, const mb_batch* b, const uint8_t* d_text, 
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   if (dev != b->device) return fail(MB_EINVAL, "batch was prepared on another device");
-  int rc = stage_begin(c);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ctx_enter(c, st);
   if (rc) return rc;
-  rc = run_batch(c, b->d_pats, b->h_pats.data(), b->K, d_text, n, d_out, cap, d_offsets, (cudaStream_t)stream,
-                 &b->pass, b->d_mp);
-  if (rc) tickets_recover(c, (cudaStream_t)stream);
-  const int rc2 = stage_end(c, (cudaStream_t)stream);
-  return rc ? rc : rc2;
+  if ((rc = stage_begin(c))) return rc;
+  rc = run_batch(c, b->d_pats, b->h_pats.data(), b->K, d_text, n, d_out, cap, d_offsets, st, &b->pass, b->d_mp);
+  if (rc) tickets_recover(c, st);
+  const int rc2 = stage_end(c, st);
+  const int rc3 = ctx_leave(c, st);
+  return rc ? rc : rc2 ? rc2 : rc3;
 }
 
 int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, void* stream) {

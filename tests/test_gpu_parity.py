@@ -470,6 +470,28 @@ def test_streams_and_device_tensor_inputs(cuda):
     assert run(d).cpu().tolist() == oracle.search(p, t).tolist()
 
 
+def test_one_context_two_streams_unsynchronised(cuda):
+    """Searches of one context (one thread) issued back to back on two streams
+    without synchronisation: the engine orders them (they share the context's
+    tickets and scratch), so both results are complete."""
+    rng = np.random.default_rng(8)
+    t = rand_bytes(rng, 4, 24 << 20)
+    d = torch.from_numpy(np.frombuffer(t, dtype=np.uint8).copy()).cuda()
+    pats = [t[1000:1006], t[5000:5009], b"\x00\x01\x02", t[7 << 20 : (7 << 20) + 40]]
+    plans = [engine.Plan(p) for p in pats]
+    wants = [oracle.search(p, t) for p in pats]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty(w.size + 1, dtype=torch.int64, device="cuda") for w in wants]
+    cnts = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in wants]
+    torch.cuda.synchronize()
+    for i, (pl, o, c) in enumerate(zip(plans, outs, cnts)):
+        engine.find_into(pl, d, o, c, streams[i % 2])
+    torch.cuda.synchronize()
+    for w, o, c in zip(wants, outs, cnts):
+        assert int(c.item()) == w.size
+        assert np.array_equal(o[: w.size].cpu().numpy(), w)
+
+
 def test_batch_sub_batching_chains_csr(cuda, monkeypatch):
     """A batch larger than the scratch budget runs as chained sub-batches (MP and
     per-pattern paths, patterns longer than the text included)."""
