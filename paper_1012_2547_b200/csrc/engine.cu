@@ -123,6 +123,8 @@ struct BatchPass {
   int pre = 0, post = 0;                        // staged margins the verification needs
   std::vector<uint32_t> need;                   // per pattern: 0 = in the pass, 1 = per-pattern scan
   std::vector<int32_t> rep;                     // per pattern: first identical pattern of the batch (itself if none)
+  std::vector<uint8_t> dcopy;                   // per duplicate: 1 = copy the representative's range afterwards
+                                                // (sparse-ish outputs), 0 = expand the representative's segments
   int ndup = 0;                                 // patterns with rep[k] != k (searched once, through their rep)
   int64_t words() const { return (int64_t)img.size(); }
 };
@@ -279,7 +281,8 @@ static void prefer_max_smem() {
   static std::once_flag once;
   std::call_once(once, [] {
     const void* fns[] = {(const void*)offsets_kernel<8, NT>, (const void*)offsets_kernel<16, NT>,
-                         (const void*)offsets_kernel<64, NT / 2>, (const void*)expand_kernel, (const void*)fill_kernel};
+                         (const void*)offsets_kernel<64, NT / 2>, (const void*)expand_kernel, (const void*)fill_kernel,
+                         (const void*)replicate_kernel};
     for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaGetLastError();
   });
@@ -658,7 +661,6 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     }
   }
   const std::vector<int32_t>& rep = bp->rep;
-  if (K - bp->ndup < 8 || K > MP_CHUNK * MAX_MP_CHUNKS) return;
   double hist[256] = {0}, tot = 0;
   int64_t minm = INT64_MAX;
   for (int k = 0; k < K; k++) {
@@ -674,6 +676,17 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     for (int i = 0; i < q; i++) r *= pr[g[i]];
     return r;
   };
+  // duplicates of patterns expected below 256 matches per 2 KiB segment are
+  // copied from the representative's output (expansion there costs more
+  // instructions per position than a copy); denser ones re-expand its
+  // segments (a copy would add the source reads to a write-bound stream)
+  bp->dcopy.assign(K, 0);
+  for (int k = 0; k < K; k++)
+    if (rep[k] != k) {
+      const auto& pb = plans[k]->h.pat;
+      bp->dcopy[k] = 2048.0 * gp(pb.data(), (int)std::min<size_t>(pb.size(), 32)) < 256.0 ? 1 : 0;
+    }
+  if (K - bp->ndup < 8 || K > MP_CHUNK * MAX_MP_CHUNKS) return;
   // kind 1
   if (minm >= 7) {
     double rate = 0;
@@ -875,7 +888,9 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.toff = c->toff;
   P.seglist = c->seglist;
   P.qpos = c->qpos;
+  int ndup = 0;  // duplicates in this (sub-)batch
   if (h_rep) {
+    for (int k = 0; k < K; k++) ndup += (h_rep[k] & REP_COPY) != 0;  // duplicates filled by replicate_kernel
     if ((rc = grow(&c->rep, &c->rep_cap, K, "pattern representatives"))) return rc;
     if ((rc = stage_upload(c, c->rep, h_rep, sizeof(int32_t) * K, st))) return rc;
     P.rep = c->rep;
@@ -916,6 +931,11 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       CUDA_TRY(launch_pdl(expand_kernel, (int)eg, EXP_WARPS * 32, st, P));
       g_launches++;
       CUDA_TRY(cudaGetLastError());
+      if (ndup) {  // duplicates marked REP_COPY: copy the representatives' ranges
+        CUDA_TRY(launch_pdl(replicate_kernel, (int)std::min<int64_t>(K, (int64_t)c->nsm * 4), 512, st, P));
+        g_launches++;
+        CUDA_TRY(cudaGetLastError());
+      }
     }
     return MB_OK;
   };
@@ -1047,7 +1067,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     if (!h_need || h_need[k]) add(k, false), nlisted++;
   if (mp_used)
     for (int k = 0; k < K; k++)
-      if (!h_need[k] && (!h_rep || h_rep[k] == k)) add(k, true), nlisted++;
+      if (!h_need[k] && (!h_rep || h_rep[k] == k)) add(k, true), nlisted++;  // (h_rep[k] == k: no flag)
   if ((int)groups.size() > MAX_GROUPS) return fail(MB_EINVAL, "too many kernel families in one batch");
   const bool identity = groups.size() == 1 && nlisted == K;  // all patterns in order: no index list needed
   if (!identity && nlisted) {
@@ -1129,6 +1149,7 @@ static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int 
       for (int i = 0; i < kk; i++) {
         const int r = dups ? bp->rep[k0 + i] : k0 + i;
         lrep[i] = r >= k0 ? r - k0 : i;
+        if (lrep[i] != i && bp->dcopy[k0 + i]) lrep[i] |= REP_COPY;  // copy the representative's range
         const bool orphan = r != k0 + i && r < k0;
         lneed[i] = whole ? (orphan ? 1u : bp->need[k0 + i]) : (lrep[i] == i ? 1u : 0u);
       }

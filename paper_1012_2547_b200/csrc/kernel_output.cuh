@@ -65,11 +65,13 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
   // A thread's PER <= 32 segments span at most patterns kq and kq + 1
   // (seg_per_pat >= 16)
   int64_t rb0 = kq * seg_per_pat, rb1 = (kq + 1) * seg_per_pat;  // data bases of kq, kq + 1
+  bool cp0 = false, cp1 = false;  // kq, kq + 1 filled by replicate_kernel
   if (P.rep) {
-    if (kq < P.K) rb0 = (int64_t)P.rep[kq] * seg_per_pat;
-    if (kq + 1 < P.K) rb1 = (int64_t)P.rep[kq + 1] * seg_per_pat;
+    if (kq < P.K) rb0 = (int64_t)(P.rep[kq] & ~REP_COPY) * seg_per_pat, cp0 = (P.rep[kq] & REP_COPY) != 0;
+    if (kq + 1 < P.K) rb1 = (int64_t)(P.rep[kq + 1] & ~REP_COPY) * seg_per_pat, cp1 = (P.rep[kq + 1] & REP_COPY) != 0;
   }
   int64_t rbase = rb0;  // data base of cur_k
+  bool rcopy = cp0;     // cur_k is filled by replicate_kernel
   pdl_wait();     // counts / lists / bitmaps of the count kernel(s)
   MB_TRACE_MARK(4);
   MB_TRACE_MARK(5);
@@ -224,40 +226,45 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
           shift = P.pats[kq].delta + P.off;
           cur_k = (int)kq;
           rbase = rb1;  // a thread's range reaches at most pattern kq + 1
+          rcopy = cp1;
         }
-        const int64_t ds = rbase + rem;  // data segment (the representative's when a duplicate)
-        if (vq <= fuse_max) {
-          const int64_t pos0 = (rem / NWARP) * TILE - shift;  // position of tile offset 0
-          const uint16_t* L = P.lists + ds * LIST_CAP;
-          if (!P.unsorted_lists) {
-            for (uint32_t e = 0; e < vq; e++) {
-              uint32_t x;
-              if (q == fq && e < 8) {  // prefetched
-                const uint32_t w = (e >> 1) == 0 ? pre.x : (e >> 1) == 1 ? pre.y : (e >> 1) == 2 ? pre.z : pre.w;
-                x = (w >> (16 * (e & 1))) & 0xFFFFu;
-              } else {
-                x = L[e];
+        // a REP_COPY duplicate's positions are copied from its representative's
+        // range afterwards (replicate_kernel): no list or queue work here
+        if (!rcopy) {
+          const int64_t ds = rbase + rem;  // data segment (the representative's for a duplicate)
+          if (vq <= fuse_max) {
+            const int64_t pos0 = (rem / NWARP) * TILE - shift;  // position of tile offset 0
+            const uint16_t* L = P.lists + ds * LIST_CAP;
+            if (!P.unsorted_lists) {
+              for (uint32_t e = 0; e < vq; e++) {
+                uint32_t x;
+                if (q == fq && e < 8) {  // prefetched
+                  const uint32_t w = (e >> 1) == 0 ? pre.x : (e >> 1) == 1 ? pre.y : (e >> 1) == 2 ? pre.z : pre.w;
+                  x = (w >> (16 * (e & 1))) & 0xFFFFu;
+                } else {
+                  x = L[e];
+                }
+                if (run + e < P.cap) P.out[run + e] = pos0 + x;
               }
-              if (run + e < P.cap) P.out[run + e] = pos0 + x;
+            } else {
+              const uint4 raw = q == fq ? pre : *reinterpret_cast<const uint4*>(L);  // 8 slots (64-byte aligned list)
+              uint32_t v[8] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16,
+                               raw.z & 0xFFFFu, raw.z >> 16, raw.w & 0xFFFFu, raw.w >> 16};
+  #pragma unroll
+              for (int e = 0; e < 8; e++)
+                if ((uint32_t)e >= vq) v[e] = 0xFFFFFFFFu;
+              sort8(v);
+  #pragma unroll
+              for (int e = 0; e < 8; e++)
+                if ((uint32_t)e < vq && run + e < P.cap) P.out[run + e] = pos0 + v[e];
             }
           } else {
-            const uint4 raw = q == fq ? pre : *reinterpret_cast<const uint4*>(L);  // 8 slots (64-byte aligned list)
-            uint32_t v[8] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16,
-                             raw.z & 0xFFFFu, raw.z >> 16, raw.w & 0xFFFFu, raw.w >> 16};
-#pragma unroll
-            for (int e = 0; e < 8; e++)
-              if ((uint32_t)e >= vq) v[e] = 0xFFFFFFFFu;
-            sort8(v);
-#pragma unroll
-            for (int e = 0; e < 8; e++)
-              if ((uint32_t)e < vq && run + e < P.cap) P.out[run + e] = pos0 + v[e];
+            // queue entry: segment | count << 48, output offset, position of bit 0
+            const unsigned long long slot = atomicAdd(&P.ticket[P.dense_slot], 1ULL);
+            P.seglist[slot] = ds | ((int64_t)vq << 48);
+            P.toff[slot] = run;
+            P.qpos[slot] = rem * SEG - shift;
           }
-        } else {
-          // queue entry: segment | count << 48, output offset, position of bit 0
-          const unsigned long long slot = atomicAdd(&P.ticket[P.dense_slot], 1ULL);
-          P.seglist[slot] = ds | ((int64_t)vq << 48);
-          P.toff[slot] = run;
-          P.qpos[slot] = rem * SEG - shift;
         }
       }
       if (rem == seg_per_pat - 1) P.offsets_plus1[kq] = run + vq;
@@ -413,5 +420,31 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
   MB_TRACE_SYNC_MARK(13);
 }
 
+
+// ------------------------------------------------ kernel 4: duplicate patterns
+// A batch pattern identical to an earlier one (its representative) gets the
+// representative's positions copied into its own CSR range, once expand_kernel
+// has written them: a write stream (the source is usually L2-resident) instead
+// of extracting the same segments again.  A CTA per duplicate, 8-byte copies
+// (source and destination parities may differ), capacity-bounded.
+__global__ void __launch_bounds__(512) replicate_kernel(const ScanParams P) {
+  pdl_wait();  // the representatives' positions (expand_kernel)
+  const int64_t base0 = P.out_base ? *P.out_base : 0;
+  for (int k = blockIdx.x; k < P.K; k += gridDim.x) {
+    if (!(P.rep[k] & REP_COPY)) continue;
+    const int r = P.rep[k] & ~REP_COPY;
+    const int64_t d0 = k ? P.offsets_plus1[k - 1] : base0, d1 = P.offsets_plus1[k];
+    const int64_t s0 = r ? P.offsets_plus1[r - 1] : base0;
+    const int64_t lim = min(d1, P.cap) - d0;
+    const int64_t* src = P.out + s0;
+    int64_t* dst = P.out + d0;
+    int64_t i = threadIdx.x;
+    for (; i + 3 * 512 < lim; i += 4 * 512) {
+      const int64_t a = src[i], b = src[i + 512], c = src[i + 1024], d = src[i + 1536];
+      dst[i] = a, dst[i + 512] = b, dst[i + 1024] = c, dst[i + 1536] = d;
+    }
+    for (; i < lim; i += 512) dst[i] = src[i];
+  }
+}
 
 }  // namespace mb

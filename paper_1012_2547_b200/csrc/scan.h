@@ -60,6 +60,7 @@ constexpr int TICKET_DENSE_ODD = 34;
 constexpr int TICKET_OFFBAR = 35;   // offsets_kernel grid barrier (co-resident grid)
 constexpr int NTICKETS = 36;
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
+constexpr int32_t REP_COPY = 1 << 30;  // ScanParams.rep flag (see there)
 
 struct StageHdr {
   int64_t tk;   // global tile ticket (-1: no more work)
@@ -99,7 +100,8 @@ struct ScanParams {
   int64_t* seglist;     // expand queue (length in ticket[dense_slot]): segment | count << 48
   int64_t* toff;        // per queue entry: exclusive output offset
   int64_t* qpos;        // per queue entry: position of the segment's bit 0
-  const int32_t* rep;   // batch pattern -> representative whose segments hold its matches (null: itself)
+  const int32_t* rep;   // batch pattern -> representative whose segments hold its matches (null: itself);
+                        // | REP_COPY: its output is copied from the representative's (replicate_kernel)
   uint64_t* state;      // look-back flags of offsets_kernel (per chunk)
   uint32_t epoch;
   int64_t* out;         // positions (may be null: count only)
