@@ -200,6 +200,8 @@ struct mb_batch {
   PatDev* d_pats = nullptr;
   BatchPass pass;
   uint32_t* d_mp = nullptr;  // pass tables on the device
+  int32_t* d_rep = nullptr;   // representatives (| REP_COPY) when the batch has duplicates
+  uint32_t* d_need = nullptr; // per-pattern scan flags (pass / duplicates)
 };
 
 extern "C" {
@@ -834,7 +836,8 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
                       int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st,
                       const int64_t* out_base = nullptr, const BatchPass* bp = nullptr,
                       const uint32_t* d_tab = nullptr, int chunk0 = 0, const int32_t* h_rep = nullptr,
-                      const uint32_t* h_need = nullptr) {
+                      const uint32_t* h_need = nullptr, int64_t* csr0 = nullptr,
+                      const int32_t* d_rep_pre = nullptr, const uint32_t* d_need_pre = nullptr) {
   ScanParams P;
   memset(&P, 0, sizeof(P));
   const uintptr_t addr = (uintptr_t)d_text;
@@ -845,6 +848,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   int64_t nbits = 0;
   for (int k = 0; k < K; k++)
     if (h_pats[k].m <= n) nbits = std::max<int64_t>(nbits, P.off + h_pats[k].delta + n - h_pats[k].m + 1);
+  if (nbits == 0 && csr0) CUDA_TRY(cudaMemsetAsync(csr0, 0, sizeof(int64_t), st));
   if (nbits == 0) {  // every pattern longer than the text: no output, offsets stay at the base
     if (out_base) {
       fill_kernel<<<(K + 255) / 256, 256, 0, st>>>(offsets_plus1, out_base, K);
@@ -891,9 +895,13 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   int ndup = 0;  // duplicates in this (sub-)batch
   if (h_rep) {
     for (int k = 0; k < K; k++) ndup += (h_rep[k] & REP_COPY) != 0;  // duplicates filled by replicate_kernel
-    if ((rc = grow(&c->rep, &c->rep_cap, K, "pattern representatives"))) return rc;
-    if ((rc = stage_upload(c, c->rep, h_rep, sizeof(int32_t) * K, st))) return rc;
-    P.rep = c->rep;
+    if (d_rep_pre) {  // prepared batch: resident on the device
+      P.rep = d_rep_pre;
+    } else {
+      if ((rc = grow(&c->rep, &c->rep_cap, K, "pattern representatives"))) return rc;
+      if ((rc = stage_upload(c, c->rep, h_rep, sizeof(int32_t) * K, st))) return rc;
+      P.rep = c->rep;
+    }
   }
   P.state = c->state;
   P.ticket = c->ticket;
@@ -901,6 +909,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   P.cap = d_out ? cap : 0;
   P.offsets_plus1 = offsets_plus1;
   P.out_base = out_base;
+  P.csr0 = csr0;
 
   // one epoch per search: look-back flags of older searches never match, and
   // its parity picks the expand-queue ticket slot (consecutive searches alternate)
@@ -957,13 +966,16 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     M.counts = c->counts;
     M.lists = c->lists;
     M.overflow = reinterpret_cast<unsigned int*>(c->counts + T);  // 4 spare bytes after the counts
-    CUDA_TRY(cudaMemsetAsync(c->counts, 0, sizeof(uint16_t) * (T + 2), st));
-    // per-pattern scan flags: patterns left out of the pass start at 1 (and so
-    // does the any-flag that gates the per-pattern scan launches)
+    // per-pattern scan flags (patterns left out of the pass start at 1): from
+    // the prepared batch's device copy inside the pass prologue, else uploaded;
+    // the prologue also zeroes the counts (the pass counts with atomics)
     if ((rc = grow(&c->need, &c->need_cap, K, "pass flags"))) return rc;
-    if ((rc = stage_upload(c, c->need, h_need, sizeof(uint32_t) * K, st))) return rc;
+    if (!d_need_pre && (rc = stage_upload(c, c->need, h_need, sizeof(uint32_t) * K, st))) return rc;
     M.need = c->need;
-    CUDA_TRY(cudaMemsetAsync(c->ticket, 0, NTICKETS * sizeof(unsigned long long), st));
+    M.need_src = d_need_pre;
+    M.need_k = K;
+    M.bar = c->ticket + TICKET_MPBAR;
+    // tickets are zero: the previous search's last kernel reset them
     const void* fn = bp->kind == 1 ? (const void*)mp_scan_kernel
                      : bp->q == 16 ? (const void*)mpb_scan_kernel<16>
                      : bp->q == 8  ? (const void*)mpb_scan_kernel<8>
@@ -991,6 +1003,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       M.nents = bp->chunks[ci].nent;
       M.kbase = k0;
       M.ticket = c->ticket + TICKET_MP0 + (ci - chunk0);
+      M.zero_n = k0 == 0 ? T + 2 : 0;  // the first launch's prologue (its grid is co-resident)
       auto smem_for = [&](int ns) {
         return (size_t)SM_STAGES + (size_t)ns * M.stage_bytes + 8192 + 4 * bs_words + (size_t)4 * ent_words * M.nents;
       };
@@ -1118,8 +1131,8 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
 // queue; a third of free memory, <= 16 GiB), chained through d_offsets.
 static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text, int64_t n,
                      int64_t* d_out, int64_t cap, int64_t* d_offsets, cudaStream_t st, const BatchPass* bp,
-                     const uint32_t* d_tab) {
-  CUDA_TRY(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
+                     const uint32_t* d_tab, const int32_t* d_rep_pre = nullptr,
+                     const uint32_t* d_need_pre = nullptr) {
   const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 346.0;
   // batches needing <= 1 GiB of scratch, or no more than a previous call
   // already got, skip the memory query (cudaMemGetInfo costs up to ms)
@@ -1154,9 +1167,12 @@ static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int 
         lneed[i] = whole ? (orphan ? 1u : bp->need[k0 + i]) : (lrep[i] == i ? 1u : 0u);
       }
     }
+    // the whole batch in one go: a prepared batch's device-resident flags
+    const bool all = k0 == 0 && kk == K;
     int rc = run_search(c, d_pats + k0, h_pats + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st,
                         k0 ? d_offsets + k0 : nullptr, whole ? bp : nullptr, whole ? d_tab : nullptr, k0 / MP_CHUNK,
-                        dups ? lrep.data() : nullptr, (dups || whole) ? lneed.data() : nullptr);
+                        dups ? lrep.data() : nullptr, (dups || whole) ? lneed.data() : nullptr,
+                        k0 == 0 ? d_offsets : nullptr, all ? d_rep_pre : nullptr, all ? d_need_pre : nullptr);
     if (rc) return rc;
   }
   return MB_OK;
@@ -1209,21 +1225,35 @@ int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out) {
   }
   cudaGetDevice(&b->device);
   plan_pass(plans, b->h_pats.data(), K, &b->pass);
-  const std::vector<uint32_t>& img = b->pass.img;
-  if (cudaMalloc(&b->d_pats, sizeof(PatDev) * K) != cudaSuccess ||
-      (!img.empty() && cudaMalloc(&b->d_mp, sizeof(uint32_t) * img.size()) != cudaSuccess)) {
-    cudaFree(b->d_pats);
-    delete b;
-    return fail(MB_ENOMEM, "batch upload alloc");
+  const BatchPass& bp = b->pass;
+  const std::vector<uint32_t>& img = bp.img;
+  // the whole batch's representative / scan-flag arrays (run_batch's sub-batch
+  // arrays for one sub-batch), resident so a call uploads nothing
+  const bool dups = bp.ndup > 0, whole = bp.kind != 0;
+  std::vector<int32_t> lrep(K);
+  std::vector<uint32_t> lneed(K);
+  for (int k = 0; k < K; k++) {
+    lrep[k] = bp.rep[k];
+    if (lrep[k] != k && bp.dcopy[k]) lrep[k] |= REP_COPY;
+    lneed[k] = whole ? bp.need[k] : (bp.rep[k] == k ? 1u : 0u);
   }
-  cudaError_t e = cudaMemcpy(b->d_pats, b->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMalloc(&b->d_pats, sizeof(PatDev) * K);
+  if (e == cudaSuccess && !img.empty()) e = cudaMalloc(&b->d_mp, sizeof(uint32_t) * img.size());
+  if (e == cudaSuccess && dups) e = cudaMalloc(&b->d_rep, sizeof(int32_t) * K);
+  if (e == cudaSuccess && (dups || whole)) e = cudaMalloc(&b->d_need, sizeof(uint32_t) * K);
+  if (e == cudaSuccess) e = cudaMemcpy(b->d_pats, b->h_pats.data(), sizeof(PatDev) * K, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !img.empty())
     e = cudaMemcpy(b->d_mp, img.data(), sizeof(uint32_t) * img.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && b->d_rep) e = cudaMemcpy(b->d_rep, lrep.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && b->d_need)
+    e = cudaMemcpy(b->d_need, lneed.data(), sizeof(uint32_t) * K, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(b->d_pats);
     cudaFree(b->d_mp);
+    cudaFree(b->d_rep);
+    cudaFree(b->d_need);
     delete b;
-    return cuda_fail(e, "batch upload");
+    return e == cudaErrorMemoryAllocation ? fail(MB_ENOMEM, "batch upload alloc") : cuda_fail(e, "batch upload");
   }
   *out = b;
   return MB_OK;
@@ -1233,6 +1263,8 @@ void mb_batch_destroy(mb_batch* b) {
   if (!b) return;
   cudaFree(b->d_pats);
   cudaFree(b->d_mp);
+  cudaFree(b->d_rep);
+  cudaFree(b->d_need);
   delete b;
 }
 
@@ -1247,7 +1279,8 @@ int mb_find_batch_prepared(mb_ctx* c, const mb_batch* b, const uint8_t* d_text, 
   int rc = ctx_enter(c, st);
   if (rc) return rc;
   if ((rc = stage_begin(c))) return rc;
-  rc = run_batch(c, b->d_pats, b->h_pats.data(), b->K, d_text, n, d_out, cap, d_offsets, st, &b->pass, b->d_mp);
+  rc = run_batch(c, b->d_pats, b->h_pats.data(), b->K, d_text, n, d_out, cap, d_offsets, st, &b->pass, b->d_mp,
+                 b->d_rep, b->d_need);
   if (rc) tickets_recover(c, st);
   const int rc2 = stage_end(c, st);
   const int rc3 = ctx_leave(c, st);

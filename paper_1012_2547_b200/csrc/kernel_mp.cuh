@@ -97,6 +97,28 @@ __device__ __forceinline__ void mp_verify_queued(const MPParams& P, const MPCand
   }
 }
 
+// Prologue of a search's first batch-pass launch (grid co-resident): zero the
+// segment counts (the pass counts with atomics), fill the per-pattern scan
+// flags from their immutable source, one grid barrier -- instead of two
+// separate memset / copy operations ahead of the launch.  All threads.
+__device__ __forceinline__ void mp_prologue(const MPParams& P) {
+  if (!P.zero_n) return;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n8 = P.zero_n / 8;  // uint4 = 8 counts (the counts array is 16-byte aligned)
+  for (int64_t i = gid; i < n8; i += nth) reinterpret_cast<uint4*>(P.counts)[i] = make_uint4(0, 0, 0, 0);
+  for (int64_t i = 8 * n8 + gid; i < P.zero_n; i += nth) P.counts[i] = 0;
+  if (P.need_src)
+    for (int64_t i = gid; i < P.need_k; i += nth) P.need[i] = P.need_src[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(P.bar, 1ULL);
+    while (ld_acquire(P.bar) < (unsigned long long)gridDim.x) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
 // TMA producer of the batched passes: text tiles (+ halo) into the ring.
 __device__ __forceinline__ void mp_produce(const MPParams& P, StageHdr* hdr, uint64_t* full, uint64_t* empty,
                                            uint8_t* stages) {
@@ -137,6 +159,7 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   for (int i = tid; i < 2048; i += NT + 32) bloom[i] = P.bloom[i];
   for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
   for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents[i];
+  mp_prologue(P);
   if (tid == 0) {
     for (int s = 0; s < P.nstages; s++) {
       mbar_init(&full[s], 1);
@@ -225,6 +248,7 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
   for (int i = tid; i < 2048; i += NT + 32) bloom[i] = P.bloom[i];
   for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
   for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents4[i];
+  mp_prologue(P);
   if (tid == 0) {
     for (int s = 0; s < P.nstages; s++) {
       mbar_init(&full[s], 1);

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
   }
   int64_t rbase = rb0;  // data base of cur_k
   bool rcopy = cp0;     // cur_k is filled by replicate_kernel
+  if (P.csr0 && blockIdx.x == 0 && tid == 0) *P.csr0 = 0;
   pdl_wait();     // counts / lists / bitmaps of the count kernel(s)
   MB_TRACE_MARK(4);
   MB_TRACE_MARK(5);

@@ -34,6 +34,7 @@ __device__ __forceinline__ void fused_emit(const ScanParams& P, int64_t tk, uint
       excl += P.out_base ? *P.out_base : 0;
       s_base = excl;
       if (tk == P.ntiles - 1) P.offsets_plus1[0] = excl + tot;
+      if (tk == 0 && P.csr0) *P.csr0 = 0;
     }
   }
   consumer_sync();

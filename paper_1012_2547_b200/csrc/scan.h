@@ -58,7 +58,8 @@ constexpr int TICKET_DENSE = 32;    // segments queued for expand_kernel (even e
 constexpr int TICKET_DONE = 33;     // offsets_kernel CTAs that finished (the last one zeroes the slots)
 constexpr int TICKET_DENSE_ODD = 34;
 constexpr int TICKET_OFFBAR = 35;   // offsets_kernel grid barrier (co-resident grid)
-constexpr int NTICKETS = 36;
+constexpr int TICKET_MPBAR = 36;    // batch pass: grid barrier after its prologue zeroes the counts
+constexpr int NTICKETS = 37;
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 constexpr int32_t REP_COPY = 1 << 30;  // ScanParams.rep flag (see there)
 
@@ -107,6 +108,7 @@ struct ScanParams {
   int64_t* out;         // positions (may be null: count only)
   int64_t cap;
   int64_t* offsets_plus1;   // entry k <- inclusive prefix after pattern k
+  int64_t* csr0;            // set to 0 by offsets_kernel when non-null (the CSR's leading entry)
   const int64_t* out_base;  // device: output index where this launch starts (null = 0)
   int unsorted_lists;       // lists were filled in arbitrary order (MP path): sort on expand
   const unsigned int* run_if;  // count kernels exit at once unless *run_if != 0 (batch-pass fallback)
@@ -138,6 +140,13 @@ struct MPParams {
   uint16_t* lists;
   unsigned int* overflow;  // any-flag: some pattern needs its per-pattern scan (run_if of the scans)
   unsigned int* need;      // per batch pattern: set when one of its segments exceeds LIST_CAP
+  // prologue of the first pass launch of a search (zero_n > 0): zero the
+  // counts (zero_n uint16, overflow word included), copy need_src -> need
+  // (K flags, when need_src is set), then one grid barrier on *bar
+  int64_t zero_n;
+  const unsigned int* need_src;
+  int need_k;
+  unsigned long long* bar;
 };
 
 }  // namespace mb
