@@ -100,23 +100,23 @@ __device__ __forceinline__ void mp_verify_queued(const MPParams& P, const MPCand
 // Prologue of a search's first batch-pass launch (grid co-resident): zero the
 // segment counts (the pass counts with atomics), fill the per-pattern scan
 // flags from their immutable source, one grid barrier -- instead of two
-// separate memset / copy operations ahead of the launch.  All threads.
+// separate memset / copy operations ahead of the launch.  The NT consumer
+// threads of every CTA (the producer warp is loading tiles meanwhile).
 __device__ __forceinline__ void mp_prologue(const MPParams& P) {
   if (!P.zero_n) return;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * NT;
+  const int64_t gid = (int64_t)blockIdx.x * NT + threadIdx.x;
   const int64_t n8 = P.zero_n / 8;  // uint4 = 8 counts (the counts array is 16-byte aligned)
   for (int64_t i = gid; i < n8; i += nth) reinterpret_cast<uint4*>(P.counts)[i] = make_uint4(0, 0, 0, 0);
   for (int64_t i = 8 * n8 + gid; i < P.zero_n; i += nth) P.counts[i] = 0;
   if (P.need_src)
     for (int64_t i = gid; i < P.need_k; i += nth) P.need[i] = P.need_src[i];
-  __syncthreads();
+  consumer_sync();
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(P.bar, 1ULL);
     while (ld_acquire(P.bar) < (unsigned long long)gridDim.x) __nanosleep(32);
   }
-  __syncthreads();
 }
 
 // TMA producer of the batched passes: text tiles (+ halo) into the ring.
@@ -156,10 +156,8 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
   uint32_t* bstart = bloom + 2048;
   uint2* ents = reinterpret_cast<uint2*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < 2048; i += NT + 32) bloom[i] = P.bloom[i];
-  for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
-  for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents[i];
-  mp_prologue(P);
+  // barriers first: the producer starts the tile loads while the consumers
+  // stage the tables (and run the search's prologue)
   if (tid == 0) {
     for (int s = 0; s < P.nstages; s++) {
       mbar_init(&full[s], 1);
@@ -168,6 +166,13 @@ __global__ void __launch_bounds__(NT + 32) mp_scan_kernel(const MPParams P) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (warp < NWARP) {
+    for (int i = tid; i < 2048; i += NT) bloom[i] = P.bloom[i];
+    for (int i = tid; i <= (1 << P.B); i += NT) bstart[i] = P.bstart[i];
+    for (int i = tid; i < P.nents; i += NT) ents[i] = P.ents[i];
+    mp_prologue(P);
+    consumer_sync();
+  }
 
   if (warp == NWARP) {  // ---------------- producer: text tiles only
     if (lane == 0) mp_produce(P, hdr, full, empty, stages);
@@ -245,10 +250,8 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
   uint32_t* bstart = bloom + 2048;
   uint4* ents = reinterpret_cast<uint4*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < 2048; i += NT + 32) bloom[i] = P.bloom[i];
-  for (int i = tid; i <= (1 << P.B); i += NT + 32) bstart[i] = P.bstart[i];
-  for (int i = tid; i < P.nents; i += NT + 32) ents[i] = P.ents4[i];
-  mp_prologue(P);
+  // barriers first: the producer starts the tile loads while the consumers
+  // stage the tables (and run the search's prologue)
   if (tid == 0) {
     for (int s = 0; s < P.nstages; s++) {
       mbar_init(&full[s], 1);
@@ -257,6 +260,13 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (warp < NWARP) {
+    for (int i = tid; i < 2048; i += NT) bloom[i] = P.bloom[i];
+    for (int i = tid; i <= (1 << P.B); i += NT) bstart[i] = P.bstart[i];
+    for (int i = tid; i < P.nents; i += NT) ents[i] = P.ents4[i];
+    mp_prologue(P);
+    consumer_sync();
+  }
   if (warp == NWARP) {
     if (lane == 0) mp_produce(P, hdr, full, empty, stages);
     return;
