@@ -11,13 +11,14 @@ namespace mb {
 // pattern offsets j where it occurs, each giving a candidate start s = x - j
 // that is verified against the text in global memory.  A warp owns SMP_SEGS
 // consecutive segments (8 tiles) and reads every sample whose bit range
-// [S*i, S*i + S) meets them, 4 independent 16-byte loads per lane in flight.
+// [S*i, S*i + S) meets them, 5 independent 16-byte loads per lane in flight
+// (a unit has ~130 samples at S = 1008: one batch of 160, not two of 128).
 // Output (segment counts, uint16 tile-relative lists) is the scan kernel's, so
 // offsets/expand are shared.
 constexpr int SMP_SEGS = 64;     // segments per warp unit (= 8 tiles)
 constexpr int SMP_LIST = 1024;   // per-warp match capacity per unit (bound: 131072/per + 2 < 1024)
 #ifndef MB_SMP_ILP
-#define MB_SMP_ILP 4
+#define MB_SMP_ILP 5
 #endif
 #ifndef MB_SMP_WARPS
 #define MB_SMP_WARPS 8
