@@ -12,11 +12,11 @@ namespace mb {
 // that is verified against the text in global memory.  A warp owns SMP_SEGS
 // consecutive segments (8 tiles) and reads every sample whose bit range
 // [S*i, S*i + S) meets them, 5 independent 16-byte loads per lane in flight
-// (a unit has ~130 samples at S = 1008: one batch of 160, not two of 128).
+// (a 128-segment unit has ~260 samples at S = 1008: two batches of 160).
 // Output (segment counts, uint16 tile-relative lists) is the scan kernel's, so
 // offsets/expand are shared.
-constexpr int SMP_SEGS = 64;     // segments per warp unit (= 8 tiles)
-constexpr int SMP_LIST = 1024;   // per-warp match capacity per unit (bound: 131072/per + 2 < 1024)
+constexpr int SMP_SEGS = K3_UNIT_SEGS;  // segments per warp unit (128 = 16 tiles, 256 KiB)
+constexpr int SMP_LIST = K3_LIST;       // per-warp match capacity (plan.h: the planner's period bound)
 #ifndef MB_SMP_ILP
 #define MB_SMP_ILP 5
 #endif
@@ -24,6 +24,7 @@ constexpr int SMP_LIST = 1024;   // per-warp match capacity per unit (bound: 131
 #define MB_SMP_WARPS 8
 #endif
 constexpr int SMP_ILP = MB_SMP_ILP;     // samples per lane per batch
+static_assert(4 * 32 <= K3_BATCH_HITS, "a round's gram hits must fit the planner's list headroom");
 constexpr int SMP_WARPS = MB_SMP_WARPS; // warps per sampled_kernel CTA (independent of the scan tiling)
 constexpr int SMP_NT = SMP_WARPS * 32;
 __device__ __forceinline__ int sampled_probe(const ScanParams& P, const PatDev& pd, const uint32_t* bloom,
@@ -126,10 +127,6 @@ __global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const Scan
     uint32_t* wl = lists + warp * SMP_LIST;
     uint32_t nmatch = 0, nver = 0;  // wl[0, nver) verified, wl[nver, nmatch) gram matches
     for (int64_t ib = i0; ib <= i1; ib += 32 * SMP_ILP) {
-      if (nmatch + 4 * 32 * SMP_ILP > SMP_LIST) {  // room for this batch's gram matches (<= 4 per sample)
-        __syncwarp();
-        nmatch = nver = sampled_verify(P, pd, spat, ulo, wl, nver, nmatch, lane);
-      }
       uint4 g[SMP_ILP], g2[SMP_ILP];
 #pragma unroll
       for (int r = 0; r < SMP_ILP; r++) {  // issue every load of the batch first
@@ -154,6 +151,10 @@ __global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const Scan
         // ascending: lanes own disjoint increasing bit ranges; bucket entries are in ascending start order
         const uint32_t any = __ballot_sync(0xffffffffu, nf != 0);
         if (any) {
+          if (nmatch + 4 * 32 > SMP_LIST) {  // room for this round's gram matches (<= 4 per lane)
+            __syncwarp();
+            nmatch = nver = sampled_verify(P, pd, spat, ulo, wl, nver, nmatch, lane);
+          }
           uint32_t inc = nf;
 #pragma unroll
           for (int d = 1; d < 32; d <<= 1) {

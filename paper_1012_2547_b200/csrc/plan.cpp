@@ -88,8 +88,9 @@ static inline int round16(int64_t x) { return (int)((x + 15) & ~(int64_t)15); }
 // saves DRAM traffic (S >= 256: the fetch granule is a 128-byte line) and the
 // filter stays selective: q * entropy(p) >= log2(S) + 12 bits and no gram occurs
 // at more than 4 of the S offsets (periodic patterns keep the full scan).
-static bool build_sampled(const uint8_t* pat, int64_t m, PlanHost* ph) {
+static bool build_sampled(const uint8_t* pat, int64_t m, int64_t period, PlanHost* ph) {
   if (m < 272) return false;
+  if (period < K3_MIN_PERIOD) return false;  // a unit's occurrences must fit the kernel's lists (plan.h)
   double cnt[256] = {0}, H = 0;
   for (int64_t i = 0; i < m; i++) cnt[pat[i]] += 1;
   for (int c = 0; c < 256; c++)
@@ -243,7 +244,7 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
   bool sampled_ok = false;
   if (fam == MB_FAM_AUTO || fam == MB_FAM_ALIGNED || fam == MB_FAM_SAMPLED) {
     PlanHost tmp;
-    sampled_ok = build_sampled(pat, m, &tmp);
+    sampled_ok = build_sampled(pat, m, ph->period, &tmp);
     if (sampled_ok && (opts == nullptr || opts->family == MB_FAM_AUTO || opts->family == MB_FAM_SAMPLED)) {
       fam = MB_FAM_SAMPLED;
       ph->bloom.swap(tmp.bloom);

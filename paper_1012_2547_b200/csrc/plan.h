@@ -41,6 +41,16 @@ struct PatDev {
   const uint64_t* so_masks; // K2: 256 complemented shift-or masks (device), bit j clear iff p[j] == c
 };
 
+// K3 sampled-kernel geometry shared with the planner: a warp unit covers
+// K3_UNIT_SEGS 2 KiB segments and lists at most K3_LIST matches at a time --
+// the unit's verified occurrences plus one round's unverified gram hits
+// (<= 4 per sample, one sample per lane).  The planner takes only patterns
+// whose smallest period keeps a unit's occurrences within that bound.
+constexpr int K3_UNIT_SEGS = 128;
+constexpr int K3_LIST = 1024;
+constexpr int K3_BATCH_HITS = 4 * 32;
+constexpr int64_t K3_MIN_PERIOD = (int64_t)K3_UNIT_SEGS * 2048 / (K3_LIST - K3_BATCH_HITS - 2) + 1;
+
 // gram hash shared by host table build and device lookup (words little-endian)
 __host__ __device__ inline uint32_t gram_mix(const uint32_t* w, int nw) {
   uint32_t h = 0x9E3779B9u;

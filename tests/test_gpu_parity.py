@@ -139,7 +139,8 @@ def test_sampled_family(cuda, sigmas):
 
 def test_sampled_plants_and_edges(cuda):
     rng = np.random.default_rng(7)
-    for m in (272, 300, 1024, 2047, 4096):
+    assert engine.Plan(rand_bytes(rng, 256, 272)).info().family != "sampled"  # period below K3_MIN_PERIOD
+    for m in (300, 1024, 2047, 4096):
         p = rand_bytes(rng, 256, m)
         assert engine.Plan(p).info().family == "sampled"
         n = 3 * TILE + 4321
@@ -153,6 +154,22 @@ def test_sampled_plants_and_edges(cuda):
             view = base[off : off + n - off]
             got = gpu_positions(p, view)
             assert np.array_equal(got, oracle.search(p, bytes(t)[off:n])), (m, off)
+
+
+@pytest.mark.parametrize("period", [60, 150, 294, 300, 520])
+def test_sampled_dense_periodic_occurrences(cuda, period):
+    """Long patterns with a short period over texts that repeat it: up to one
+    occurrence every `period` bytes.  The planner keeps the sampled family only
+    when a unit's occurrences fit its lists (period >= K3_MIN_PERIOD = 294);
+    either way every position must come out."""
+    rng = np.random.default_rng(period)
+    unit = rand_bytes(rng, 256, period)
+    p = (unit * (1 + 1100 // period))[:1024]
+    t = rand_bytes(rng, 256, 3000) + unit * ((6 << 20) // period) + rand_bytes(rng, 256, 3000)
+    fam = engine.Plan(p).info().family
+    if period < 294:
+        assert fam != "sampled", fam
+    check(p, t)
 
 
 @pytest.mark.parametrize("m", [1, 7, 31, 32, 33, 63, 64])
