@@ -137,6 +137,11 @@ def test_plan_info_families():
     for m in (5, 6, 7, 8):
         assert engine.Plan(bytes(rng0.integers(0, 2, m, dtype=np.uint8))).info().family == "swar", m
     assert engine.Plan(bytes(range(40, 48))).info().family == "aligned"
+    # sampled (K3) only for periods >= 294: a 256 KiB unit's occurrences fit its list
+    unit = bytes(rng0.integers(0, 256, 200, dtype=np.uint8))
+    assert engine.Plan((unit * 6)[:1024]).info().family != "sampled"
+    unit = bytes(rng0.integers(0, 256, 300, dtype=np.uint8))
+    assert engine.Plan((unit * 4)[:1024]).info().family == "sampled"
     assert not engine.Plan(b"a" * 99 + b"b").info().periodic
     with pytest.raises(ValueError):
         engine.Plan(b"x" * 8193)
