@@ -229,7 +229,10 @@ struct FiltWIN4 {
 // NW anchor words (window 4 NW + 3 bytes) words k .. k+NW-1 must all match
 // (G[4w + j] = p[a+j+4w .. +4)): small alphabets need NW = 2, 3 to keep the
 // candidate rate low.  w[] holds 4 + NW - 1 >= 5 words.
-template <int NW>
+// RUN1: c^m patterns (period 1): any hit marks the lane's 16 positions -- the
+// run test of the verify path decides every start exactly (run1_lane_matches);
+// a separate instantiation so the general filter's fast path carries no check.
+template <int NW, bool RUN1 = false>
 struct FiltALIGNED {
   __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
     if constexpr (NW == 1) {
@@ -238,9 +241,7 @@ struct FiltALIGNED {
       for (int k = 0; k < 4; k++)
         hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
       if (!hit) return 0;
-      // c^m: the run test decides every start exactly (run1_lane_matches), so
-      // any hit just marks the lane's 16 positions
-      if (P.periodic && P.per == 1) return 0xFFFFu;
+      if (RUN1) return 0xFFFFu;
     }
     uint32_t mk = 0;
 #pragma unroll

@@ -554,7 +554,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
 static int family_key(const PatDev& d) {
   if (d.family == MB_FAM_SWAR) return (int)(10 + d.m);
   if (d.family == MB_FAM_SHIFTOR) return d.m <= 32 ? 20 : 21;
-  if (d.family == MB_FAM_ALIGNED) return 30 + d.nw;
+  if (d.family == MB_FAM_ALIGNED) return d.nw == 1 && d.periodic && d.per == 1 ? 40 : 30 + d.nw;
   return d.family;
 }
 
@@ -577,6 +577,7 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
     case MB_FAM_ALIGNED:
       if (d.nw == 3) return launch_group<FiltALIGNED<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
       if (d.nw == 2) return launch_group<FiltALIGNED<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      if (d.periodic && d.per == 1) return launch_group<FiltALIGNED<1, true>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
       return launch_group<FiltALIGNED<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     case MB_FAM_SAMPLED: return launch_group<SampledTag>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     case MB_FAM_SHIFTOR: {
