@@ -10,7 +10,7 @@ namespace mb {
 // bytes); a bloom filter + bucketed offset lists in smem map a gram to the
 // pattern offsets j where it occurs, each giving a candidate start s = x - j
 // that is verified against the text in global memory.  A warp owns SMP_SEGS
-// consecutive segments (8 tiles) and reads every sample whose bit range
+// consecutive segments (16 tiles) and reads every sample whose bit range
 // [S*i, S*i + S) meets them, 5 independent 16-byte loads per lane in flight
 // (a 128-segment unit has ~260 samples at S = 1008: two batches of 160).
 // Output (segment counts, uint16 tile-relative lists) is the scan kernel's, so
