@@ -828,17 +828,35 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
 // selective batch of anchor-filter patterns, one MP pass over the text), then
 // one offsets and one expand launch over all K patterns' segments, so the
 // output is CSR in the caller's pattern order whatever the family mix.
-// h_rep / h_need (batches, host, this batch's indices; null = identity / scan
-// all): representative of each pattern (identical patterns are searched once:
-// offsets/expand read the representative's segments for the duplicate's CSR
-// range) and per-pattern scan flags (0: covered by the batch pass or by its
-// representative -- the count kernels skip its tiles).
+// Batch-only inputs of run_search (a single search passes none).
+struct SubBatch {
+  const BatchPass* bp = nullptr;     // batch-pass plan (null / kind 0: no pass)
+  const uint32_t* d_tab = nullptr;   // its tables on the device
+  int chunk0 = 0;                    // first pass-table chunk of this sub-batch
+  // host, this sub-batch's indices (null = identity / scan all): each
+  // pattern's representative (identical patterns are searched once: offsets
+  // and expand read the representative's segments for the duplicate's CSR
+  // range, or replicate_kernel copies its output when | REP_COPY) and the
+  // per-pattern scan flags (0: covered by the batch pass or by its
+  // representative -- the count kernels skip its tiles)
+  const int32_t* h_rep = nullptr;
+  const uint32_t* h_need = nullptr;
+  int64_t* csr0 = nullptr;           // the CSR's leading entry, zeroed by the search
+  const int32_t* d_rep = nullptr;    // prepared batch: h_rep already resident on the device
+  const uint32_t* d_need = nullptr;  // prepared batch: h_need already resident on the device
+};
+
 static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text,
                       int64_t n, int64_t* d_out, int64_t cap, int64_t* offsets_plus1, cudaStream_t st,
-                      const int64_t* out_base = nullptr, const BatchPass* bp = nullptr,
-                      const uint32_t* d_tab = nullptr, int chunk0 = 0, const int32_t* h_rep = nullptr,
-                      const uint32_t* h_need = nullptr, int64_t* csr0 = nullptr,
-                      const int32_t* d_rep_pre = nullptr, const uint32_t* d_need_pre = nullptr) {
+                      const int64_t* out_base = nullptr, const SubBatch& sb = SubBatch()) {
+  const BatchPass* bp = sb.bp;
+  const uint32_t* d_tab = sb.d_tab;
+  const int chunk0 = sb.chunk0;
+  const int32_t* h_rep = sb.h_rep;
+  const uint32_t* h_need = sb.h_need;
+  int64_t* csr0 = sb.csr0;
+  const int32_t* d_rep_pre = sb.d_rep;
+  const uint32_t* d_need_pre = sb.d_need;
   ScanParams P;
   memset(&P, 0, sizeof(P));
   const uintptr_t addr = (uintptr_t)d_text;
@@ -1170,10 +1188,17 @@ static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int 
     }
     // the whole batch in one go: a prepared batch's device-resident flags
     const bool all = k0 == 0 && kk == K;
+    SubBatch sb;
+    sb.bp = whole ? bp : nullptr;
+    sb.d_tab = whole ? d_tab : nullptr;
+    sb.chunk0 = k0 / MP_CHUNK;
+    sb.h_rep = dups ? lrep.data() : nullptr;
+    sb.h_need = (dups || whole) ? lneed.data() : nullptr;
+    sb.csr0 = k0 == 0 ? d_offsets : nullptr;
+    sb.d_rep = all ? d_rep_pre : nullptr;
+    sb.d_need = all ? d_need_pre : nullptr;
     int rc = run_search(c, d_pats + k0, h_pats + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st,
-                        k0 ? d_offsets + k0 : nullptr, whole ? bp : nullptr, whole ? d_tab : nullptr, k0 / MP_CHUNK,
-                        dups ? lrep.data() : nullptr, (dups || whole) ? lneed.data() : nullptr,
-                        k0 == 0 ? d_offsets : nullptr, all ? d_rep_pre : nullptr, all ? d_need_pre : nullptr);
+                        k0 ? d_offsets + k0 : nullptr, sb);
     if (rc) return rc;
   }
   return MB_OK;
