@@ -120,7 +120,10 @@ int mb_find_batch_prepared(mb_ctx* ctx, const mb_batch* batch, const uint8_t* d_
 
 /* ---- host-buffer entry (the search_X(pattern, text) analogue, synchronous) ----
  * Copies the text host->device, scans, copies positions device->host.  Returns
- * MB_EOVERFLOW (with *h_count set) if cap is too small. */
+ * MB_EOVERFLOW (with *h_count set) if cap is too small.  Compiled plans are
+ * cached in the context by pattern bytes (up to 4096, freed with the context).
+ * With cap <= 2^20 all cap entries of h_out may be written (those past the
+ * count are unspecified). */
 int mb_search_host(mb_ctx* ctx, const uint8_t* h_pattern, int64_t m, const uint8_t* h_text, int64_t n,
                    int64_t* h_out, int64_t cap, int64_t* h_count);
 int mb_search_batch_host(mb_ctx* ctx, const uint8_t* const* h_patterns, const int64_t* ms, int K,
