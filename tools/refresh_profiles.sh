@@ -14,4 +14,5 @@ for w in cfg1 cfg3 cfg5; do python bench.py --workload $w --steps 10 > gpurun_ou
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/prof/bench_reference_arm.json 2> gpurun_out/prof/ref.err
 python tools/one_cell.py 95 16 0 > /dev/null && ncu --set full --import-source on --clock-control none -k regex:"mp_scan|mpb_scan" -s 1 -c 1 \
     -o gpurun_out/prof/ncu_full_mp_cfg3 python tools/kprof.py cfg2 95 16 > gpurun_out/prof/ncu_mp.log 2>&1
+python tools/m_sweep.py 4 > gpurun_out/prof/m_sweep_4GiB.jsonl 2> gpurun_out/prof/m_sweep.err
 echo done
