@@ -150,6 +150,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workloads
+def cfg4_desc(n):
+    return (f"cfg4: {n / 2**30:.0f} GiB i.i.d. uniform sigma=256 text per GPU, 1 pattern per m in "
+            f"{list(CFG4_LENGTHS)} copied from a random offset")
+
+
 def build_workload(args, rank, world):
     """Host text (pinned) + patterns for this rank; returns dict."""
     import numpy as np
@@ -173,8 +178,7 @@ def build_workload(args, rank, world):
             _cfg4_stripes(nxt, stripe0 + max(n // inputs.STRIPE, 1), nxt.size)
             h[n:] = nxt[:halo]
         pats = inputs.config4_patterns(h[:n]) if rank == 0 else None
-        desc = (f"cfg4: {n / 2**30:.0f} GiB i.i.d. uniform sigma=256 text per GPU, 1 pattern per m in "
-                f"{list(CFG4_LENGTHS)} copied from a random offset")
+        desc = cfg4_desc(n)
         sigma = 256
     elif args.workload == "cfg1":
         t, pats = inputs.config1()
@@ -237,7 +241,10 @@ def run_reference(args, rank, world):
 
     threads = os.cpu_count() or 1
     sample = min(args.cpu_sample, args.n or (16 << 30)) if args.workload == "cfg4" else 0
-    if args.workload == "cfg4":
+    if args.workload == "cfg4":  # the arm's workload; the reference's CPU path times a prefix of it
+        n_full = args.n or (16 << 30)
+        n_full = (n_full // inputs.STRIPE) * inputs.STRIPE if n_full >= inputs.STRIPE else n_full
+        desc = cfg4_desc(n_full)
         sample = max(inputs.STRIPE, (sample // inputs.STRIPE) * inputs.STRIPE) if sample >= inputs.STRIPE else sample
         t = np.empty(sample, dtype=np.uint8)
         _cfg4_stripes(t, 0, sample)
@@ -247,7 +254,8 @@ def run_reference(args, rank, world):
         wl = build_workload(args, 0, 1)
         t = wl["host"].numpy()[: wl["n"]]
         pats, sigma = wl["patterns"], wl["sigma"]
-        sample = t.size
+        sample = n_full = t.size
+        desc = wl["desc"]
     algos = [select_applicable(sigma, len(p)).id for p in pats]
 
     def step():
@@ -265,7 +273,8 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": args.workload, "sample_bytes": int(sample), "patterns_m": [len(p) for p in pats]},
+        "config": {"workload": desc, "text_bytes_per_gpu": int(n_full), "patterns_m": [len(p) for p in pats],
+                   "sample_bytes": int(sample)},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": f"{sample / 2**20:.0f} MiB prefix x {len(pats)} patterns, algorithms {algos} "
                                    f"(oracle/oracle.c restatement, {threads} threads, halo-overlapped chunks)"},
