@@ -223,6 +223,31 @@ struct FiltWIN4 {
   }
 };
 
+// K1 / 5 <= m <= 6 (auto): every occurrence's 5-byte anchor window [a, a+5)
+// holds a 4-byte text window at an even offset e, equal to G0 = p[a..a+4) (e =
+// s + a) or G1 = p[a+1..a+5) (e = s + a + 1): two windows per text word (the
+// word and its 16-bit funnel shift) instead of WIN4's four.  delta = a + 1:
+// word k's bits 4k..4k+3 = {w == G1, w == G0, f == G1, f == G0}.
+struct FiltWIN4E {
+  __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
+    const uint32_t g0 = P.G[0], g1 = P.G[1];
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint32_t f = __funnelshift_r(w[k], w[k + 1], 16);
+      hit |= (w[k] == g0) | (w[k] == g1) | (f == g0) | (f == g1);
+    }
+    if (!hit) return 0;
+    uint32_t mk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint32_t f = __funnelshift_r(w[k], w[k + 1], 16);
+      mk |= ((w[k] == g1 ? 1u : 0u) | (w[k] == g0 ? 2u : 0u) | (f == g1 ? 4u : 0u) | (f == g0 ? 8u : 0u)) << (4 * k);
+    }
+    return mk;
+  }
+};
+
 // K1/K3 / m >= 7: every occurrence contains one 4-aligned text word inside its
 // 7-byte anchor window [a, a+7); that word equals p[a+j .. a+j+4) for exactly
 // one j in 0..3.  Word k matching G_j marks bitmap position 4k + 3 - j.  With

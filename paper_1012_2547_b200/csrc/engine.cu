@@ -559,6 +559,7 @@ static int family_key(const PatDev& d) {
   if (d.family == MB_FAM_SWAR) return (int)(10 + d.m);
   if (d.family == MB_FAM_SHIFTOR) return d.m <= 32 ? 20 : 21;
   if (d.family == MB_FAM_ALIGNED) return d.nw == 1 && d.periodic && d.per == 1 ? 40 : 30 + d.nw;
+  if (d.family == MB_FAM_WIN4 && d.nw == 2) return 50;  // even-offset windows
   return d.family;
 }
 
@@ -577,7 +578,9 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
         case 8: return launch_group<FiltSWAR<8>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
       }
       return fail(MB_EINVAL, "SWAR family needs m in 1..3 or 5..8");
-    case MB_FAM_WIN4: return launch_group<FiltWIN4>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+    case MB_FAM_WIN4:
+      if (d.nw == 2) return launch_group<FiltWIN4E>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      return launch_group<FiltWIN4>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     case MB_FAM_ALIGNED:
       if (d.nw == 3) return launch_group<FiltALIGNED<3>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
       if (d.nw == 2) return launch_group<FiltALIGNED<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);

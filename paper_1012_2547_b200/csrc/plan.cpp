@@ -325,6 +325,24 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       d.delta = a;
       d.G[0] = load_le32(pat + a);
       d.exact = (m == 4);
+      // m = 5, 6 (auto): even-offset windows of a 5-byte anchor (FiltWIN4E,
+      // two compares per text word instead of four) unless they hit > 4x as often
+      if ((opts == nullptr || opts->family == MB_FAM_AUTO) && (m == 5 || m == 6)) {
+        int ae = 0;
+        double re = 1e300;
+        for (int64_t b = 0; b + 5 <= m; b++) {
+          const double r = 2 * (gram_prob(pat + b, pr) + gram_prob(pat + b + 1, pr));
+          if (r < re * (1 - 1e-12)) re = r, ae = (int)b;
+        }
+        if (re <= 4 * rw || re < 1e-4) {
+          ph->anchor = ae;
+          d.nw = 2;  // WIN4E
+          d.delta = ae + 1;
+          d.G[0] = load_le32(pat + ae);
+          d.G[1] = load_le32(pat + ae + 1);
+          d.exact = 0;
+        }
+      }
       break;
     }
     case MB_FAM_ALIGNED: {
