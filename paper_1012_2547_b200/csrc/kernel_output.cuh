@@ -15,6 +15,7 @@ namespace mb {
 #define MB_FUSE_MAX 16
 #endif
 constexpr int FUSE_MAX = MB_FUSE_MAX;  // sorted lists; unsorted ones at most 8 (the sort network's width)
+static_assert(FUSE_MAX <= 16, "fused lists are read as two 16-byte vectors");
 
 // 8-input sorting network (19 compare-exchanges)
 __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
@@ -237,15 +238,16 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
             const int64_t pos0 = (rem / NWARP) * TILE - shift;  // position of tile offset 0
             const uint16_t* L = P.lists + ds * LIST_CAP;
             if (!P.unsorted_lists) {
+              // the list's (<= FUSE_MAX = 16) entries as two 16-byte loads
+              // issued together (the first 8 prefetched for the first list)
+              const uint4* L4 = reinterpret_cast<const uint4*>(L);  // 64-byte aligned list
+              const uint4 la = q == fq ? pre : L4[0];
+              const uint4 lb = vq > 8 ? L4[1] : make_uint4(0, 0, 0, 0);
               for (uint32_t e = 0; e < vq; e++) {
-                uint32_t x;
-                if (q == fq && e < 8) {  // prefetched
-                  const uint32_t w = (e >> 1) == 0 ? pre.x : (e >> 1) == 1 ? pre.y : (e >> 1) == 2 ? pre.z : pre.w;
-                  x = (w >> (16 * (e & 1))) & 0xFFFFu;
-                } else {
-                  x = L[e];
-                }
-                if (run + e < P.cap) P.out[run + e] = pos0 + x;
+                const uint4 lq = e < 8 ? la : lb;
+                const uint32_t i = e & 7;
+                const uint32_t w = (i >> 1) == 0 ? lq.x : (i >> 1) == 1 ? lq.y : (i >> 1) == 2 ? lq.z : lq.w;
+                if (run + e < P.cap) P.out[run + e] = pos0 + ((w >> (16 * (i & 1))) & 0xFFFFu);
               }
             } else {
               const uint4 raw = q == fq ? pre : *reinterpret_cast<const uint4*>(L);  // 8 slots (64-byte aligned list)
