@@ -213,6 +213,13 @@ struct FiltWIN4 {
              (shr8(w[k], w[k + 1], 3) == g);
     }
     if (!hit) return 0;
+    return run_direct(w, P);
+  }
+  // The mask alone (no early-out test): cheaper where most warps would take
+  // the mask pass anyway (the scan kernel switches to it per warp while the
+  // previous segment had candidates, e.g. m = 4 over a 4-letter alphabet).
+  __device__ static __forceinline__ uint32_t run_direct(const uint32_t* w, const PatDev& P) {
+    const uint32_t g = P.G[0];
     uint32_t mk = 0;
 #pragma unroll
     for (int k = 0; k < 4; k++)
@@ -266,8 +273,14 @@ struct FiltALIGNED {
       for (int k = 0; k < 4; k++)
         hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
       if (!hit) return 0;
-      if (RUN1) return 0xFFFFu;
+      if constexpr (RUN1) return 0xFFFFu;
     }
+    if constexpr (!RUN1) return run_direct(w, P);
+    return 0;
+  }
+  __device__ static __forceinline__ uint32_t run_direct(const uint32_t* w, const PatDev& P) {
+    static_assert(!RUN1 || NW == 1, "RUN1 is a one-word filter");
+    if constexpr (RUN1) return run(w, P);
     uint32_t mk = 0;
 #pragma unroll
     for (int k = 0; k < 4; k++)
@@ -294,6 +307,13 @@ template <class F, class = void>
 struct always_exact : std::false_type {};
 template <class F>
 struct always_exact<F, std::void_t<decltype(F::kAlwaysExact)>> : std::true_type {};
+
+// Filters with a run_direct (the mask without the early-out test), used per
+// warp while the previous segment had candidates (kernel_scan.cuh `busy`).
+template <class F, class = void>
+struct has_direct : std::false_type {};
+template <class F>
+struct has_direct<F, std::void_t<decltype(&F::run_direct)>> : std::true_type {};
 
 template <class F, class = void>
 struct is_shiftor : std::false_type {};

@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   uint32_t ph = 0;
   uint32_t f_w0 = 0, f_w1 = 0, f_ex = 0, f_cnt = 0;  // FUSED: the one tile's results
   int64_t f_tk = -1, f_pos0 = 0;
+  bool busy = false;  // the previous segment had candidates (has_direct filters: masks without the early-out)
   for (;; s = (s + 1 == NS) ? (ph ^= 1u, 0) : s + 1) {
     mbar_wait(&full[s], ph);
     const int64_t tk = hdr[s].tk;
@@ -195,10 +196,14 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
         const uint4 X = *reinterpret_cast<const uint4*>(S + c);
         const uint2 Y = *reinterpret_cast<const uint2*>(S + c + 16);
         const uint32_t w[6] = {X.x, X.y, X.z, X.w, Y.x, Y.y};
-        mk[r] = Filt::run(w, pd);
+        if constexpr (has_direct<Filt>::value)
+          mk[r] = busy ? Filt::run_direct(w, pd) : Filt::run(w, pd);
+        else
+          mk[r] = Filt::run(w, pd);
         anyc |= (mk[r] != 0);
       }
       have = __any_sync(0xffffffffu, anyc);
+      busy = have;
       if (have) {
         // ---- slow path: validity mask at text edges, linear segment bitmap
 #pragma unroll
