@@ -967,7 +967,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       g_launches++;
       CUDA_TRY(cudaGetLastError());
       if (ndup) {  // duplicates marked REP_COPY: copy the representatives' ranges
-        CUDA_TRY(launch_pdl(replicate_kernel, (int)std::min<int64_t>(K, (int64_t)c->nsm * 4), 512, st, P));
+        CUDA_TRY(launch_pdl(replicate_kernel, K > REPL_MAXK ? (int)std::min<int64_t>(K, (int64_t)c->nsm * 4) : c->nsm * 4, 512, st, P));
         g_launches++;
         CUDA_TRY(cudaGetLastError());
       }

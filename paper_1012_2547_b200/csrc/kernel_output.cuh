@@ -509,7 +509,19 @@ __global__ void __launch_bounds__(512) replicate_kernel(const ScanParams P) {
       const int64_t run_end = min(e_end, s_pref[d + 1]);
       const int64_t* src = P.out + start(r) - s_pref[d];
       int64_t* dst = P.out + start(k) - s_pref[d];
-      for (int64_t i = e + lane; i < run_end; i += 32) dst[i] = src[i];
+      // all of a lane's loads first (src and dst share P.out, so the compiler
+      // would otherwise keep each load behind the previous store)
+      int64_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int64_t i = e + lane + 32 * j;
+        if (i < run_end) v[j] = src[i];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int64_t i = e + lane + 32 * j;
+        if (i < run_end) __stcs(dst + i, v[j]);
+      }
       e = run_end;
     }
   }
