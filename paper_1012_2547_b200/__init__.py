@@ -19,12 +19,15 @@ from .core import (
     brute_force_search,
     verify_equal,
 )
+from .differential import DifferentialReport, Mismatch, run_differential
 from .harness import (
     ALLOWED_SIGMAS,
+    CORPUS_EXPECTATIONS,
     DEFAULT_LENGTHS,
     BenchConfig,
     Measurement,
     generate_rand_text,
+    load_corpus,
     run_benchmark,
     sample_patterns,
     sample_positions,

@@ -162,11 +162,20 @@ def gpu_benchmark(text_bytes, text_id, algos, lengths, patterns_per_length, seed
     return rows
 
 
+def sort_rows(rows):
+    """Row order of the reference's CSV (report.py:50-51 _row_key): registry
+    order, then unknown ids (B200) by name, then m."""
+    from .registry import REGISTRY
+
+    order = {a.id: i for i, a in enumerate(REGISTRY)}
+    return sorted(rows, key=lambda r: (order.get(r[3], len(order)), r[3], r[4]))
+
+
 def render_csv(rows) -> str:
     buf = io.StringIO()
     w = csv.writer(buf, lineterminator="\n")
     w.writerow(CSV_HEADER)
-    for r in rows:
+    for r in sort_rows(rows):
         w.writerow([r[0], r[1], r[2], r[3], r[4], format_value(r[5]), format_value(r[6]), format_value(r[7]), r[8]])
     return buf.getvalue()
 

@@ -422,6 +422,11 @@ static int stage_end(mb_ctx* c, cudaStream_t st) {
 // Stream ordering of the searches of one context (they share its tickets and
 // scratch): a search on another stream than the previous one waits for it.
 static int ctx_enter(mb_ctx* c, cudaStream_t st) {
+  // a context's scratch, tickets and plan uploads live on its device: refuse
+  // to launch from another current device (its pointers would be foreign)
+  int dev = -1;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev != c->device) return fail(MB_EINVAL, "current CUDA device differs from the context's device");
   if (c->have_last && c->last_st != st) CUDA_TRY(cudaStreamWaitEvent(st, c->done_ev, 0));
   return MB_OK;
 }
@@ -1107,7 +1112,8 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
   if (mp_used)
     for (int k = 0; k < K; k++)
       if (!h_need[k] && (!h_rep || h_rep[k] == k)) add(k, true), nlisted++;  // (h_rep[k] == k: no flag)
-  if ((int)groups.size() > MAX_GROUPS) return fail(MB_EINVAL, "too many kernel families in one batch");
+  // at most NFAMILY_KEYS keys, each once ungated and once gated: always fits
+  if ((int)groups.size() > MAX_GROUPS) return fail(MB_ECUDA, "internal: more family groups than ticket slots");
   const bool identity = groups.size() == 1 && nlisted == K;  // all patterns in order: no index list needed
   if (!identity && nlisted) {
     if ((rc = grow(&c->plist, &c->plist_cap, nlisted, "family index lists"))) return rc;
@@ -1136,14 +1142,14 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
   if (n < 0 || cap < 0) return fail(MB_EINVAL, "negative size");
   if (n > 0 && !d_text) return fail(MB_EINVAL, "null text");
   cudaStream_t st = (cudaStream_t)stream;
+  int rc = ctx_enter(c, st);
+  if (rc) return rc;
   if (p->h.m > n) {
     CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(int64_t), st));
-    return MB_OK;
+    return ctx_leave(c, st);
   }
   const PatDev* dd = nullptr;
-  int rc = plan_device(p, &dd);
-  if (rc) return rc;
-  if ((rc = ctx_enter(c, st))) return rc;
+  if ((rc = plan_device(p, &dd))) return rc;
   if ((rc = stage_begin(c))) return rc;
   rc = run_search(c, dd, &p->dview, 1, d_text, n, d_out, cap, d_count, st);
   if (rc) tickets_recover(c, st);
@@ -1216,6 +1222,8 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
   if (!c || !plans || K < 1 || !d_offsets) return fail(MB_EINVAL, "bad argument");
   if (n < 0 || cap < 0) return fail(MB_EINVAL, "negative size");
   cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ctx_enter(c, st))) return rc;
   c->h_pats.resize(K);
   for (int k = 0; k < K; k++) {
     if (!plans[k]) return fail(MB_EINVAL, "null plan in batch");
@@ -1224,9 +1232,7 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
     if (rc) return rc;
     c->h_pats[k] = plans[k]->dview;
   }
-  int rc;
   if ((rc = grow(&c->d_pats, &c->pats_cap, K, "batch params"))) return rc;
-  if ((rc = ctx_enter(c, st))) return rc;
   if ((rc = stage_begin(c))) return rc;
   if ((rc = stage_upload(c, c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, st))) return rc;
   plan_pass(plans, c->h_pats.data(), K, &c->pass);
@@ -1323,6 +1329,9 @@ int mb_find_batch_prepared(mb_ctx* c, const mb_batch* b, const uint8_t* d_text, 
 int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, void* stream) {
   if (!c || !d_hist) return fail(MB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
+  int dev = -1;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev != c->device) return fail(MB_EINVAL, "current CUDA device differs from the context's device");
   CUDA_TRY(cudaMemsetAsync(d_hist, 0, 256 * sizeof(int64_t), st));
   if (n <= 0) return MB_OK;
   int64_t blocks = std::min<int64_t>((n + 4095) / 4096, (int64_t)c->nsm * 8);
@@ -1331,6 +1340,19 @@ int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, v
   CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }
+
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 static int ensure_host_bufs(mb_ctx* c, int64_t n, int64_t outcap, int64_t nofs) {
   if (!c->stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -1367,6 +1389,9 @@ static int ensure_host_bufs(mb_ctx* c, int64_t n, int64_t outcap, int64_t nofs) 
 int mb_search_batch_host(mb_ctx* c, const uint8_t* const* h_patterns, const int64_t* ms, int K,
                          const uint8_t* h_text, int64_t n, int64_t* h_out, int64_t cap, int64_t* h_offsets) {
   if (!c || !h_patterns || !ms || K < 1 || !h_offsets) return fail(MB_EINVAL, "bad argument");
+  // host buffers in and out: run on the context's device whatever is current
+  DeviceGuard guard(c->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   if (n < 0 || cap < 0 || (n > 0 && !h_text)) return fail(MB_EINVAL, "bad text");
   // plans come from the context's cache (created and uploaded on first use;
   // the cache is dropped wholesale past 4096 patterns)
@@ -1390,27 +1415,30 @@ int mb_search_batch_host(mb_ctx* c, const uint8_t* const* h_patterns, const int6
   int rc = ensure_host_bufs(c, n, std::max<int64_t>(cap, 1), K + 1);
   if (rc) return rc;
   cudaStream_t st = c->stream;
-  if (n > 0) cudaMemcpyAsync(c->d_text, h_text, n, cudaMemcpyHostToDevice, st);
+  if (n > 0) CUDA_TRY(cudaMemcpyAsync(c->d_text, h_text, n, cudaMemcpyHostToDevice, st));
   rc = mb_find_batch(c, plans.data(), K, c->d_text, n, c->d_out, cap, c->d_offs, st);
-  // small outputs come back with the offsets, before the one synchronisation
-  // (entries past the count are don't-care); large ones once the count is known
-  const bool eager = cap > 0 && cap <= (1 << 20);
-  if (!rc) {
-    cudaMemcpyAsync(h_offsets, c->d_offs, sizeof(int64_t) * (K + 1), cudaMemcpyDeviceToHost, st);
-    if (eager) cudaMemcpyAsync(h_out, c->d_out, sizeof(int64_t) * cap, cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) rc = cuda_fail(e, "batch search");
+  if (rc) {
+    cudaStreamSynchronize(st);  // the upload may still read h_text
+    return rc;
   }
-  if (!rc) {
-    int64_t total = h_offsets[K];
-    int64_t ncopy = std::min(total, cap);
-    if (ncopy > 0 && !eager) {
-      cudaError_t e = cudaMemcpy(h_out, c->d_out, sizeof(int64_t) * ncopy, cudaMemcpyDeviceToHost);
-      if (e != cudaSuccess) rc = cuda_fail(e, "position copy");
-    }
-    if (!rc && total > cap) rc = fail(MB_EOVERFLOW, "output capacity too small");
+  // the first EAGER positions come back with the offsets, before the one
+  // synchronisation (entries past the count are don't-care); the rest, if
+  // any, once the count is known
+  const int64_t eager = std::min<int64_t>(cap, (int64_t)1 << 16);
+  cudaError_t e = cudaMemcpyAsync(h_offsets, c->d_offs, sizeof(int64_t) * (K + 1), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && eager > 0)
+    e = cudaMemcpyAsync(h_out, c->d_out, sizeof(int64_t) * eager, cudaMemcpyDeviceToHost, st);
+  const cudaError_t es = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "result copy");
+  if (es != cudaSuccess) return cuda_fail(es, "batch search");
+  const int64_t total = h_offsets[K];
+  const int64_t ncopy = std::min(total, cap);
+  if (ncopy > eager) {
+    e = cudaMemcpy(h_out + eager, c->d_out + eager, sizeof(int64_t) * (ncopy - eager), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "position copy");
   }
-  return rc;
+  if (total > cap) return fail(MB_EOVERFLOW, "output capacity too small");
+  return MB_OK;
 }
 
 int mb_search_host(mb_ctx* c, const uint8_t* h_pattern, int64_t m, const uint8_t* h_text, int64_t n,

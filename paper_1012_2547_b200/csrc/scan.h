@@ -49,17 +49,21 @@ constexpr int SEG_WORDS = SEG / 32;
 constexpr int STAGES = MB_STAGES;  // TMA ring depth (max; scan_kernel may run with 2, see ScanParams.nstages)
 constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offsets
 // ticket counters (one uint64 each, zeroed between searches):
-constexpr int MAX_GROUPS = 24;      // count-kernel launches of one batch: slots 0..23 (10 family keys,
-                                    // twice with a batch pass: scans + overflow fallback)
-constexpr int TICKET_OFFSETS = 24;  // offsets_kernel chunks (when the grid is not co-resident)
-constexpr int MAX_MP_CHUNKS = 7;    // batch-pass table chunks (MP_CHUNK patterns each): slots 25..31
-constexpr int TICKET_MP0 = 25;
-constexpr int TICKET_DENSE = 32;    // segments queued for expand_kernel (even epochs; odd: TICKET_DENSE_ODD)
-constexpr int TICKET_DONE = 33;     // offsets_kernel CTAs that finished (the last one zeroes the slots)
-constexpr int TICKET_DENSE_ODD = 34;
-constexpr int TICKET_OFFBAR = 35;   // offsets_kernel grid barrier (co-resident grid)
-constexpr int TICKET_MPBAR = 36;    // batch pass: grid barrier after its prologue zeroes the counts
-constexpr int NTICKETS = 37;
+// count-kernel launches of one batch: one per family key (engine.cu
+// family_key: SWAR m = 1,2,3,5..8 (7), WIN4 and WIN4E (2), ALIGNED 1/2/3 words
+// and RUN1 (4), SAMPLED (1), SO32/SO64 (2) = NFAMILY_KEYS), twice with a batch
+// pass (scans + overflow fallback)
+constexpr int NFAMILY_KEYS = 16;
+constexpr int MAX_GROUPS = 2 * NFAMILY_KEYS;  // slots 0..31
+constexpr int TICKET_OFFSETS = MAX_GROUPS;    // offsets_kernel chunks (ticket order)
+constexpr int MAX_MP_CHUNKS = 7;    // batch-pass table chunks (MP_CHUNK patterns each)
+constexpr int TICKET_MP0 = TICKET_OFFSETS + 1;
+constexpr int TICKET_DENSE = TICKET_MP0 + MAX_MP_CHUNKS;  // segments queued for expand_kernel (even epochs)
+constexpr int TICKET_DONE = TICKET_DENSE + 1;       // offsets_kernel CTAs that finished (the last one zeroes the slots)
+constexpr int TICKET_DENSE_ODD = TICKET_DONE + 1;   // expand queue of odd epochs
+constexpr int TICKET_OFFBAR = TICKET_DENSE_ODD + 1; // offsets_kernel grid barrier (co-resident grid)
+constexpr int TICKET_MPBAR = TICKET_OFFBAR + 1;     // batch pass: grid barrier after its prologue zeroes the counts
+constexpr int NTICKETS = TICKET_MPBAR + 1;
 constexpr int MP_CHUNK = 512;     // patterns per MP table (smem budget)
 constexpr int32_t REP_COPY = 1 << 30;  // ScanParams.rep flag (see there)
 

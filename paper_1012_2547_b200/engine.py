@@ -265,11 +265,25 @@ def context(device: int | None = None) -> Context:
     return c
 
 
-def _stream_handle(stream=None):
+def _stream_handle(stream=None, device=None):
     import torch
 
-    s = torch.cuda.current_stream() if stream is None else stream
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev_index(t) -> int:
+    return t.device.index if t.device.index is not None else 0
+
+
+def _wait(stream, device):
+    """Before a host read of a search result: a search on a stream other than
+    the device's current one is not ordered before .item()/.cpu() (which sync
+    only the current stream)."""
+    import torch
+
+    if stream is not None and stream != torch.cuda.current_stream(device):
+        stream.synchronize()
 
 
 def to_device_text(text, device=None):
@@ -299,18 +313,32 @@ def to_device_text(text, device=None):
     return out
 
 
+def _take(out, c, stream, device):
+    """Copy of out[:c] ordered after the search: on the search's stream, which
+    is then drained, so the next search into the shared buffer cannot overtake it."""
+    import torch
+
+    if stream is None or stream == torch.cuda.current_stream(device):
+        return out[:c].clone()
+    with torch.cuda.stream(stream):
+        res = out[:c].clone()
+    stream.synchronize()
+    return res
+
+
 class _OutBuf:
-    """Per-thread, per-device growable int64 output buffer."""
+    """Per-thread, per-device growable int64 output buffers."""
 
     def __init__(self):
-        self.t = None
+        self.t = {}
 
-    def get(self, cap):
+    def get(self, cap, device):
         import torch
 
-        if self.t is None or self.t.numel() < cap or self.t.device.index != torch.cuda.current_device():
-            self.t = torch.empty(max(cap, 1 << 16), dtype=torch.int64, device="cuda")
-        return self.t
+        t = self.t.get(device.index)
+        if t is None or t.numel() < cap:
+            t = self.t[device.index] = torch.empty(max(cap, 1 << 16), dtype=torch.int64, device=device)
+        return t
 
 
 def _outbuf() -> _OutBuf:
@@ -322,13 +350,18 @@ def _outbuf() -> _OutBuf:
 
 def find_into(plan: Plan, d_text, out, count, stream=None):
     """Asynchronous: positions -> out (int64 CUDA tensor or None), total -> count
-    (1-element int64 CUDA tensor).  Returns nothing; caller syncs."""
+    (1-element int64 CUDA tensor).  Runs on the text's device (its context,
+    its current stream unless `stream` is given).  Returns nothing; caller syncs."""
+    import torch
+
     L = load_library()
-    ctx = context()
-    cap = 0 if out is None else out.numel()
-    _check(L.mb_find(ctx.handle, plan.handle, ctypes.c_void_p(d_text.data_ptr() if d_text.numel() else 0),
-                     d_text.numel(), ctypes.c_void_p(out.data_ptr() if out is not None else 0), cap,
-                     ctypes.c_void_p(count.data_ptr()), _stream_handle(stream)))
+    dev = _dev_index(d_text)
+    with torch.cuda.device(dev):
+        ctx = context(dev)
+        cap = 0 if out is None else out.numel()
+        _check(L.mb_find(ctx.handle, plan.handle, ctypes.c_void_p(d_text.data_ptr() if d_text.numel() else 0),
+                         d_text.numel(), ctypes.c_void_p(out.data_ptr() if out is not None else 0), cap,
+                         ctypes.c_void_p(count.data_ptr()), _stream_handle(stream, dev)))
 
 
 def find(plan: Plan, text, stream=None):
@@ -336,16 +369,19 @@ def find(plan: Plan, text, stream=None):
     import torch
 
     d_text = to_device_text(text)
-    count = torch.zeros(1, dtype=torch.int64, device=d_text.device)
+    dev = d_text.device
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
     buf = _outbuf()
-    out = buf.get(1 << 16)
+    out = buf.get(1 << 16, dev)
     find_into(plan, d_text, out, count, stream)
+    _wait(stream, dev)
     c = int(count.item())
     if c > out.numel():
-        out = buf.get(c)
+        out = buf.get(c, dev)
         find_into(plan, d_text, out, count, stream)
+        _wait(stream, dev)
         c = int(count.item())
-    return out[:c].clone()
+    return _take(out, c, stream, dev)
 
 
 def count(plan: Plan, text, stream=None) -> int:
@@ -354,6 +390,7 @@ def count(plan: Plan, text, stream=None) -> int:
     d_text = to_device_text(text)
     cnt = torch.zeros(1, dtype=torch.int64, device=d_text.device)
     find_into(plan, d_text, None, cnt, stream)
+    _wait(stream, d_text.device)
     return int(cnt.item())
 
 
@@ -381,20 +418,23 @@ class Batch:
 
 
 def find_batch_into(plans, d_text, out, offsets, stream=None):
+    import torch
+
     L = load_library()
-    ctx = context()
-    if isinstance(plans, Batch):
+    dev = _dev_index(d_text)
+    with torch.cuda.device(dev):
+        ctx = context(dev)
         cap = 0 if out is None else out.numel()
-        _check(L.mb_find_batch_prepared(ctx.handle, plans._h, ctypes.c_void_p(d_text.data_ptr() if d_text.numel() else 0),
-                                        d_text.numel(), ctypes.c_void_p(out.data_ptr() if out is not None else 0), cap,
-                                        ctypes.c_void_p(offsets.data_ptr()), _stream_handle(stream)))
-        return
-    K = len(plans)
-    arr = (ctypes.c_void_p * K)(*[p.handle.value for p in plans])
-    cap = 0 if out is None else out.numel()
-    _check(L.mb_find_batch(ctx.handle, arr, K, ctypes.c_void_p(d_text.data_ptr() if d_text.numel() else 0),
-                           d_text.numel(), ctypes.c_void_p(out.data_ptr() if out is not None else 0), cap,
-                           ctypes.c_void_p(offsets.data_ptr()), _stream_handle(stream)))
+        tp = ctypes.c_void_p(d_text.data_ptr() if d_text.numel() else 0)
+        op = ctypes.c_void_p(out.data_ptr() if out is not None else 0)
+        if isinstance(plans, Batch):
+            _check(L.mb_find_batch_prepared(ctx.handle, plans._h, tp, d_text.numel(), op, cap,
+                                            ctypes.c_void_p(offsets.data_ptr()), _stream_handle(stream, dev)))
+            return
+        K = len(plans)
+        arr = (ctypes.c_void_p * K)(*[p.handle.value for p in plans])
+        _check(L.mb_find_batch(ctx.handle, arr, K, tp, d_text.numel(), op, cap,
+                               ctypes.c_void_p(offsets.data_ptr()), _stream_handle(stream, dev)))
 
 
 def find_batch(plans, text, stream=None):
@@ -403,18 +443,21 @@ def find_batch(plans, text, stream=None):
     import torch
 
     d_text = to_device_text(text)
+    dev = d_text.device
     K = len(plans)
-    offsets = torch.zeros(K + 1, dtype=torch.int64, device=d_text.device)
+    offsets = torch.zeros(K + 1, dtype=torch.int64, device=dev)
     buf = _outbuf()
-    out = buf.get(1 << 16)
+    out = buf.get(1 << 16, dev)
     find_batch_into(plans, d_text, out, offsets, stream)
+    _wait(stream, dev)
     offs = offsets.cpu()
     total = int(offs[-1])
     if total > out.numel():
-        out = buf.get(total)
+        out = buf.get(total, dev)
         find_batch_into(plans, d_text, out, offsets, stream)
+        _wait(stream, dev)
         offs = offsets.cpu()
-    return out[:total].clone(), offs
+    return _take(out, total, stream, dev), offs
 
 
 def histogram(text, stream=None):
@@ -422,9 +465,14 @@ def histogram(text, stream=None):
     import torch
 
     d_text = to_device_text(text)
-    hist = torch.zeros(256, dtype=torch.int64, device=d_text.device)
-    _check(load_library().mb_histogram(context().handle, ctypes.c_void_p(d_text.data_ptr() if d_text.numel() else 0),
-                                       d_text.numel(), ctypes.c_void_p(hist.data_ptr()), _stream_handle(stream)))
+    dev = _dev_index(d_text)
+    with torch.cuda.device(dev):
+        hist = torch.zeros(256, dtype=torch.int64, device=d_text.device)
+        _check(load_library().mb_histogram(context(dev).handle,
+                                           ctypes.c_void_p(d_text.data_ptr() if d_text.numel() else 0),
+                                           d_text.numel(), ctypes.c_void_p(hist.data_ptr()),
+                                           _stream_handle(stream, dev)))
+    _wait(stream, d_text.device)
     return hist
 
 

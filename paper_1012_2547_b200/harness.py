@@ -12,7 +12,9 @@ is rejected).
 from __future__ import annotations
 
 import statistics
+import warnings
 from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
 
@@ -102,6 +104,34 @@ def standard_texts(cfg: BenchConfig, sigmas=ALLOWED_SIGMAS) -> list[Text]:
     return [generate_rand_text(s, cfg.text_size, derive_seed(cfg.seed, "rand", s)) for s in sigmas]
 
 
+#: bench.py:104-109 -- (bytes, approximate distinct symbols) of the paper's corpora
+CORPUS_EXPECTATIONS = {
+    "ecoli": (4_638_690, 4),
+    "bible": (4_047_392, 63),
+    "world192": (2_473_400, 94),
+    "hs": (3_295_751, 20),
+}
+
+
+def load_corpus(path, expected_id: str | None = None) -> Text:
+    """bench.py:112-138: a corpus file as raw bytes.  For the known corpus ids
+    a length or alphabet that differs from the expectation only warns (corpus
+    editions vary); sigma is counted on the device (K0 histogram)."""
+    path = Path(path)
+    data = path.read_bytes()
+    text = Text(data, expected_id or path.stem)
+    exp = CORPUS_EXPECTATIONS.get(text.id)
+    if exp is not None:
+        exp_n, exp_sigma = exp
+        if len(data) != exp_n:
+            warnings.warn(f"corpus {text.id!r}: expected n={exp_n:,} bytes, got {len(data):,} (different edition?)",
+                          stacklevel=2)
+        sigma = text.alphabet_size()
+        if abs(sigma - exp_sigma) > 2:
+            warnings.warn(f"corpus {text.id!r}: expected sigma~{exp_sigma}, got {sigma}", stacklevel=2)
+    return text
+
+
 def run_benchmark(cfg: BenchConfig, texts, algos=None, parallel: bool = False) -> list[Measurement]:
     """bench.py:204-238 cells, each search timed on the GPU (compile untimed, one
     warm-up, CUDA events around the search, mean/pstdev over the patterns)."""
@@ -124,6 +154,7 @@ def run_benchmark(cfg: BenchConfig, texts, algos=None, parallel: bool = False) -
     return out
 
 
-__all__ = ["ALLOWED_SIGMAS", "DEFAULT_LENGTHS", "PRNG_NAME", "BenchConfig", "Measurement", "derive_seed",
+__all__ = ["ALLOWED_SIGMAS", "CORPUS_EXPECTATIONS", "DEFAULT_LENGTHS", "PRNG_NAME", "BenchConfig", "Measurement",
+           "derive_seed", "load_corpus",
            "generate_rand_text", "run_benchmark", "sample_patterns", "sample_positions", "standard_texts",
            "state_word_count"]

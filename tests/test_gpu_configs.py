@@ -7,6 +7,8 @@ occurrences present, batched == single-pattern results.
 """
 from __future__ import annotations
 
+import hashlib
+import json
 import os
 
 import numpy as np
@@ -39,43 +41,70 @@ def test_config1_full(cuda):
     props(got, pats[0], t)
 
 
+def _digests():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cfg23_digests.json")) as f:
+        return json.load(f)
+
+
+def digest(pos: np.ndarray) -> str:
+    return hashlib.sha1(np.ascontiguousarray(pos, dtype="<i8").tobytes()).hexdigest()[:16]
+
+
+def check_every_list(pos: np.ndarray, offs: np.ndarray, want: list, tag) -> None:
+    """Every pattern's CSR slice: count and digest of all positions
+    (tests/golden/make_cfg23_digests.py, C oracle brute force)."""
+    assert offs.size == len(want) + 1 and offs[0] == 0
+    bad = []
+    for k, (cnt, dg) in enumerate(want):
+        got = pos[offs[k] : offs[k + 1]]
+        if got.size != cnt or digest(got) != dg:
+            bad.append((k, got.size, cnt))
+    assert not bad, (tag, f"{len(bad)} of {len(want)} lists differ", bad[:5])
+
+
 @pytest.mark.parametrize("sigma", [2, 4, 8, 16, 32, 64, 128])
 def test_config2_full_sigma(cuda, sigma):
-    """All 10 m x 500 patterns of one sigma: one batched launch per m; exact per pattern."""
+    """All 10 m x 500 patterns of one sigma: one batched launch per m; EVERY
+    pattern's full position list against its oracle digest; single-pattern
+    searches for a spread of patterns."""
+    gold = _digests()
     t = inputs.config2_text(sigma)
+    assert hashlib.sha1(t.tobytes()).hexdigest()[:16] == gold["texts"][f"cfg2_{sigma}"], "text generator drifted"
     d = torch.from_numpy(t).cuda()
     for m in inputs.DEFAULT_LENGTHS:
         pats = inputs.config2_patterns(t, sigma, m)
-        pos, offs = engine.find_batch([engine.Plan(p) for p in pats], d)
+        want = gold["cfg2"][str(sigma)][str(m)]
+        batch = engine.Batch([engine.Plan(p) for p in pats])
+        pos, offs = engine.find_batch(batch, d)
         pos = pos.cpu().numpy()
         offs = offs.numpy()
-        want_counts = [oracle.count(p, t, threads=THREADS) for p in pats]
-        assert np.array_equal(np.diff(offs), want_counts), (sigma, m)
-        for k in range(0, len(pats), 97):  # full position check on a spread of patterns
-            assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(pats[k], t, threads=THREADS))
+        check_every_list(pos, offs, want, (sigma, m, "batched"))
         for k in range(0, len(pats), 50):
             props(pos[offs[k] : offs[k + 1]], pats[k], t)
+        for k in range(3, len(pats), 61):  # single-pattern path on a spread
+            got = engine.find(engine.Plan(pats[k]), d).cpu().numpy()
+            assert got.size == want[k][0] and digest(got) == want[k][1], (sigma, m, k, "single")
 
 
 def test_config3_full(cuda):
+    gold = _digests()
     t = inputs.config3()
+    assert hashlib.sha1(t.tobytes()).hexdigest()[:16] == gold["texts"]["cfg3"], "text generator drifted"
     d = torch.from_numpy(t).cuda()
     for m in (4, 16, 64, 256, 1024):
         pats = inputs.config3_patterns(t, m)
+        want = gold["cfg3"][str(m)]
         before = engine.mp_batches()
         pos, offs = engine.find_batch([engine.Plan(p) for p in pats], d)
         if m in (16, 64, 256, 1024):
             assert engine.mp_batches() == before + 1, f"cfg3 m={m} batch did not take the MP pass"
         pos = pos.cpu().numpy()
         offs = offs.numpy()
-        for k in range(len(pats)):
-            want = oracle.search(pats[k], t, threads=THREADS) if k % 25 == 0 else None
-            got = pos[offs[k] : offs[k + 1]]
-            if want is not None:
-                assert np.array_equal(got, want), (m, k)
-            else:
-                assert got.size == oracle.count(pats[k], t, threads=THREADS), (m, k)
+        check_every_list(pos, offs, want, (m, "batched"))
         props(pos[offs[0] : offs[1]], pats[0], t)
+        for k in range(7, len(pats), 49):
+            got = engine.find(engine.Plan(pats[k]), d).cpu().numpy()
+            assert got.size == want[k][0] and digest(got) == want[k][1], (m, k, "single")
 
 
 def test_config5_full(cuda):

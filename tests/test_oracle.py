@@ -151,3 +151,56 @@ def test_threaded_chunking_matches_single():
         p = rng.integers(0, sigma, m, dtype=np.uint8).tobytes()
         k = int(rng.integers(2, 17))
         assert oracle.search(p, t, threads=k).tolist() == oracle.search(p, t).tolist()
+
+
+# The algorithms the CPU legs of bench.py time (the reference's auto path on
+# configs 3-5: FJS, EBOM, SSEF, LBNDM -- registry.py:209-222) and the other
+# restated searchers, each against the reference-generated digests of every
+# fuzz and differential case inside its applicability bounds.
+BOUNDS = {"SSEF": (32, None), "EBOM": (2, None), "FSBNDM": (1, 63), "HASH3": (3, None), "HASH5": (5, None),
+          "HASH8": (8, None)}
+
+
+@pytest.mark.parametrize("algo", [a for a in ALL if a != "BF"])
+def test_fuzz_and_differential_golden_per_algorithm(algo):
+    lo, hi = BOUNDS.get(algo, (1, None))
+    ran = 0
+    for fx in load("fuzz.json"):
+        prm = fx["params"]
+        kw = {k: v for k, v in prm.items() if k not in ("seed", "count", "m_lo", "m_hi")}
+        if "sigmas" in kw:
+            kw["sigmas"] = tuple(kw["sigmas"])
+        for (p, t), (m, n, cd, cnt, dg) in zip(fuzz_cases(prm["seed"], prm["count"], prm["m_lo"], prm["m_hi"], **kw),
+                                                fx["cases"]):
+            if m < lo or (hi is not None and m > hi):
+                continue
+            r = oracle.search(p, t, algo)
+            assert (r.size, digest(r)) == (cnt, dg), (algo, "fuzz", prm["seed"], m, n)
+            ran += 1
+    fx = load("differential.json")
+    for aid, row in fx["algos"].items():
+        for i, (sigma, n, m, kind, cnt, dg) in enumerate(row["cases"][::4]):
+            if m < lo or (hi is not None and m > hi) or (m > 256 and algo in ("HOR", "QS", "BR", "TVSBS", "BOM")):
+                continue
+            _, _, _, _, p, t = make_diff_case(row["m_min"], row["m_max"], derive_seed(fx["seed"], aid, 4 * i))
+            r = oracle.search(p, t, algo)
+            assert (r.size, digest(r)) == (cnt, dg), (algo, "differential", aid, 4 * i)
+            ran += 1
+    assert ran >= 500, ran
+
+
+def test_cfg23_digests_spot_check():
+    """A seeded sample of the 37,500 config-2/3 list digests re-derived here
+    (the full set is checked on the GPU in tests/test_gpu_configs.py)."""
+    fx = load("cfg23_digests.json")
+    rng = np.random.default_rng(23)
+    for sigma in (2, 16, 128):
+        t = inputs.config2_text(sigma)
+        assert tdigest(t.tobytes()) == fx["texts"][f"cfg2_{sigma}"]
+        for m in rng.choice(inputs.DEFAULT_LENGTHS, 3, replace=False):
+            pats = inputs.config2_patterns(t, sigma, int(m))
+            for k in rng.integers(0, 500, 2):
+                r = oracle.search(pats[k], t, threads=4)
+                assert [r.size, digest(r)] == fx["cfg2"][str(sigma)][str(m)][k], (sigma, m, k)
+    assert sum(len(v) for c in fx["cfg2"].values() for v in c.values()) == 35000
+    assert sum(len(v) for v in fx["cfg3"].values()) == 2500
