@@ -365,19 +365,38 @@ static cudaError_t occupancy(const void* fn, int threads, size_t smem, int* out)
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // before its predecessor in the stream completes and must call pdl_wait()
 // before touching the predecessor's results.
-template <class K>
-static cudaError_t launch_pdl(K kernel, int grid, int block, cudaStream_t st, const ScanParams& P) {
+// coop: the kernel passes a grid barrier (offsets_kernel's resident mode, the
+// batch pass prologue) -- a cooperative launch makes the driver schedule the
+// whole grid at once, so two contexts (host threads, streams) running such
+// kernels concurrently cannot each hold part of the GPU and spin forever; a
+// grid that could not be co-resident fails the launch instead of hanging.
+template <class K, class PT>
+static cudaError_t launch_ex(K kernel, int grid, int block, size_t smem, cudaStream_t st, const PT& P, bool pdl,
+                             bool coop) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3((unsigned)block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    na++;
+  }
+  if (coop) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    na++;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kernel, P);
+}
+template <class K>
+static cudaError_t launch_pdl(K kernel, int grid, int block, cudaStream_t st, const ScanParams& P, bool coop = false) {
+  return launch_ex(kernel, grid, block, 0, st, P, true, coop);
 }
 
 // ---- pinned upload staging (see mb_ctx::stage)
@@ -954,12 +973,13 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     // chunk = NT * scan_per counts; the largest chunks run as 256-thread CTAs
     // x 64 counts (4 CTAs per SM, so 16 GiB's 512 chunks stay co-resident)
     P.offs_resident = nchunks <= (int64_t)c->nsm * (scan_per == 32 ? 4 : 2) ? 1 : 0;  // __launch_bounds__
+    const bool coop = P.offs_resident != 0;  // grid barrier: cooperative launch (see launch_ex)
     if (scan_per == 32)
-      CUDA_TRY(launch_pdl(offsets_kernel<64, NT / 2>, (int)nchunks, NT / 2, st, P));
+      CUDA_TRY(launch_pdl(offsets_kernel<64, NT / 2>, (int)nchunks, NT / 2, st, P, coop));
     else if (scan_per == 16)
-      CUDA_TRY(launch_pdl(offsets_kernel<16, NT>, (int)nchunks, NT, st, P));
+      CUDA_TRY(launch_pdl(offsets_kernel<16, NT>, (int)nchunks, NT, st, P, coop));
     else
-      CUDA_TRY(launch_pdl(offsets_kernel<8, NT>, (int)nchunks, NT, st, P));
+      CUDA_TRY(launch_pdl(offsets_kernel<8, NT>, (int)nchunks, NT, st, P, coop));
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     if (d_out && cap > 0) {
@@ -1053,18 +1073,22 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       }
       if (per_sm < 1) return fail(MB_ECUDA, "batched pass kernel does not fit on an SM");
       const int grid = (int)std::min<int64_t>(M.ntiles_text, (int64_t)c->nsm * per_sm);
+      // the first launch's prologue ends in a grid barrier: cooperative (see launch_ex)
+      const bool coop = M.zero_n > 0;
+      cudaError_t le;
       if (bp->kind == 1)
-        mp_scan_kernel<<<grid, NT + 32, smem, st>>>(M);
+        le = launch_ex(mp_scan_kernel, grid, NT + 32, smem, st, M, false, coop);
       else if (bp->q == 16)
-        mpb_scan_kernel<16><<<grid, NT + 32, smem, st>>>(M);
+        le = launch_ex(mpb_scan_kernel<16>, grid, NT + 32, smem, st, M, false, coop);
       else if (bp->q == 8)
-        mpb_scan_kernel<8><<<grid, NT + 32, smem, st>>>(M);
+        le = launch_ex(mpb_scan_kernel<8>, grid, NT + 32, smem, st, M, false, coop);
       else if (bp->q == 4)
-        mpb_scan_kernel<4><<<grid, NT + 32, smem, st>>>(M);
+        le = launch_ex(mpb_scan_kernel<4>, grid, NT + 32, smem, st, M, false, coop);
       else if (bp->q == 3)
-        mpb_scan_kernel<3><<<grid, NT + 32, smem, st>>>(M);
+        le = launch_ex(mpb_scan_kernel<3>, grid, NT + 32, smem, st, M, false, coop);
       else
-        mpb_scan_kernel<2><<<grid, NT + 32, smem, st>>>(M);
+        le = launch_ex(mpb_scan_kernel<2>, grid, NT + 32, smem, st, M, false, coop);
+      CUDA_TRY(le);
       g_launches++;
       CUDA_TRY(cudaGetLastError());
     }

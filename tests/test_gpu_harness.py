@@ -137,7 +137,7 @@ def test_reference_cli_search_resolves_b200(cuda, ref, tmp_path, capsys, monkeyp
 
 def test_integration_md_ctypes_snippet(cuda):
     md = open(os.path.join(ROOT, "INTEGRATION.md")).read()
-    block = re.search(r"```python\n(.*?)```", md, re.S).group(1)
+    block = next(b for b in re.findall(r"```python\n(.*?)```", md, re.S) if "def compile_b200" in b)
     block = block.replace('ctypes.CDLL("libmatchb200.so")', f"ctypes.CDLL({engine.LIB_PATH!r})")
     ns: dict = {}
     exec(compile(block, "INTEGRATION.md", "exec"), ns)

@@ -540,3 +540,40 @@ def test_batch_duplicate_patterns(cuda, sigma, m, monkeypatch):
     monkeypatch.setenv("MB_SCRATCH_BUDGET", str(3_000_000))  # sub-batches of a few patterns
     res = mb.search_many(pats, t)
     assert all(r == want[p] for r, p in zip(res, pats))
+
+
+def test_batch_every_family_key_with_pass(cuda):
+    """All 16 family keys of engine.cu family_key (SWAR m = 1,2,3,5..8, WIN4,
+    even-window WIN4, ALIGNED 1/2/3 words, the c^m run filter, sampled,
+    shift-or 32/64) in ONE batch together with enough sparse long patterns for
+    a batch pass -- every key then launches twice (ungated, and gated behind
+    the pass's overflow flag): 32 count-kernel groups, the ticket-slot limit."""
+    rng = np.random.default_rng(405)
+    n = 6 * ENGINE_TILE + 777
+    t = bytearray(rand_bytes(rng, 256, n))
+    tb = rand_bytes(rng, 2, 8192)
+    t[20000:20000 + len(tb)] = tb
+    t[40000:40300] = b"\x07" * 300
+    t = bytes(t)
+    specs = [(t[100:101], "auto", 0), (t[200:202], "auto", 0), (t[300:303], "auto", 0),
+             (t[400:404], "auto", 0), (t[450:455], "auto", 0)]
+    specs += [(tb[i * 40: i * 40 + m], "swar", 0) for i, m in enumerate((5, 6, 7, 8), 1)]
+    specs += [(t[500:524], "auto", 1), (tb[300:340], "auto", 2), (tb[400:460], "auto", 3),
+              (b"\x07" * 20, "auto", 0), (t[60000:60700], "auto", 0),
+              (t[2000:2020], "shiftor", 0), (t[3000:3050], "shiftor", 0)]
+    plans = [engine.Plan(p, fam, anchor_words=nw) for p, fam, nw in specs]
+    infos = [pl.info() for pl in plans]
+    keys = {(i.family, i.m if i.family == "swar" else i.words, i.m <= 32 if i.family == "shiftor" else None,
+             i.periodic and i.period == 1 if i.family == "aligned" else i.m == 4 if i.family == "win4" else None)
+            for i in infos}
+    assert len(keys) == 16, keys
+    # sparse m >= 7 patterns for the aligned-word batch pass (the short ones make it byte-offset)
+    sparse = [t[i : i + 32] for i in rng.integers(70000, n - 40, 40)]
+    mp0 = engine.mp_batches()
+    for obj in (plans + [engine.Plan(p) for p in sparse], [engine.Plan(p) for p in sparse] + plans * 2):
+        for b in (obj, engine.Batch(obj)):
+            pos, offs = engine.find_batch(b, t)
+            pos = pos.cpu().numpy()
+            for k, pl in enumerate(obj):
+                assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(pl.pattern, t)), (k, pl.m)
+    assert engine.mp_batches() > mp0, "no batch pass: the gated groups were not exercised"
