@@ -47,6 +47,7 @@ extern "C" {
 #define MB_FAM_ALIGNED 3 /* K1/K3, m >= 7: aligned-word q-gram anchor + smem verify */
 #define MB_FAM_SHIFTOR 4 /* K2, m <= 64: per-thread bit-parallel shift-or */
 #define MB_FAM_SAMPLED 5 /* K3, m >= 272: sampled q-gram hash filter, sublinear DRAM reads */
+#define MB_FAM_GRAM 6    /* K1G, m >= 15: strided q-gram bloom filter over the staged tile (small alphabets) */
 
 typedef struct mb_plan mb_plan;
 typedef struct mb_ctx mb_ctx;
@@ -65,8 +66,8 @@ typedef struct {
   int delta;      /* bitmap index shift: bit b <-> position b - delta */
   int period;     /* smallest period of the pattern (== m if aperiodic) */
   int periodic;   /* 1 if verification uses the period/break-run test */
-  int stride;     /* K3 sampling stride S in bytes (0 unless family == MB_FAM_SAMPLED) */
-  int gram;       /* K3 gram length q in bytes (0 unless family == MB_FAM_SAMPLED) */
+  int stride;     /* sampling stride S in bytes (K3 SAMPLED, K1G GRAM; else 0) */
+  int gram;       /* gram length q in bytes (K3 SAMPLED, K1G GRAM; else 0) */
   int words;      /* ALIGNED anchor words (window 4 words + 3 bytes; 0 for other families) */
 } mb_plan_info_t;
 

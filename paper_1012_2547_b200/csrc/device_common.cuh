@@ -303,6 +303,45 @@ struct FiltSO {
   static constexpr bool kShiftOr = true;
   static constexpr int kW = W;
 };
+__device__ __forceinline__ uint32_t lds32u(const uint8_t* p);
+// K1G / m >= Q + S - 1, small alphabets (plan.cpp choose_gram): the Q-byte gram
+// at every S-th staged position x (S-aligned, S = 8 or 16) is hashed once and
+// tested against the warp's blocked bloom of the pattern grams p[j..j+Q),
+// j in [0, S) (gram_bloom_hash, 2 bits in one smem word); a bloom hit compares
+// the gram with the S pattern grams in the staged pattern and marks bit
+// x + S - 1 - j (delta = S - 1) for each equal one.  ~10 instructions per 16
+// text bytes for S = 16 against ALIGNED's 32-48 compares at 2-3 anchor words.
+template <int S, int Q>
+struct FiltGRAM {
+  static constexpr bool kGram = true;
+  static constexpr int kS = S, kQ = Q;
+  static_assert((S == 8 || S == 16) && (Q == 8 || Q == 16), "K1G variants");
+};
+template <class F, class = void>
+struct is_gram : std::false_type {};
+template <class F>
+struct is_gram<F, std::void_t<decltype(F::kGram)>> : std::true_type {};
+
+// w[0..5]: the lane's 16 staged bytes at x0 and the next 8; tab: the warp's
+// GRAM_TABLE_WORDS (smem): bloom, then the S pattern gram hashes.  A bloom hit
+// marks the offsets j whose gram hash equals the sample's (verified later).
+template <int S, int Q>
+__device__ __forceinline__ uint32_t gram_mask(const uint32_t* w, const uint32_t* tab) {
+  uint32_t mk = 0;
+#pragma unroll
+  for (int t = 0; t < 16 / S; t++) {
+    const uint32_t* g = w + t * (S / 4);
+    const uint32_t h = gram_bloom_hash(g, Q / 4);
+    const uint32_t bits = gram_bloom_bits(h);
+    if ((tab[h >> 25] & bits) == bits) {  // rare
+#pragma unroll
+      for (int j = 0; j < S; j++)
+        if (tab[GRAM_BLOOM_WORDS + j] == h) mk |= 1u << (t * S + S - 1 - j);
+    }
+  }
+  return mk;
+}
+
 template <class F, class = void>
 struct always_exact : std::false_type {};
 template <class F>

@@ -245,8 +245,9 @@ int mb_plan_info(const mb_plan* p, mb_plan_info_t* info) {
   info->delta = p->h.dev.delta;
   info->period = p->h.period;
   info->periodic = p->h.dev.periodic;
-  info->stride = p->h.family == MB_FAM_SAMPLED ? p->h.dev.S : 0;
-  info->gram = p->h.family == MB_FAM_SAMPLED ? p->h.dev.q : 0;
+  const bool strided = p->h.family == MB_FAM_SAMPLED || p->h.family == MB_FAM_GRAM;
+  info->stride = strided ? p->h.dev.S : 0;
+  info->gram = strided ? p->h.dev.q : 0;
   info->words = p->h.family == MB_FAM_ALIGNED ? p->h.dev.nw : 0;
   return MB_OK;
 }
@@ -539,7 +540,8 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
   } else {
     auto smem_for = [&](int ns) {
       return (size_t)SM_STAGES + (size_t)ns * P.stage_bytes + NWARP * SEG_WORDS * 4 +
-             (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * 256 * 8 : 0);
+             (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * 256 * 8 : 0) +
+             (is_gram<F>::value ? NWARP * GRAM_TABLE_WORDS * 4 : 0);
     };
     if (fused && *fused) {
       // one stage: each CTA stages exactly one tile
@@ -584,6 +586,7 @@ static int family_key(const PatDev& d) {
   if (d.family == MB_FAM_SHIFTOR) return d.m <= 32 ? 20 : 21;
   if (d.family == MB_FAM_ALIGNED) return d.nw == 1 && d.periodic && d.per == 1 ? 40 : 30 + d.nw;
   if (d.family == MB_FAM_WIN4 && d.nw == 2) return 50;  // even-offset windows
+  if (d.family == MB_FAM_GRAM) return 60 + (d.S == 16 ? 2 : 0) + (d.q == 16 ? 1 : 0);
   return d.family;
 }
 
@@ -611,6 +614,11 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
       if (d.periodic && d.per == 1) return launch_group<FiltALIGNED<1, true>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
       return launch_group<FiltALIGNED<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     case MB_FAM_SAMPLED: return launch_group<SampledTag>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+    case MB_FAM_GRAM:
+      if (d.S == 16 && d.q == 8) return launch_group<FiltGRAM<16, 8>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      if (d.S == 16) return launch_group<FiltGRAM<16, 16>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      if (d.q == 8) return launch_group<FiltGRAM<8, 8>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      return launch_group<FiltGRAM<8, 16>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
     case MB_FAM_SHIFTOR: {
       int64_t maxm = 0;
       for (int i = 0; i < gk; i++) maxm = std::max<int64_t>(maxm, h_pats[h_idx[i]].m);

@@ -79,6 +79,10 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   uint64_t* so_s = reinterpret_cast<uint64_t*>(stages + NS * P.stage_bytes + NWARP * SEG_WORDS * 4 +
                                                NWARP * 2 * (P.brk_words + 4) * 4) +
                    warp * 256;  // K2 only: per-warp shift-or masks
+  uint32_t* gbl = reinterpret_cast<uint32_t*>(stages + NS * P.stage_bytes + NWARP * SEG_WORDS * 4 +
+                                              NWARP * 2 * (P.brk_words + 4) * 4) +
+                  warp * GRAM_TABLE_WORDS;  // K1G only: per-warp gram bloom + hashes (same region as K2's masks)
+  (void)gbl;
 
   if (tid == 0) {
     for (int s = 0; s < NS; s++) {
@@ -159,6 +163,11 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
         for (int i = lane; i < 256; i += 32) so_s[i] = pd.so_masks[i];
         __syncwarp();
       }
+      if constexpr (is_gram<Filt>::value) {  // this warp's copy of the pattern's gram bloom
+        __syncwarp();
+        for (int i = lane; i < GRAM_TABLE_WORDS; i += 32) gbl[i] = pd.bloom[i];
+        __syncwarp();
+      }
     }
     const int64_t B0 = hdr[s].tau * TILE;
     const uint8_t* spat = stages + s * P.stage_bytes;
@@ -196,7 +205,9 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
         const uint4 X = *reinterpret_cast<const uint4*>(S + c);
         const uint2 Y = *reinterpret_cast<const uint2*>(S + c + 16);
         const uint32_t w[6] = {X.x, X.y, X.z, X.w, Y.x, Y.y};
-        if constexpr (has_direct<Filt>::value)
+        if constexpr (is_gram<Filt>::value)
+          mk[r] = gram_mask<Filt::kS, Filt::kQ>(w, gbl);
+        else if constexpr (has_direct<Filt>::value)
           mk[r] = busy ? Filt::run_direct(w, pd) : Filt::run(w, pd);
         else
           mk[r] = Filt::run(w, pd);

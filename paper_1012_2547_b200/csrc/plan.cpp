@@ -204,6 +204,56 @@ static int best_win4(const uint8_t* p, int64_t m, const double* pr, double* rate
   return best;
 }
 
+// K1G strided q-gram filter: every occurrence s holds exactly one S-aligned
+// virtual position x in [s, s + S), and p[x - s .. x - s + Q) lies inside the
+// pattern when m >= Q + S - 1.  Variants (S, Q) in order of filter cost; the
+// first whose expected true gram hits per 16 text bytes stay below
+// GRAM_QUIET_RATE (a hit sends the warp's whole segment down the slow path,
+// and a tile's stage is freed only when its slowest warp is done) is taken;
+// failing that, the most selective one under GRAM_MAX_RATE or under the
+// ALIGNED filter's own candidate rate (the same selectivity for a third of
+// the instructions).
+#ifndef MB_GRAM_QUIET_RATE
+#define MB_GRAM_QUIET_RATE 2e-5
+#endif
+#ifndef MB_GRAM_MAX_RATE
+#define MB_GRAM_MAX_RATE 1e-3
+#endif
+static bool choose_gram(const uint8_t* p, int64_t m, const double* pr, double aligned_rate16, int* S_out,
+                        int* Q_out) {
+  static const int variants[4][2] = {{16, 8}, {16, 16}, {8, 8}, {8, 16}};
+  double best = 1e300;
+  for (int pass = 0; pass < 2; pass++)
+    for (const auto& v : variants) {
+      const int S = v[0], Q = v[1];
+      if (m < Q + S - 1) continue;
+      double r = 0;
+      for (int j = 0; j < S; j++) {
+        double g = 1;
+        for (int i = 0; i < Q; i++) g *= pr[p[j + i]];
+        r += g;
+      }
+      r *= 16.0 / S;  // per 16 text bytes
+      if (pass == 0 && r <= MB_GRAM_QUIET_RATE) {
+        *S_out = S, *Q_out = Q;
+        return true;
+      }
+      if (pass == 1 && r <= std::max(MB_GRAM_MAX_RATE, 2 * aligned_rate16) && r < best * (1 - 1e-9))
+        best = r, *S_out = S, *Q_out = Q;
+    }
+  return best < 1e300;
+}
+static void build_gram_table(const uint8_t* p, int S, int Q, std::vector<uint32_t>* tab) {
+  tab->assign(GRAM_TABLE_WORDS, 0u);
+  for (int j = 0; j < S; j++) {
+    uint32_t g[4] = {0, 0, 0, 0};
+    for (int i = 0; i < Q / 4; i++) g[i] = load_le32(p + j + 4 * i);
+    const uint32_t h = gram_bloom_hash(g, Q / 4);
+    (*tab)[h >> 25] |= gram_bloom_bits(h);
+    (*tab)[GRAM_BLOOM_WORDS + j] = h;
+  }
+}
+
 int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost* ph, std::string* err) {
   if (m < 1) {
     *err = "pattern must have length >= 1";
@@ -285,6 +335,32 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       // wider (costlier) multi-word ones
       const double margin = nw == 1 ? 8.0 : 2.0;
       if (ra > 1e-3 && margin * rw < ra && !(m >= 16 && ph->period <= m / 2)) fam = MB_FAM_WIN4;
+    }
+  }
+  // Small alphabets: the ALIGNED filter needs 2-3 anchor words (8-12 word
+  // compares per text word, ALU-bound at ~0.5 of the HBM roofline); the
+  // strided gram filter hashes one 8- or 16-byte gram per 8-16 text bytes
+  int gram_S = 0, gram_Q = 0;
+  if (auto_long && fam == MB_FAM_ALIGNED && !(m >= 16 && ph->period <= m / 2) &&
+      !(opts && opts->anchor_words)) {
+    double pr[256];
+    byte_probs(pat, m, hist, pr);
+    double r1, rn;
+    best_aligned(pat, m, pr, 1, &r1);  // one-word anchor hits per text word
+    const int nw = choose_aligned_words(pat, m, pr);
+    best_aligned(pat, m, pr, nw, &rn);
+    if ((nw >= 2 || 4 * r1 > 1e-3) && choose_gram(pat, m, pr, 4 * rn, &gram_S, &gram_Q)) fam = MB_FAM_GRAM;
+  }
+  if (opts && opts->family == MB_FAM_GRAM) {
+    double pr[256];
+    byte_probs(pat, m, hist, pr);
+    if (!choose_gram(pat, m, pr, 0.0, &gram_S, &gram_Q)) {
+      if (m < 15) {
+        *err = "gram family needs m >= 15";
+        return MB_EINVAL;
+      }
+      gram_S = 8, gram_Q = 8;
+      if (m >= 23) gram_S = 16;
     }
   }
   if (opts && opts->family == MB_FAM_SAMPLED && !sampled_ok) {
@@ -379,6 +455,17 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       for (int64_t j = 0; j < m; j++) ph->so_masks[pat[j]] &= ~(1ULL << j);
       break;
     }
+    case MB_FAM_GRAM:
+      // as K3: the sample at x covers bits [x, x + S), b = s + S - 1
+      ph->anchor = 0;
+      d.S = gram_S;
+      d.q = gram_Q;
+      d.delta = gram_S - 1;
+      d.exact = 0;
+      build_gram_table(pat, gram_S, gram_Q, &ph->bloom);
+      ph->bstart.clear();
+      ph->bent.clear();
+      break;
     case MB_FAM_SAMPLED:
       // bit b of the sample at x = S*i covers b in [x, x + S): b = s + S - 1
       ph->anchor = 0;

@@ -28,14 +28,14 @@ struct PatDev {
   int32_t pre;      // staged bytes before the tile's first bit (multiple of 16)
   int32_t post;     // staged bytes after the tile's last bit (multiple of 16)
   uint32_t G[12];   // filter words (family specific); ALIGNED: G[4w + j] = p[a+j+4w .. +4)
-  // K3 sampled q-gram filter (family MB_FAM_SAMPLED)
-  int32_t S;        // sampling stride in bytes (multiple of 16, >= 256)
-  int32_t q;        // gram bytes (4, 8, 16 or 32)
+  // K3 sampled q-gram filter (family MB_FAM_SAMPLED); K1G (MB_FAM_GRAM) uses S, q
+  int32_t S;        // sampling stride in bytes (K3: multiple of 16, >= 256; K1G: 8 or 16)
+  int32_t q;        // gram bytes (K3: 4, 8, 16 or 32; K1G: 8 or 16)
   int32_t B;        // log2 of the bucket count
   int32_t nw;       // ALIGNED: anchor words (window 4 nw + 3 bytes), 1..3
   int32_t mpa;      // K5 batched pass: 7-byte anchor window offset (m >= 7), whatever the family
   uint32_t mpG[4];  // K5 grams p[mpa+j .. mpa+j+4), j = 0..3
-  const uint32_t* bloom;   // 65536-bit filter over gram hashes (device)
+  const uint32_t* bloom;   // K3: 65536-bit filter over gram hashes; K1G: GRAM_BLOOM_WORDS words (device)
   const uint16_t* bstart;  // (1 << B) + 1 bucket starts (device)
   const uint16_t* bent;    // S entries: pattern offsets j sorted by bucket (device)
   const uint64_t* so_masks; // K2: 256 complemented shift-or masks (device), bit j clear iff p[j] == c
@@ -56,6 +56,23 @@ __host__ __device__ inline uint32_t gram_mix(const uint32_t* w, int nw) {
   uint32_t h = 0x9E3779B9u;
   for (int i = 0; i < nw; i++) h = (h ^ w[i]) * 0x85EBCA6Bu + (h >> 15);
   return h ^ (h >> 13);
+}
+
+// K1G (MB_FAM_GRAM): strided q-gram bloom filter over the staged tile.  One
+// sample per S bytes (S = 8 or 16, S-aligned virtual positions) hashed once:
+// GRAM_BLOOM_WORDS words per warp in smem, 3 bits per gram inside one word
+// (blocked bloom), filled with the grams p[j..j+Q), j in [0, S); followed by
+// the S gram hashes (GRAM_TABLE_WORDS in all), which resolve a bloom hit to
+// its candidate offsets j by hash equality (the slow path verifies them).
+constexpr int GRAM_BLOOM_WORDS = 128;
+constexpr int GRAM_TABLE_WORDS = GRAM_BLOOM_WORDS + 16;
+__host__ __device__ inline uint32_t gram_bloom_hash(const uint32_t* g, int nw) {
+  uint32_t h = g[0] * 0x9E3779B1u ^ g[1] * 0x85EBCA77u;
+  if (nw == 4) h ^= g[2] * 0xC2B2AE3Du ^ g[3] * 0x27D4EB2Fu;
+  return h;
+}
+__host__ __device__ inline uint32_t gram_bloom_bits(uint32_t h) {
+  return (1u << ((h >> 20) & 31)) | (1u << ((h >> 15) & 31)) | (1u << ((h >> 10) & 31));
 }
 
 struct PlanHost {

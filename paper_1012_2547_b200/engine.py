@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("MB_ENGINE_LIB") or os.path.join(_HERE, "libmatchb200.
 
 MB_OK, MB_EINVAL, MB_ENOMEM, MB_ECUDA, MB_EOVERFLOW = 0, 1, 2, 3, 4
 MB_MAX_M = 8192
-FAMILIES = {"auto": 0, "swar": 1, "win4": 2, "aligned": 3, "shiftor": 4, "sampled": 5}
+FAMILIES = {"auto": 0, "swar": 1, "win4": 2, "aligned": 3, "shiftor": 4, "sampled": 5, "gram": 6}
 FAMILY_NAMES = {v: k for k, v in FAMILIES.items()}
 
 # every symbol include/matchb200.h declares
@@ -144,8 +144,8 @@ class PlanInfo:
     delta: int
     period: int
     periodic: bool
-    stride: int = 0  # K3 sampling stride (bytes)
-    gram: int = 0    # K3 gram length (bytes)
+    stride: int = 0  # K3 / K1G sampling stride (bytes)
+    gram: int = 0    # K3 / K1G gram length (bytes)
     words: int = 0   # ALIGNED anchor words (window 4 * words + 3 bytes)
 
 

@@ -115,7 +115,8 @@ def test_sigma1_and_zero_bytes(cuda):
         check(b"\x00" * m, b"\x00" * 3000 + b"\x01" + b"\x00" * 50)
 
 
-@pytest.mark.parametrize("family,lo,hi", [("win4", 4, 40), ("aligned", 7, 200), ("shiftor", 1, 64), ("swar", 5, 8)])
+@pytest.mark.parametrize("family,lo,hi", [("win4", 4, 40), ("aligned", 7, 200), ("shiftor", 1, 64), ("swar", 5, 8),
+                                          ("gram", 15, 300)])
 def test_forced_families(cuda, family, lo, hi):
     for p, t in fuzz_cases(77, 150, lo, hi, n_max=3000):
         check(p, t, family)
@@ -577,3 +578,50 @@ def test_batch_every_family_key_with_pass(cuda):
             for k, pl in enumerate(obj):
                 assert np.array_equal(pos[offs[k] : offs[k + 1]], oracle.search(pl.pattern, t)), (k, pl.m)
     assert engine.mp_batches() > mp0, "no batch pass: the gated groups were not exercised"
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 8])
+def test_gram_family_small_alphabets(cuda, sigma):
+    """K1G strided gram filter (auto for small alphabets at m >= 15..31): every
+    (S, Q) variant, occurrences planted across tile and segment boundaries, at
+    the text edges, over all 16 pointer misalignments, and dense self-overlapping
+    patterns (forced) whose grams hit at every sample."""
+    rng = np.random.default_rng(500 + sigma)
+    n = 3 * ENGINE_TILE + 999
+    variants = set()
+    for m in (15, 16, 22, 23, 24, 30, 31, 32, 47, 64, 65, 100, 257):
+        t = bytearray(rand_bytes(rng, sigma, n))
+        p = bytes(t[777 : 777 + m])
+        for b in (ENGINE_TILE, 2 * ENGINE_TILE, SEG * 5):
+            for d in (-m - 1, -m + 1, -9, -1, 0, 1, 8, 15):
+                if 0 <= b + d <= n - m:
+                    t[b + d : b + d + m] = p
+        t[:m] = p
+        t[n - m :] = p
+        t = bytes(t)
+        info = engine.Plan(p).info()
+        if info.family == "gram":
+            variants.add((info.stride, info.gram))
+        check(p, t)
+        check(p, t, "gram")
+    if sigma == 2:
+        assert {(8, 16), (16, 16)} <= variants, variants
+    if sigma == 4:
+        assert {(8, 8), (16, 16)} <= variants, variants
+    if sigma == 8:
+        assert {(8, 8), (16, 8)} <= variants, variants
+    base = torch.from_numpy(np.frombuffer(rand_bytes(rng, sigma, 90000 + 64), dtype=np.uint8).copy()).cuda()
+    for off in range(16):
+        view = base[off : off + 90000 - off]
+        host = view.cpu().numpy().tobytes()
+        for m in (15, 23, 31, 40):
+            i = int(rng.integers(0, len(host) - m))
+            p = host[i : i + m]
+            for fam in ("auto", "gram"):
+                got = engine.find(engine.Plan(p, fam), view).cpu().numpy()
+                assert np.array_equal(got, oracle.search(p, host)), (off, m, fam)
+    for unit in (b"ab", b"abc", b"aab", b"abcdefgh"):
+        for m in (15, 24, 40, 100):
+            p = (unit * 64)[:m]
+            t = (unit * (n // len(unit)))[: n - 5] + b"zzzzz"
+            check(p, t, "gram")

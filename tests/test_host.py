@@ -159,18 +159,30 @@ def test_plan_info_families():
     with pytest.raises(ValueError):
         engine.Plan(b"a" * 1024, family="sampled")
     # K2 shift-or is exact and selectable, but auto keeps the faster K1 filter
-    assert engine.Plan(bytes(rng.integers(0, 4, 40, dtype=np.uint8))).info().family == "aligned"
+    assert engine.Plan(bytes(rng.integers(0, 4, 40, dtype=np.uint8))).info().family == "gram"
+    # K1G strided gram filter: small alphabets from m = 15 (S = 8) / 23 (S = 16); sigma >= 16 keeps ALIGNED
+    i4 = engine.Plan(bytes(rng.integers(0, 4, 64, dtype=np.uint8))).info()
+    assert (i4.family, i4.stride, i4.gram, i4.delta) == ("gram", 16, 16, 15)
+    i8 = engine.Plan(bytes(rng.integers(0, 8, 16, dtype=np.uint8))).info()
+    assert (i8.family, i8.stride, i8.gram, i8.delta) == ("gram", 8, 8, 7)
+    assert engine.Plan(bytes(rng.integers(0, 16, 64, dtype=np.uint8))).info().family == "aligned"
+    assert engine.Plan(bytes(rng.integers(0, 4, 12, dtype=np.uint8))).info().family == "aligned"
+    assert engine.Plan(b"ab" * 20).info().family == "aligned"  # periodic: break-run verification
+    assert engine.Plan(bytes(rng.integers(0, 256, 15, dtype=np.uint8)), family="gram").info().family == "gram"
+    with pytest.raises(ValueError):
+        engine.Plan(bytes(14), family="gram")
     assert engine.Plan(bytes(rng.integers(0, 4, 40, dtype=np.uint8)), family="shiftor").info().family == "shiftor"
     with pytest.raises(ValueError):
         engine.Plan(b"x" * 65, family="shiftor")
 
 
 def test_aligned_anchor_words():
-    """Small alphabets widen the ALIGNED anchor to 2 words (11-byte window);
-    large alphabets keep one word; forced values are validated."""
+    """Small alphabets widen the ALIGNED anchor to 2 words (11-byte window)
+    where the strided gram filter does not apply (m < 15..23); large alphabets
+    keep one word; forced values are validated."""
     rng = np.random.default_rng(3)
     for sigma, words in ((2, 2), (4, 2), (64, 1), (256, 1)):
-        p = rng.integers(0, sigma, 64, dtype=np.uint8).tobytes()
+        p = rng.integers(0, sigma, 14 if sigma <= 4 else 64, dtype=np.uint8).tobytes()
         info = engine.Plan(p).info()
         assert (info.family, info.words) == ("aligned", words), sigma
     p = rng.integers(0, 256, 40, dtype=np.uint8).tobytes()

@@ -43,6 +43,9 @@ for sigma in (2, 4, 256):
             check(p, t, "aligned")
         if m <= 64:
             check(p, t, "shiftor")
+        if m >= 15:
+            check(p, t, "gram")
+            check(p, t, "gram", 5)
 dense = bytearray(b"a" * n)
 for i in rng.choice(n, 40, replace=False):
     dense[i] = ord("b")
