@@ -295,14 +295,55 @@ struct FiltALIGNED {
   }
 };
 
-// K2 / 7 <= m <= 64, small alphabets (bitparallel.py:41-63 compile_so): per-lane
-// bit-parallel Shift-Or over a 64-position run of the segment (+ m-1 bytes of
-// look-ahead).  Exact, no verification.  W = 32 or 64 bits of state.
-template <int W>
+// K2 / m <= 64, small alphabets (bitparallel.py:66-84 compile_sa, Shift-And,
+// turned sideways): instead of one state word per text position, the text is
+// packed into NP bit planes -- plane bit i = one chosen bit of text byte i, the
+// bits picked by the planner so that the pattern's symbols get distinct codes
+// (NP = 1 separates 2 symbols, NP = 2 up to 4) -- and every lane runs the
+// bit-parallel AND over its 64 start positions at once:
+//   M = AND_j ~((T >> j) ^ a_j),  a_j = plane bit of p[j], j in [a, a + D)
+// i.e. 2 funnel shifts + 2 LOP3 per pattern position, plane and 64 starts.
+// The planner picks the D <= SO_MAX_STEPS consecutive pattern positions that
+// bring the expected survivors below 2^-16 per start (sigma = 2: 16 steps);
+// survivors are verified like any other filter's candidates (verify_direct),
+// which also rejects text bytes outside the pattern's alphabet (they alias to
+// one of its codes).
+template <int NP>
 struct FiltSO {
   static constexpr bool kShiftOr = true;
-  static constexpr int kW = W;
+  static constexpr int kNP = NP;
+  static_assert(NP == 1 || NP == 2, "one or two symbol bit planes");
 };
+
+// 16 staged bytes -> 16 plane bits (bit i = selected bit of byte i).  Per word:
+// mask the chosen bit of every byte, one IMAD gathers the four flags into the
+// top nibble (mult = (2^28 + 2^21 + 2^14 + 2^7) >> bit: the partial products
+// never overlap), one funnel shift appends it.
+__device__ __forceinline__ uint32_t so_pack16(const uint4& X, uint32_t mask, uint32_t mult) {
+  uint32_t acc = ((X.w & mask) * mult) >> 28;
+  acc = __funnelshift_l((X.z & mask) * mult, acc, 4);
+  acc = __funnelshift_l((X.y & mask) * mult, acc, 4);
+  acc = __funnelshift_l((X.x & mask) * mult, acc, 4);
+  return acc;
+}
+
+// `steps` AND steps over the 96-bit plane windows (a0, a1, a2) [and (b0, b1,
+// b2)] of a lane's 64 starts; tab[k] = {shift, plane-A xor mask, plane-B xor
+// mask, -}, one broadcast LDS.128 per step.
+template <int NP>
+__device__ __forceinline__ void so_and_steps(const uint4* tab, int steps, uint32_t a0, uint32_t a1, uint32_t a2,
+                                             uint32_t b0, uint32_t b1, uint32_t b2, uint32_t& M0, uint32_t& M1) {
+#pragma unroll 4
+  for (int k = 0; k < steps; k++) {
+    const uint4 e = tab[k];
+    M0 &= __funnelshift_r(a0, a1, e.x) ^ e.y;
+    M1 &= __funnelshift_r(a1, a2, e.x) ^ e.y;
+    if constexpr (NP == 2) {
+      M0 &= __funnelshift_r(b0, b1, e.x) ^ e.z;
+      M1 &= __funnelshift_r(b1, b2, e.x) ^ e.z;
+    }
+  }
+}
 __device__ __forceinline__ uint32_t lds32u(const uint8_t* p);
 // K1G / m >= Q + S - 1, small alphabets (plan.cpp choose_gram): the Q-byte gram
 // at every S-th staged position x (S-aligned, S = 8 or 16) is hashed once and
@@ -358,31 +399,6 @@ template <class F, class = void>
 struct is_shiftor : std::false_type {};
 template <class F>
 struct is_shiftor<F, std::void_t<decltype(F::kShiftOr)>> : std::true_type {};
-
-template <int W>
-__device__ __forceinline__ void shiftor_lane(const uint8_t* q, int m, const uint64_t* masks, uint32_t& w0,
-                                             uint32_t& w1) {
-  using T = typename std::conditional<W == 32, uint32_t, uint64_t>::type;
-  T D = ~T(0);
-  uint64_t acc = 0;  // shift register of match bits; after 64 + m - 1 bytes holds positions 0..63
-  const int total = 64 + m - 1;
-  const int hb = m - 1;
-  int y = 0;
-  for (; y + 4 <= total; y += 4) {
-    const uint32_t word = *reinterpret_cast<const uint32_t*>(q + y);
-#pragma unroll
-    for (int b = 0; b < 4; b++) {
-      D = (D << 1) | (T)masks[(word >> (8 * b)) & 0xFFu];
-      acc = (acc >> 1) | ((uint64_t)((~D >> hb) & 1u) << 63);
-    }
-  }
-  for (; y < total; y++) {
-    D = (D << 1) | (T)masks[q[y]];
-    acc = (acc >> 1) | ((uint64_t)((~D >> hb) & 1u) << 63);
-  }
-  w0 = (uint32_t)acc;
-  w1 = (uint32_t)(acc >> 32);
-}
 
 // ------------------------------------------------------------ verification
 // Direct window compare in shared memory (core.py:131-136 match_at), 4 bytes

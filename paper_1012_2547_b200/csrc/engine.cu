@@ -80,8 +80,7 @@ static int plan_device(const mb_plan* p, const PatDev** out) {
   const size_t bloom_bytes = h.bloom.size() * 4;
   const size_t bs_bytes = (h.bstart.size() * 2 + 15) & ~(size_t)15;
   const size_t be_bytes = (h.bent.size() * 2 + 15) & ~(size_t)15;
-  const size_t so_bytes = h.so_masks.size() * 8;
-  const size_t total = pat_bytes + bloom_bytes + bs_bytes + be_bytes + so_bytes;
+  const size_t total = pat_bytes + bloom_bytes + bs_bytes + be_bytes;
   if (cudaMalloc(&p->d_buf, total) != cudaSuccess) return fail(MB_ENOMEM, "plan upload alloc");
   if (cudaMalloc(&p->d_dev, sizeof(PatDev)) != cudaSuccess) {
     cudaFree(p->d_buf);
@@ -93,15 +92,12 @@ static int plan_device(const mb_plan* p, const PatDev** out) {
   if (bloom_bytes) memcpy(img.data() + pat_bytes, h.bloom.data(), bloom_bytes);
   if (!h.bstart.empty()) memcpy(img.data() + pat_bytes + bloom_bytes, h.bstart.data(), h.bstart.size() * 2);
   if (!h.bent.empty()) memcpy(img.data() + pat_bytes + bloom_bytes + bs_bytes, h.bent.data(), h.bent.size() * 2);
-  if (so_bytes) memcpy(img.data() + pat_bytes + bloom_bytes + bs_bytes + be_bytes, h.so_masks.data(), so_bytes);
   CUDA_TRY(cudaMemcpy(p->d_buf, img.data(), total, cudaMemcpyHostToDevice));
   PatDev d = h.dev;
   d.bytes = p->d_buf;
   d.bloom = bloom_bytes ? reinterpret_cast<const uint32_t*>(p->d_buf + pat_bytes) : nullptr;
   d.bstart = bloom_bytes ? reinterpret_cast<const uint16_t*>(p->d_buf + pat_bytes + bloom_bytes) : nullptr;
   d.bent = bloom_bytes ? reinterpret_cast<const uint16_t*>(p->d_buf + pat_bytes + bloom_bytes + bs_bytes) : nullptr;
-  d.so_masks = so_bytes ? reinterpret_cast<const uint64_t*>(p->d_buf + pat_bytes + bloom_bytes + bs_bytes + be_bytes)
-                        : nullptr;
   CUDA_TRY(cudaMemcpy(p->d_dev, &d, sizeof(PatDev), cudaMemcpyHostToDevice));
   p->dview = d;
   p->device = dev;
@@ -540,7 +536,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
   } else {
     auto smem_for = [&](int ns) {
       return (size_t)SM_STAGES + (size_t)ns * P.stage_bytes + NWARP * SEG_WORDS * 4 +
-             (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * 256 * 8 : 0) +
+             (size_t)NWARP * 2 * (P.brk_words + 4) * 4 + (is_shiftor<F>::value ? NWARP * SO_WARP_WORDS * 4 : 0) +
              (is_gram<F>::value ? NWARP * GRAM_TABLE_WORDS * 4 : 0);
     };
     if (fused && *fused) {
@@ -583,7 +579,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
 // family key: patterns sharing a key share one count-kernel launch
 static int family_key(const PatDev& d) {
   if (d.family == MB_FAM_SWAR) return (int)(10 + d.m);
-  if (d.family == MB_FAM_SHIFTOR) return d.m <= 32 ? 20 : 21;
+  if (d.family == MB_FAM_SHIFTOR) return 19 + d.nw;  // one or two symbol planes
   if (d.family == MB_FAM_ALIGNED) return d.nw == 1 && d.periodic && d.per == 1 ? 40 : 30 + d.nw;
   if (d.family == MB_FAM_WIN4 && d.nw == 2) return 50;  // even-offset windows
   if (d.family == MB_FAM_GRAM) return 60 + (d.S == 16 ? 2 : 0) + (d.q == 16 ? 1 : 0);
@@ -619,12 +615,9 @@ static int launch_family(mb_ctx* c, const ScanParams& P, const PatDev* h_pats, c
       if (d.S == 16) return launch_group<FiltGRAM<16, 16>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
       if (d.q == 8) return launch_group<FiltGRAM<8, 8>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
       return launch_group<FiltGRAM<8, 16>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
-    case MB_FAM_SHIFTOR: {
-      int64_t maxm = 0;
-      for (int i = 0; i < gk; i++) maxm = std::max<int64_t>(maxm, h_pats[h_idx[i]].m);
-      if (maxm <= 32) return launch_group<FiltSO<32>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
-      return launch_group<FiltSO<64>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
-    }
+    case MB_FAM_SHIFTOR:
+      if (d.nw == 2) return launch_group<FiltSO<2>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
+      return launch_group<FiltSO<1>>(c, P, h_pats, h_idx, d_idx, gk, slot, st, fused);
   }
   return fail(MB_EINVAL, "unknown kernel family");
 }

@@ -61,7 +61,7 @@ __device__ __forceinline__ void fused_emit(const ScanParams& P, int64_t tk, uint
 // handed over through full/empty mbarriers; there is no block-wide barrier in
 // the loop, so warps drift independently within the ring.
 template <class Filt, bool FUSED>
-__global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
+__global__ void __launch_bounds__(NT + 32, is_shiftor<Filt>::value ? 2 : 0) scan_kernel(const ScanParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
   StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + SM_HDR);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM_FULL);
@@ -76,9 +76,10 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
   uint32_t* brk = reinterpret_cast<uint32_t*>(stages + NS * P.stage_bytes + NWARP * SEG_WORDS * 4) +
                   warp * 2 * (P.brk_words + 4);
   int32_t* nbw = reinterpret_cast<int32_t*>(brk + P.brk_words + 4);
-  uint64_t* so_s = reinterpret_cast<uint64_t*>(stages + NS * P.stage_bytes + NWARP * SEG_WORDS * 4 +
+  uint32_t* so_s = reinterpret_cast<uint32_t*>(stages + NS * P.stage_bytes + NWARP * SEG_WORDS * 4 +
                                                NWARP * 2 * (P.brk_words + 4) * 4) +
-                   warp * 256;  // K2 only: per-warp shift-or masks
+                   warp * SO_WARP_WORDS;  // K2 only: per-warp symbol bit planes of the segment + AND-step table
+  (void)so_s;
   uint32_t* gbl = reinterpret_cast<uint32_t*>(stages + NS * P.stage_bytes + NWARP * SEG_WORDS * 4 +
                                               NWARP * 2 * (P.brk_words + 4) * 4) +
                   warp * GRAM_TABLE_WORDS;  // K1G only: per-warp gram bloom + hashes (same region as K2's masks)
@@ -159,8 +160,9 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
       blo = P.off + pd.delta;               // valid bits: s = b - delta - off in [0, n-m]
       bhi = P.off + pd.delta + P.n - pd.m;  // inclusive (may be < blo)
       cur_k = k;
-      if constexpr (is_shiftor<Filt>::value) {  // this warp's copy of the 256 shift-or masks
-        for (int i = lane; i < 256; i += 32) so_s[i] = pd.so_masks[i];
+      if constexpr (is_shiftor<Filt>::value) {  // this warp's copy of the pattern's AND-step table
+        __syncwarp();
+        for (int i = lane; i < 4 * (pd.S + pd.q); i += 32) so_s[2 * SO_PLANE_WORDS + i] = pd.bloom[i];
         __syncwarp();
       }
       if constexpr (is_gram<Filt>::value) {  // this warp's copy of the pattern's gram bloom
@@ -183,9 +185,37 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
     uint32_t w0 = 0, w1 = 0;
     bool have;
     if constexpr (is_shiftor<Filt>::value) {
-      // ---- K2: exact per-lane shift-or over positions [c0 + 64 lane, +64)
-      MB_CHECK(S + c0 + 64 * lane + 64 + pd.m + 3 <= send);
-      shiftor_lane<Filt::kW>(S + c0 + 64 * lane, (int)pd.m, so_s, w0, w1);
+      // ---- K2: the segment's bytes packed into symbol bit planes (16 bytes
+      // per lane and round, even lanes store a 32-bit plane word; lanes 0..3
+      // add the 64-byte halo), then each lane ANDs the pattern's m shifted
+      // plane words over its 64 starts [c0 + 64 lane, +64) (so_and_steps)
+      constexpr int NP = Filt::kNP;
+      MB_CHECK(S + c0 + SEG + 64 <= send);
+      __syncwarp();  // the previous segment's plane words have been read
+#pragma unroll
+      for (int r = 0; r <= SEG / 512; r++) {
+        if (r == SEG / 512 && lane >= 4) break;
+        const uint4 X = *reinterpret_cast<const uint4*>(S + c0 + r * 512 + lane * 16);
+#pragma unroll
+        for (int pl = 0; pl < NP; pl++) {
+          const uint32_t a = so_pack16(X, pd.G[4 * pl], pd.G[4 * pl + 1]);
+          const uint32_t o = __shfl_down_sync(r == SEG / 512 ? 0xFu : 0xffffffffu, a, 1);
+          if (!(lane & 1)) so_s[pl * SO_PLANE_WORDS + r * 16 + (lane >> 1)] = a | (o << 16);
+        }
+      }
+      __syncwarp();
+      w0 = w1 = 0xFFFFFFFFu;
+      uint2 ta[2], tb[2];
+#pragma unroll
+      for (int pl = 0; pl < NP; pl++) {
+        ta[pl] = *reinterpret_cast<const uint2*>(so_s + pl * SO_PLANE_WORDS + 2 * lane);
+        tb[pl] = *reinterpret_cast<const uint2*>(so_s + pl * SO_PLANE_WORDS + 2 * lane + 2);
+      }
+      if constexpr (NP == 1) ta[1] = tb[1] = make_uint2(0u, 0u);
+      // pd.S steps at pattern positions < 32 (window words 0..2), pd.q at >= 32 (words 1..3)
+      const uint4* tab = reinterpret_cast<const uint4*>(so_s + 2 * SO_PLANE_WORDS);
+      so_and_steps<NP>(tab, pd.S, ta[0].x, ta[0].y, tb[0].x, ta[1].x, ta[1].y, tb[1].x, w0, w1);
+      if (pd.q) so_and_steps<NP>(tab + pd.S, pd.q, ta[0].y, tb[0].x, tb[0].y, ta[1].y, tb[1].x, tb[1].y, w0, w1);
       if (!interior) {
         const int64_t b = segb + 64 * lane;
         uint64_t vm = 0;
@@ -238,7 +268,7 @@ __global__ void __launch_bounds__(NT + 32) scan_kernel(const ScanParams P) {
     uint32_t cnt = 0;
     if (have) {
       // ---- verify (exact filters skip this)
-      if (!always_exact<Filt>::value && !is_shiftor<Filt>::value && !pd.exact &&
+      if (!always_exact<Filt>::value && !pd.exact &&
           __any_sync(0xffffffffu, (w0 | w1) != 0)) {
         const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
         if (pd.periodic && pd.per == 1) {

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace mb {
@@ -57,14 +58,16 @@ static inline uint32_t load_le32(const uint8_t* p) {
   return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
 }
 
-// K2 (per-lane shift-or) would be auto-chosen for 7 <= m <= 64 at pattern byte
-// entropies up to this many bits.  Measured on B200 (profiles/r1/
-// cfg2_family_sweep.json) it loses to the K1 anchor filter in every config-2
-// cell, even sigma = 2 (0.83-0.94 vs 1.09-1.42 TB/s aggregated): the per-byte
-// mask lookup + dependent D update chain costs more than verifying K1's
-// frequent candidates.  So auto never picks it (threshold < 0); it stays an
-// exact, tested family selectable through mb_plan_opts.family.
-constexpr double K2_MAX_ENTROPY = -1.0;
+// K2 (bit-plane Shift-And, device_common.cuh FiltSO): auto for small alphabets
+// where the word filters are busy (see build_plan); costs ~0.75 operations per
+// text byte and plane for the packing plus ~4.5 (one plane) / 8.5 (two) per
+// pattern position and 64 starts, whatever the candidate density.
+#ifndef MB_K2_LOG2_SURVIVORS
+#define MB_K2_LOG2_SURVIVORS -16.0  // log2 of the expected survivors per start the AND steps aim for (one plane; two: +3)
+#endif
+#ifndef MB_K2_MAX_CAND
+#define MB_K2_MAX_CAND (1.0 / 24)  // expected plane-code candidates per start above which verification dominates
+#endif
 
 // ALIGNED anchor-word thresholds (expected one-/two-word anchor hits per text
 // word above which one more word is added); tuned on config 2.
@@ -254,6 +257,30 @@ static void build_gram_table(const uint8_t* p, int S, int Q, std::vector<uint32_
   }
 }
 
+// K2 symbol planes: NP text-byte bit positions whose values give the pattern's
+// symbols distinct codes where possible -- chosen to minimise the expected
+// candidate rate prod_j P(code(text byte) == code(p[j])) under the byte
+// probabilities pr.  Returns that rate; bits[] = the chosen bit positions.
+static double choose_planes(const uint8_t* p, int64_t m, const double* pr, int np, int* bits) {
+  double best = 1e300;
+  for (int b0 = 0; b0 < 8; b0++)
+    for (int b1 = (np == 2 ? b0 + 1 : 8); b1 < (np == 2 ? 8 : 9); b1++) {
+      double cls[4] = {0, 0, 0, 0};
+      auto code = [&](int c) { return ((c >> b0) & 1) | (np == 2 ? ((c >> b1) & 1) << 1 : 0); };
+      for (int c = 0; c < 256; c++) cls[code(c)] += pr[c];
+      double lr = 0;
+      for (int64_t j = 0; j < m; j++) lr += std::log(std::max(cls[code(p[j])], 1e-300));
+      if (lr < best - 1e-12) best = lr, bits[0] = b0, bits[1] = np == 2 ? b1 : 0;
+    }
+  return std::exp(best);
+}
+// one plane while at most two byte values carry the text (each above 1%), else two
+static int plane_count(const double* pr) {
+  int d = 0;
+  for (int c = 0; c < 256; c++) d += pr[c] > 0.01;
+  return d <= 2 ? 1 : 2;
+}
+
 int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost* ph, std::string* err) {
   if (m < 1) {
     *err = "pattern must have length >= 1";
@@ -285,8 +312,6 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       fam = MB_FAM_SWAR;
     else if (m <= 6)
       fam = MB_FAM_WIN4;
-    else if (m <= 64 && ph->entropy <= K2_MAX_ENTROPY)
-      fam = MB_FAM_SHIFTOR;  // small alphabet: 4-byte anchors are unselective, shift-or needs no verify
     else
       fam = MB_FAM_ALIGNED;  // may become SAMPLED or WIN4 below
   }
@@ -350,6 +375,44 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
     const int nw = choose_aligned_words(pat, m, pr);
     best_aligned(pat, m, pr, nw, &rn);
     if ((nw >= 2 || 4 * r1 > 1e-3) && choose_gram(pat, m, pr, 4 * rn, &gram_S, &gram_Q)) fam = MB_FAM_GRAM;
+  }
+  // K2 where the word filters are busy: exact SWAR at 5 <= m <= 8 (~m/2
+  // operations per byte), WIN4 / ALIGNED flagging more than one word in 50,
+  // multi-word ALIGNED, or a gram filter above its rate limit -- and two bit
+  // planes tell the pattern's symbols apart well enough that the survivors
+  // are mostly occurrences.  Periodic patterns keep the break-run test.
+  const bool auto_fam = opts == nullptr || opts->family == MB_FAM_AUTO;
+  if (auto_fam && m >= 5 && m <= 64 && !(m >= 16 && ph->period <= m / 2) && ph->period > 1 &&
+      (fam == MB_FAM_SWAR || fam == MB_FAM_WIN4 || fam == MB_FAM_ALIGNED || fam == MB_FAM_GRAM)) {
+    double pr[256], r = 0;
+    byte_probs(pat, m, hist, pr);
+    bool busy = fam == MB_FAM_SWAR;
+    // (m >= 7 on WIN4: a rare byte confined to one gram, a^(m-1)b -- that window is more selective than the model says)
+    if (fam == MB_FAM_WIN4) best_win4(pat, m, pr, &r), busy = m <= 6 && r > 2e-2;
+    if (fam == MB_FAM_ALIGNED) {
+      const int nw = (opts && opts->anchor_words) ? opts->anchor_words : choose_aligned_words(pat, m, pr);
+      best_aligned(pat, m, pr, 1, &r);
+      busy = !(opts && opts->anchor_words) && (nw >= 2 || r > 2e-2);
+    }
+    if (fam == MB_FAM_GRAM) {
+      double g = 0;
+      for (int j = 0; j < gram_S; j++) {
+        double x = 1;
+        for (int i = 0; i < gram_Q; i++) x *= pr[pat[j + i]];
+        g += x;
+      }
+      busy = g * 16.0 / gram_S > MB_GRAM_MAX_RATE;  // (sigma = 2, m = 16..22: 0.40 ms; quieter variants run at 0.17-0.20)
+    }
+    if (busy) {
+      // measured on 1 GiB texts (profiles/r2/k2_*): one plane (binary texts) wins from
+      // m = 7 (0.47 vs 0.51 ms; m = 8: 0.38 vs 0.46; m = 12..22: 0.24-0.28 vs 0.40-0.44);
+      // two planes (sigma 3..4) at m = 5 (0.36 vs 0.47) and narrowly from m = 7
+      // (0.27-0.29 vs 0.28-0.30), not at m = 6 (exact SWAR 0.29 vs 0.31)
+      int bits[2];
+      const int np = plane_count(pr);
+      const bool len_ok = np == 1 ? m >= 7 : (m == 5 || m >= 7);
+      if (len_ok && choose_planes(pat, m, pr, np, bits) <= MB_K2_MAX_CAND) fam = MB_FAM_SHIFTOR;
+    }
   }
   if (opts && opts->family == MB_FAM_GRAM) {
     double pr[256];
@@ -446,13 +509,56 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       break;
     }
     case MB_FAM_SHIFTOR: {
-      // bitparallel.py:41-63 compile_so: complemented forward masks over m bits
-      ph->anchor = 0;
+      // bitparallel.py:66-84 compile_sa on symbol bit planes (FiltSO): G[4 pl + ..] =
+      // {byte-bit mask, gather multiplier}; the AND steps cover the D consecutive
+      // pattern positions [a, a + D) whose codes are expected to survive at
+      // <= 2^-16 (one plane) / 2^-13 (two) of the starts (fewest steps; at most SO_MAX_STEPS), as a
+      // table of {shift, plane-A xor mask, plane-B xor mask, 0}: positions < 32
+      // first (S entries), then >= 32 (q entries)
+      double pr[256];
+      byte_probs(pat, m, hist, pr);
+      int bits[2];
+      const int np = plane_count(pr);
+      choose_planes(pat, m, pr, np, bits);
+      double cls[4] = {0, 0, 0, 0};
+      auto code = [&](int c) { return ((c >> bits[0]) & 1) | (np == 2 ? ((c >> bits[1]) & 1) << 1 : 0); };
+      for (int c = 0; c < 256; c++) cls[code(c)] += pr[c];
+      // windows reaching the survivor target beat those that do not; then fewer steps; then fewer survivors
+      double target = np == 1 ? MB_K2_LOG2_SURVIVORS : MB_K2_LOG2_SURVIVORS + 3.0;
+      if (const char* env = getenv("MB_K2_LOG2")) target = atof(env);  // tuning (tools/k2_check.sh)
+      int best_a = 0, best_d = 0;
+      double best_l = 1;
+      bool best_ok = false;
+      for (int64_t a = 0; a < m; a++) {
+        double l = 0;
+        int dd = 0;
+        while (a + dd < m && dd < SO_MAX_STEPS && l > target) l += std::log2(std::max(cls[code(pat[a + dd])], 1e-300)), dd++;
+        const bool ok = l <= target;
+        const bool better = best_d == 0 || (ok && !best_ok) ||
+                            (ok == best_ok && (ok ? (dd < best_d || (dd == best_d && l < best_l - 1e-9)) : l < best_l - 1e-9));
+        if (better) best_a = (int)a, best_d = dd, best_l = l, best_ok = ok;
+      }
+      ph->anchor = best_a;
       d.delta = 0;
-      d.exact = 1;
-      const uint64_t full = m == 64 ? ~0ULL : ((1ULL << m) - 1);
-      ph->so_masks.assign(256, full);
-      for (int64_t j = 0; j < m; j++) ph->so_masks[pat[j]] &= ~(1ULL << j);
+      d.exact = 0;
+      d.nw = np;
+      for (int pl = 0; pl < np; pl++) {
+        d.G[4 * pl] = 0x01010101u << bits[pl];
+        d.G[4 * pl + 1] = ((1u << 28) | (1u << 21) | (1u << 14) | (1u << 7)) >> bits[pl];
+      }
+      ph->bloom.clear();
+      d.S = d.q = 0;
+      for (int half = 0; half < 2; half++)
+        for (int j = best_a; j < best_a + best_d; j++) {
+          if ((j >= 32) != (half == 1)) continue;
+          ph->bloom.push_back((uint32_t)(j & 31));
+          ph->bloom.push_back(((pat[j] >> bits[0]) & 1) ? 0u : ~0u);
+          ph->bloom.push_back(np == 2 && !((pat[j] >> bits[1]) & 1) ? ~0u : 0u);
+          ph->bloom.push_back(0u);
+          (half ? d.q : d.S)++;
+        }
+      ph->bstart.clear();
+      ph->bent.clear();
       break;
     }
     case MB_FAM_GRAM:
@@ -485,6 +591,7 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
   // staged-tile margins (bytes before / after the tile's bit range)
   d.pre = round16(d.delta);
   d.post = round16(m - d.delta + 40) + 16;
+  if (fam == MB_FAM_SHIFTOR) d.post = std::max(d.post, 80);  // the 64-byte plane halo of a tile's last segment
   return MB_OK;
 }
 

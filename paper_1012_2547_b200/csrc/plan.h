@@ -27,18 +27,18 @@ struct PatDev {
   int32_t exact;    // filter alone decides (no verification)
   int32_t pre;      // staged bytes before the tile's first bit (multiple of 16)
   int32_t post;     // staged bytes after the tile's last bit (multiple of 16)
-  uint32_t G[12];   // filter words (family specific); ALIGNED: G[4w + j] = p[a+j+4w .. +4)
+  uint32_t G[12];   // filter words (family specific); ALIGNED: G[4w + j] = p[a+j+4w .. +4);
+                    // K2: per plane {byte-bit mask, gather multiplier, pattern plane bits 0..31, 32..63}
   // K3 sampled q-gram filter (family MB_FAM_SAMPLED); K1G (MB_FAM_GRAM) uses S, q
-  int32_t S;        // sampling stride in bytes (K3: multiple of 16, >= 256; K1G: 8 or 16)
-  int32_t q;        // gram bytes (K3: 4, 8, 16 or 32; K1G: 8 or 16)
+  int32_t S;        // sampling stride in bytes (K3: multiple of 16, >= 256; K1G: 8 or 16); K2: AND steps at pattern positions < 32
+  int32_t q;        // gram bytes (K3: 4, 8, 16 or 32; K1G: 8 or 16); K2: AND steps at positions >= 32
   int32_t B;        // log2 of the bucket count
-  int32_t nw;       // ALIGNED: anchor words (window 4 nw + 3 bytes), 1..3
+  int32_t nw;       // ALIGNED: anchor words (window 4 nw + 3 bytes), 1..3; K2: symbol bit planes (1 or 2)
   int32_t mpa;      // K5 batched pass: 7-byte anchor window offset (m >= 7), whatever the family
   uint32_t mpG[4];  // K5 grams p[mpa+j .. mpa+j+4), j = 0..3
-  const uint32_t* bloom;   // K3: 65536-bit filter over gram hashes; K1G: GRAM_BLOOM_WORDS words (device)
+  const uint32_t* bloom;   // K3: 65536-bit filter over gram hashes; K1G: GRAM_BLOOM_WORDS words; K2: step table (device)
   const uint16_t* bstart;  // (1 << B) + 1 bucket starts (device)
   const uint16_t* bent;    // S entries: pattern offsets j sorted by bucket (device)
-  const uint64_t* so_masks; // K2: 256 complemented shift-or masks (device), bit j clear iff p[j] == c
 };
 
 // K3 sampled-kernel geometry shared with the planner: a warp unit covers
@@ -75,6 +75,11 @@ __host__ __device__ inline uint32_t gram_bloom_bits(uint32_t h) {
   return (1u << ((h >> 20) & 31)) | (1u << ((h >> 15) & 31)) | (1u << ((h >> 10) & 31));
 }
 
+// K2 (MB_FAM_SHIFTOR, bit-plane Shift-And) geometry shared with the planner
+constexpr int SO_PLANE_WORDS = 68;  // per plane: 64 segment words + 2 halo words (m - 1 <= 63 bits), padded
+constexpr int SO_MAX_STEPS = 24;    // AND steps per start; table entries {shift, plane-A xor mask, plane-B xor mask, 0}
+constexpr int SO_WARP_WORDS = 2 * SO_PLANE_WORDS + 4 * SO_MAX_STEPS;  // per-warp smem: planes + step table
+
 struct PlanHost {
   int64_t m = 0;
   std::vector<uint8_t> pat;
@@ -88,7 +93,6 @@ struct PlanHost {
   // K3 tables (host copies; uploaded with the pattern)
   std::vector<uint32_t> bloom;
   std::vector<uint16_t> bstart, bent;
-  std::vector<uint64_t> so_masks;  // K2 (bitparallel.py:47-49 convention)
   double entropy = 0;              // bits per byte of the pattern's byte distribution
 };
 

@@ -189,6 +189,47 @@ def test_shiftor_edges(cuda, m):
             assert np.array_equal(got, oracle.search(p, bytes(t)[off:n])), (m, sigma, off)
 
 
+def test_shiftor_foreign_bytes_and_code_collisions(cuda):
+    """K2 packs text bytes into 1-2 symbol bit planes chosen for the pattern's
+    alphabet: bytes outside it alias to a pattern symbol's code (candidates the
+    verification must reject), and alphabets no two byte bits can separate
+    ({0,1,2,4}) share codes."""
+    rng = np.random.default_rng(4242)
+    n = 3 * ENGINE_TILE + 1234
+    for sym, noise in (([0x41, 0x43], [0x45, 0x47, 0x61, 0x63, 0xC1]),       # A/C differ in bit 1 only
+                       ([0, 1, 2, 4], [8, 16, 3, 5, 6, 255]),               # no separating bit pair
+                       ([0x41, 0x43, 0x47, 0x54], [0x4E, 0x61, 0x63, 0x00]),  # ACGT + N / lower case
+                       ([7, 7 ^ 0x80], [0x07 ^ 0x01, 0x87 ^ 0x10])):
+        for m in (1, 2, 5, 8, 13, 31, 32, 33, 64):
+            syms = np.array(sym, dtype=np.uint8)
+            t = syms[rng.integers(0, len(sym), n)]
+            # a tenth of the text replaced by bytes that alias onto pattern codes
+            idx = rng.choice(n, n // 10, replace=False)
+            t[idx] = np.array(noise, dtype=np.uint8)[rng.integers(0, len(noise), idx.size)]
+            p = bytes(syms[rng.integers(0, len(sym), m)])
+            tb = bytearray(t.tobytes())
+            for s0 in (0, SEG - 3, ENGINE_TILE - m, ENGINE_TILE - 1, 2 * ENGINE_TILE - m // 2, n - m):
+                tb[s0 : s0 + m] = p
+            check(p, bytes(tb), "shiftor")
+
+
+@pytest.mark.parametrize("sigma", [2, 3, 4, 8])
+def test_shiftor_auto_small_alphabets(cuda, sigma):
+    """Auto plans over small alphabets at 5 <= m <= 64 (K2 where the word filters
+    are busy) equal the oracle; sigma = 2, m = 8 must take K2."""
+    rng = np.random.default_rng(900 + sigma)
+    n = 4 * ENGINE_TILE + 999
+    t = rand_bytes(rng, sigma, n)
+    fams = set()
+    for m in (5, 6, 7, 8, 9, 12, 14, 16, 20, 22, 24, 33, 48, 64):
+        off = int(rng.integers(0, n - m))
+        p = t[off : off + m]
+        fams.add((m, engine.Plan(p).info().family))
+        check(p, t)
+    if sigma == 2:
+        assert (8, "shiftor") in fams, fams
+
+
 @pytest.mark.parametrize("tiles", [1, 2, 150, 295, 296, 297, 300, 450])
 def test_single_wave_fused_boundary(cuda, tiles):
     """Texts of up to one resident wave of tiles run as ONE fused launch (scan,

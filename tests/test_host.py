@@ -133,9 +133,9 @@ def test_plan_info_families():
         assert engine.Plan(b"\x05" * (m - 1) + b"\x07").info().family == "win4", m
         assert engine.Plan(b"\x07" + b"\x05" * (m - 1)).info().family == "win4", m
     assert engine.Plan(b"a" * 100).info().periodic
-    # small alphabets, 5 <= m <= 8: exact SWAR instead of a busy anchor filter
-    for m in (5, 6, 7, 8):
-        assert engine.Plan(bytes(rng0.integers(0, 2, m, dtype=np.uint8))).info().family == "swar", m
+    # small alphabets: exact SWAR at m = 5, 6 instead of a busy anchor filter, K2 from m = 7
+    for m, fam in ((5, "swar"), (6, "swar"), (7, "shiftor"), (8, "shiftor")):
+        assert engine.Plan(bytes(rng0.integers(0, 2, m, dtype=np.uint8))).info().family == fam, m
     assert engine.Plan(bytes(range(40, 48))).info().family == "aligned"
     # sampled (K3) only for periods >= 294: a 256 KiB unit's occurrences fit its list
     unit = bytes(rng0.integers(0, 256, 200, dtype=np.uint8))
@@ -158,15 +158,19 @@ def test_plan_info_families():
     assert engine.Plan(long_random, family="aligned").info().family == "aligned"
     with pytest.raises(ValueError):
         engine.Plan(b"a" * 1024, family="sampled")
-    # K2 shift-or is exact and selectable, but auto keeps the faster K1 filter
+    # K2 (bit-plane Shift-And): auto for binary texts at 7 <= m <= 22 and 4-letter ones at m = 5, 7..14,
+    # where the word filters are busy; longer patterns take the strided gram filter
     assert engine.Plan(bytes(rng.integers(0, 4, 40, dtype=np.uint8))).info().family == "gram"
+    assert engine.Plan(bytes([0, 1, 1, 0, 1, 0, 0, 0, 1, 1, 1, 0])).info().family == "shiftor"
+    assert engine.Plan(bytes([0, 1, 2, 3, 1, 0, 2, 2, 3, 1, 0, 3])).info().family == "shiftor"
+    assert engine.Plan(bytes([0, 1, 1, 0, 1, 0])).info().family == "swar"  # m = 6: exact SWAR stays
     # K1G strided gram filter: small alphabets from m = 15 (S = 8) / 23 (S = 16); sigma >= 16 keeps ALIGNED
     i4 = engine.Plan(bytes(rng.integers(0, 4, 64, dtype=np.uint8))).info()
     assert (i4.family, i4.stride, i4.gram, i4.delta) == ("gram", 16, 16, 15)
     i8 = engine.Plan(bytes(rng.integers(0, 8, 16, dtype=np.uint8))).info()
     assert (i8.family, i8.stride, i8.gram, i8.delta) == ("gram", 8, 8, 7)
     assert engine.Plan(bytes(rng.integers(0, 16, 64, dtype=np.uint8))).info().family == "aligned"
-    assert engine.Plan(bytes(rng.integers(0, 4, 12, dtype=np.uint8))).info().family == "aligned"
+    assert engine.Plan(bytes(rng.integers(0, 4, 12, dtype=np.uint8)), family="aligned").info().words == 2
     assert engine.Plan(b"ab" * 20).info().family == "aligned"  # periodic: break-run verification
     assert engine.Plan(bytes(rng.integers(0, 256, 15, dtype=np.uint8)), family="gram").info().family == "gram"
     with pytest.raises(ValueError):
@@ -177,13 +181,13 @@ def test_plan_info_families():
 
 
 def test_aligned_anchor_words():
-    """Small alphabets widen the ALIGNED anchor to 2 words (11-byte window)
-    where the strided gram filter does not apply (m < 15..23); large alphabets
-    keep one word; forced values are validated."""
+    """The ALIGNED family widens its anchor to 2 words (11-byte window) over
+    small alphabets (auto plans take K2 or the strided gram filter there);
+    large alphabets keep one word; forced values are validated."""
     rng = np.random.default_rng(3)
     for sigma, words in ((2, 2), (4, 2), (64, 1), (256, 1)):
         p = rng.integers(0, sigma, 14 if sigma <= 4 else 64, dtype=np.uint8).tobytes()
-        info = engine.Plan(p).info()
+        info = engine.Plan(p, family="aligned" if sigma <= 4 else "auto").info()
         assert (info.family, info.words) == ("aligned", words), sigma
     p = rng.integers(0, 256, 40, dtype=np.uint8).tobytes()
     for nw in (1, 2, 3):
