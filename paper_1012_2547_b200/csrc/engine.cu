@@ -988,7 +988,11 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       // runs (it triggers its dependents at entry) and loop over the queue
       int exp_per_sm = 0;
       CUDA_TRY(occupancy((const void*)expand_kernel, EXP_WARPS * 32, 0, &exp_per_sm));
-      const int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS, (int64_t)c->nsm * std::max(exp_per_sm, 1));
+      // CTAs per SM capped (MB_EXP_CTAS, tuning): fewer concurrently advancing 16 KB
+      // output regions keep more of their DRAM pages open (tools/probe_expand_pattern.cu)
+      static const int exp_cap = [] { const char* e = getenv("MB_EXP_CTAS"); return e ? atoi(e) : 8; }();
+      const int64_t eg = std::min<int64_t>((T + EXP_WARPS - 1) / EXP_WARPS,
+                                           (int64_t)c->nsm * std::max(std::min(exp_per_sm, exp_cap), 1));
       CUDA_TRY(launch_pdl(expand_kernel, (int)eg, EXP_WARPS * 32, st, P));
       g_launches++;
       CUDA_TRY(cudaGetLastError());

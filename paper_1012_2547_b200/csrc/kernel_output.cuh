@@ -216,6 +216,31 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
   // network); longer ones go to expand_kernel, whose warp per segment writes
   // them coalesced (a thread looping over 32 scattered stores is slower)
   const uint32_t fuse_max = !P.out ? 0u : P.unsorted_lists ? (uint32_t)min(FUSE_MAX, 8) : (uint32_t)FUSE_MAX;
+  // expand-queue slots: a thread's queued segments take consecutive slots in
+  // segment order and a warp's threads consecutive ranges (one atomic per
+  // warp), so expand_kernel's neighbouring warps write neighbouring output
+  // regions (a dense text queues every segment)
+  unsigned long long qslot = 0;
+  {
+    uint32_t nqd = 0;
+    if (P.out)
+#pragma unroll 1
+      for (int q = 0; q < PER; q++) {
+        const uint32_t vq = (s_cnt[(q >> 1) * OT + tid] >> (16 * (q & 1))) & 0xFFFFu;
+        const bool cp = rem + q < seg_per_pat ? cp0 : cp1;
+        nqd += (base + (int64_t)tid * PER + q < nseg && vq > fuse_max && !cp) ? 1u : 0u;
+      }
+    uint32_t qinc = nqd;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, qinc, d);
+      if (lane >= d) qinc += v;
+    }
+    const uint32_t wtotal = __shfl_sync(0xffffffffu, qinc, 31);
+    unsigned long long wbase = 0;
+    if (lane == 0 && wtotal) wbase = atomicAdd(&P.ticket[P.dense_slot], (unsigned long long)wtotal);
+    qslot = __shfl_sync(0xffffffffu, wbase, 0) + (qinc - nqd);
+  }
   // nothing to emit and no pattern ends in this thread's range: done
   const bool idle = tsum == 0 && rem + PER < seg_per_pat;
 #pragma unroll 1
@@ -263,7 +288,7 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
             }
           } else {
             // queue entry: segment | count << 48, output offset, position of bit 0
-            const unsigned long long slot = atomicAdd(&P.ticket[P.dense_slot], 1ULL);
+            const unsigned long long slot = qslot++;
             P.seglist[slot] = ds | ((int64_t)vq << 48);
             P.toff[slot] = run;
             P.qpos[slot] = rem * SEG - shift;
@@ -286,14 +311,21 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
 // / bitmap words one step ahead are in flight while the current segment is
 // written.  An entry carries everything but the match bits (segment | count,
 // output offset, position of bit 0), so no pattern lookup or division sits on
-// the path.  Unsorted (MP) lists get a 32-lane bitonic sort; dense segments
-// are staged in smem as uint16 offsets (set bits extracted one by one, or, at
-// >= 50% density, by an unrolled predicated pass over all 64 bits of a lane),
-// then streamed out with coalesced 256-byte stores.
+// the path.  Unsorted (MP) lists get a 32-lane bitonic sort.  Dense segments
+// (bitmaps; each lane holds 64 consecutive bits) are written in 256-byte rows
+// ALIGNED to the output's 256-byte lines (first and last row partial), from
+//  * a table of its runs of ones when there are at most EXP_RUNS of them
+//    (c^m over a text of mostly c): position = row index + a per-run offset;
+//  * else a per-warp smem run of uint16 offsets, the set bits extracted one
+//    by one (brev + clz, a running pointer; >= 50% set: a predicated pass).
+// tools/probe_expand_pattern.cu (B200): rows starting at the segment's own
+// offset straddle two lines each and write at 4.0-4.6 TB/s (16 KB regions, a
+// warp each); line-aligned rows at 5.5-6.0.
 #ifndef MB_EXP_WARPS
 #define MB_EXP_WARPS 8
 #endif
 constexpr int EXP_WARPS = MB_EXP_WARPS;
+constexpr int EXP_RUNS = 32;  // run table entries per warp (one per lane)
 
 struct ExpSeg {  // one queued segment as a lane holds it
   int64_t g, o, sp;
@@ -310,19 +342,33 @@ __device__ __forceinline__ ExpSeg exp_load(const ScanParams& P, int64_t ent, int
   e.c = (uint32_t)(ent >> 48);
   e.o = o;
   e.sp = sp;
-  e.lv = P.lists[e.g * LIST_CAP + lane];  // meaningful when c <= LIST_CAP
-  e.xa = P.bitmaps[e.g * SEG_WORDS + lane];  // meaningful when c > LIST_CAP
-  e.xb = P.bitmaps[e.g * SEG_WORDS + 32 + lane];
+  e.lv = e.xa = e.xb = 0;
+  if (e.c <= LIST_CAP) {
+    e.lv = P.lists[e.g * LIST_CAP + lane];
+  } else {  // bits [64 lane, 64 lane + 64) of the segment
+    const uint2 x = reinterpret_cast<const uint2*>(P.bitmaps + e.g * SEG_WORDS)[lane];
+    e.xa = x.x, e.xb = x.y;
+  }
   return e;
 }
-// smem run index of entry e: XOR-swizzled by its 32-entry block, so all-ones
-// words (lane l writing entries 64 l + k) do not pile onto two banks
-__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 5) & 31u); }
+
+// out[i] = sp + v: the 64-bit add done once per segment when the low word cannot carry
+__device__ __forceinline__ void exp_store(int64_t* d, int64_t sp, uint32_t v, bool nocarry) {
+  if (nocarry) {
+    const uint2 r = make_uint2((uint32_t)sp + v, (uint32_t)((uint64_t)sp >> 32));
+    *reinterpret_cast<uint2*>(d) = r;
+  } else {
+    *d = sp + v;
+  }
+}
 
 __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint16_t s_run[EXP_WARPS][SEG];  // dense segments: staged offsets per warp
+  __shared__ uint32_t s_tab[EXP_WARPS][2 * EXP_RUNS + 2];  // run table: first position, output rank
   uint16_t* const sb = s_run[warp];
+  uint32_t* const tab_s = s_tab[warp];
+  uint32_t* const tab_o = s_tab[warp] + EXP_RUNS + 1;
   MB_TRACE_MARK(10);
   pdl_wait();  // queue and offsets of offsets_kernel
   MB_TRACE_MARK(12);
@@ -332,6 +378,8 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
   if (blockIdx.x == 0 && threadIdx.x < NTICKETS && threadIdx.x != P.dense_slot) P.ticket[threadIdx.x] = 0ULL;
   const int64_t nq = (int64_t)P.ticket[P.dense_slot];
   const int64_t stride = (int64_t)gridDim.x * EXP_WARPS;
+  // element misalignment of the output against its 256-byte lines
+  const uint32_t omis = (uint32_t)(((uintptr_t)P.out >> 3) & 31u);
   int64_t qi = (int64_t)blockIdx.x * EXP_WARPS + warp;
   ExpSeg cur;
   int64_t h_ent = 0, h_o = 0, h_sp = 0;  // entry qi + stride
@@ -370,48 +418,101 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
         }
         if (lane < (int)c && o + lane < P.cap) P.out[o + lane] = pos0 + v;
       } else {
-        // dense: exclusive popcount prefix of the 64 words (2 per lane); each
-        // lane writes its words' set bits into the warp's smem run; the warp
-        // then streams the c positions out coalesced
-        const uint32_t pa = __popc(cur.xa), pb = __popc(cur.xb);
-        uint32_t ia = pa, ib = pb;
+        // dense: the lane's 64 bits, exclusive prefix e of the ones before them
+        const uint32_t xa = cur.xa, xb = cur.xb;
+        const uint32_t pc = __popc(xa) + __popc(xb);
+        // starts of runs of ones (bit b set, bit b - 1 clear; the previous lane's top bit carries in)
+        const uint32_t prev_top = __shfl_up_sync(0xffffffffu, xb, 1) >> 31;
+        const uint32_t sa = xa & ~((xa << 1) | (lane ? prev_top : 0u));
+        const uint32_t sb2 = xb & ~((xb << 1) | (xa >> 31));
+        const uint32_t nr = __popc(sa) + __popc(sb2);
+        uint32_t inc = pc | (nr << 16);  // both prefixes in one scan (sum pc <= 2048, sum nr <= 1024)
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t va = __shfl_up_sync(0xffffffffu, ia, d);
-          const uint32_t vb = __shfl_up_sync(0xffffffffu, ib, d);
-          if (lane >= d) ia += va, ib += vb;
+          const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
+          if (lane >= d) inc += v;
         }
-        const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31);
-        uint32_t ea = ia - pa, eb = ta + ib - pb;
-        const uint32_t ba = 32u * lane, bb = 32u * (32 + lane);
-        if (c >= SEG / 2) {  // >= 50% set: every bit position once, predicated
-#pragma unroll
-          for (int b = 0; b < 32; b++) {
-            if ((cur.xa >> b) & 1u) sb[swz(ea)] = (uint16_t)(ba + b), ea++;
-            if ((cur.xb >> b) & 1u) sb[swz(eb)] = (uint16_t)(bb + b), eb++;
+        const uint32_t R = __shfl_sync(0xffffffffu, inc, 31) >> 16;
+        const uint32_t e = (inc & 0xFFFFu) - pc;
+        const uint32_t lim = (uint32_t)(P.cap - o < (int64_t)c ? P.cap - o : (int64_t)c);
+        const int64_t sp = cur.sp;
+        const bool nocarry = (uint32_t)sp <= 0xFFFF0000u;
+        int64_t* const d0 = P.out + o;
+        // rows on 256-byte lines: element i of the segment sits at line offset
+        // (o + omis + i) & 31; aligned index j = i + head
+        const uint32_t head = (uint32_t)((o + omis) & 31);
+        const uint32_t iend = head + lim;
+        if (R <= (uint32_t)EXP_RUNS) {
+          // ---- run-structured (c^m over a text of mostly c, config 5): a table of
+          // (first position, output rank) per run; a row inside one run is
+          // position = i + one warp-uniform offset -- no staging of positions
+          uint32_t ri = (inc >> 16) - nr;
+          uint32_t x = sa;
+          while (x) {
+            const uint32_t bq = __ffs(x) - 1;
+            x &= x - 1;
+            tab_s[ri] = 64u * lane + bq;
+            tab_o[ri] = e + __popc(xa & ((1u << bq) - 1u));
+            ri++;
+          }
+          x = sb2;
+          while (x) {
+            const uint32_t bq = __ffs(x) - 1;
+            x &= x - 1;
+            tab_s[ri] = 64u * lane + 32u + bq;
+            tab_o[ri] = e + __popc(xa) + __popc(xb & ((1u << bq) - 1u));
+            ri++;
+          }
+          if (lane == 0) tab_o[R] = 0xFFFFFFFFu;  // sentinel: no run starts at or after rank c
+          __syncwarp();
+          // run by run (warp-uniform bounds): the rows of run r cover the aligned
+          // indices [O_r + head, O_{r+1} + head); a row shared by two runs is
+          // written by both, each its own lanes
+          for (uint32_t r = 0; r < R; r++) {
+            const uint32_t O = tab_o[r];
+            if (O >= lim) break;
+            const uint32_t On = min(tab_o[r + 1], lim);
+            const uint32_t dl = tab_s[r] - O;  // position - rank inside this run
+            const uint32_t jlo = O + head, jhi = On + head;
+            uint32_t j = (jlo & ~31u) + lane;
+            if (j >= jlo && j < jhi) exp_store(d0 + (j - head), sp, j - head + dl, nocarry);
+            j += 32;
+#pragma unroll 4
+            for (; j < jhi; j += 32) exp_store(d0 + (j - head), sp, j - head + dl, nocarry);
           }
         } else {
-          uint32_t x = cur.xa;
-          while (x) {
-            const uint32_t b = __ffs(x) - 1;
-            x &= x - 1;
-            sb[swz(ea++)] = (uint16_t)(ba + b);
+          // ---- general: set bits -> uint16 offsets in the warp's smem run
+          uint16_t* w = sb + e;
+          const uint32_t ba = 64u * lane;
+          if (c >= SEG / 2) {  // >= 50% set: every bit position once, predicated
+#pragma unroll
+            for (int bq = 0; bq < 32; bq++)
+              if ((xa >> bq) & 1u) *w++ = (uint16_t)(ba + bq);
+#pragma unroll
+            for (int bq = 0; bq < 32; bq++)
+              if ((xb >> bq) & 1u) *w++ = (uint16_t)(ba + 32u + bq);
+          } else {
+            uint32_t y = __brev(xa);
+            while (y) {
+              const uint32_t bq = __clz(y);
+              y ^= 0x80000000u >> bq;
+              *w++ = (uint16_t)(ba + bq);
+            }
+            y = __brev(xb);
+            while (y) {
+              const uint32_t bq = __clz(y);
+              y ^= 0x80000000u >> bq;
+              *w++ = (uint16_t)(ba + 32u + bq);
+            }
           }
-          x = cur.xb;
-          while (x) {
-            const uint32_t b = __ffs(x) - 1;
-            x &= x - 1;
-            sb[swz(eb++)] = (uint16_t)(bb + b);
+          __syncwarp();
+#pragma unroll 4
+          for (uint32_t j = lane; j < iend; j += 32) {
+            const uint32_t i = j - head;  // wraps below 0 for the first row's leading lanes
+            if (i < lim) exp_store(d0 + i, sp, sb[i], nocarry);
           }
         }
-        __syncwarp();
-        const uint32_t lim = (uint32_t)(P.cap - o < (int64_t)c ? P.cap - o : (int64_t)c);
-        int64_t* d = P.out + o + lane;
-        const int64_t sp = cur.sp;
-        uint32_t i = lane;
-#pragma unroll 4
-        for (uint32_t blk = 0; i < lim; blk++, i += 32, d += 32) *d = sp + sb[i ^ (blk & 31u)];
-        __syncwarp();  // the next segment overwrites sb
+        __syncwarp();  // the next segment overwrites sb / the run table
       }
     }
     if (!have_nxt) break;
