@@ -504,7 +504,8 @@ def run_batched_sweep(args, rank, world, local_rank):
         for m in (4, 16, 64, 256, 1024):
             cells.append((95, m, t, inputs.config3_patterns(t, m)))
     flush = L2Flush(dev)
-    rows, tot_b, tot_ms, launches0 = [], 0, 0.0, engine.launch_count()
+    rows, tot_b, tot_alg, tot_ms, launches0 = [], 0, 0, 0.0, engine.launch_count()
+    peak, peak_src = measured_peak()
     dtexts = {}
     for sigma, m, t, pats in cells:
         key = id(t)
@@ -537,11 +538,17 @@ def run_batched_sweep(args, rank, world, local_rank):
         ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
         b = len(pats) * t.size
         fams = sorted({pl.info().family for pl in plans.plans})
+        # batched-mode algorithmic bytes: the text once for the whole
+        # batch, every pattern, 8 B per position, the K + 1 CSR offsets
+        alg = t.size + sum(len(p) for p in pats) + 8 * total + 8 * (len(pats) + 1)
         rows.append({"sigma": sigma, "m": m, "patterns": len(pats), "ms": round(ms, 4),
-                     "text_gbps": round(b / (ms * 1e-3) / 1e9, 1), "matches": total, "families": fams})
+                     "text_gbps": round(b / (ms * 1e-3) / 1e9, 1), "matches": total, "families": fams,
+                     "alg_bytes": alg, "hbm_frac": round(alg / (ms * 1e-3) / 1e9 / peak, 4)})
         tot_b += b
+        tot_alg += alg
         tot_ms += ms
     value = tot_b / (tot_ms * 1e-3) / 1e9
+    achieved = tot_alg / (tot_ms * 1e-3) / 1e9
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -551,6 +558,11 @@ def run_batched_sweep(args, rank, world, local_rank):
                        "l2": FLUSH_DESC + "; value aggregated K*n/t",
                        "timing": "per cell: median of the steps' CUDA-event times; a spin kernel keeps the "
                                  "GPU busy while each launch is enqueued, so host enqueue time is excluded"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                         "kernel": "whole batched launches (batch pass / per-pattern scans, offsets, expand, replicate)",
+                         "algorithmic_bytes": "n + sum(m_k) + 8 * sum(count_k) + 8 * (K + 1) per batch (SURVEY.md 8(d)): "
+                                              "the text read once for the whole batch"},
             "cells": rows, "gpu_launches": engine.launch_count() - launches0}), flush=True)
 
 

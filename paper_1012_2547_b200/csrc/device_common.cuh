@@ -261,10 +261,7 @@ struct FiltWIN4E {
 // NW anchor words (window 4 NW + 3 bytes) words k .. k+NW-1 must all match
 // (G[4w + j] = p[a+j+4w .. +4)): small alphabets need NW = 2, 3 to keep the
 // candidate rate low.  w[] holds 4 + NW - 1 >= 5 words.
-// RUN1: c^m patterns (period 1): any hit marks the lane's 16 positions -- the
-// run test of the verify path decides every start exactly (run1_lane_matches);
-// a separate instantiation so the general filter's fast path carries no check.
-template <int NW, bool RUN1 = false>
+template <int NW>
 struct FiltALIGNED {
   __device__ static __forceinline__ uint32_t run(const uint32_t* w, const PatDev& P) {
     if constexpr (NW == 1) {
@@ -273,14 +270,10 @@ struct FiltALIGNED {
       for (int k = 0; k < 4; k++)
         hit |= (w[k] == P.G[0]) | (w[k] == P.G[1]) | (w[k] == P.G[2]) | (w[k] == P.G[3]);
       if (!hit) return 0;
-      if constexpr (RUN1) return 0xFFFFu;
     }
-    if constexpr (!RUN1) return run_direct(w, P);
-    return 0;
+    return run_direct(w, P);
   }
   __device__ static __forceinline__ uint32_t run_direct(const uint32_t* w, const PatDev& P) {
-    static_assert(!RUN1 || NW == 1, "RUN1 is a one-word filter");
-    if constexpr (RUN1) return run(w, P);
     uint32_t mk = 0;
 #pragma unroll
     for (int k = 0; k < 4; k++)
@@ -294,6 +287,34 @@ struct FiltALIGNED {
     return mk;
   }
 };
+
+// Run patterns c^m (period 1, m >= 7): the filter IS the exact test.  Each
+// lane turns its 16 staged bytes per round into 16 "byte != c" bits (nothing
+// to do when all 16 are c, one existence test when none is), pairs of lanes
+// store them as words of the segment's nz bitmap (+ the m - 1 byte halo), and
+// run1_lane_matches reads every start's verdict off that bitmap: a start
+// survives iff no nz bit lies in [s, s + m).  delta = 0, no verification.
+struct FiltRUN1 {
+  static constexpr bool kRun1 = true;
+};
+template <class F, class = void>
+struct is_run1 : std::false_type {};
+template <class F>
+struct is_run1<F, std::void_t<decltype(F::kRun1)>> : std::true_type {};
+// nz bits of 16 bytes; sets anyc when a byte equals c (a start may survive nearby)
+__device__ __forceinline__ uint32_t run1_nz16(const uint4& X, uint32_t c4, bool& anyc) {
+  const uint32_t a = X.x ^ c4, b = X.y ^ c4, c = X.z ^ c4, d = X.w ^ c4;
+  if (!(a | b | c | d)) {
+    anyc = true;
+    return 0u;
+  }
+  const uint32_t k = 0x01010101u;
+  const uint32_t hz = (((a - k) & ~a) | ((b - k) & ~b) | ((c - k) & ~c) | ((d - k) & ~d)) & 0x80808080u;
+  if (!hz) return 0xFFFFu;  // no byte equals c
+  anyc = true;
+  return ((~zero_bytes4(a)) & 0xFu) | (((~zero_bytes4(b)) & 0xFu) << 4) | (((~zero_bytes4(c)) & 0xFu) << 8) |
+         (((~zero_bytes4(d)) & 0xFu) << 12);
+}
 
 // K2 / m <= 64, small alphabets (bitparallel.py:66-84 compile_sa, Shift-And,
 // turned sideways): instead of one state word per text position, the text is

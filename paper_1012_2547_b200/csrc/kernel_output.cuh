@@ -223,23 +223,25 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
   unsigned long long qslot = 0;
   {
     uint32_t nqd = 0;
-    if (P.out)
+    if (P.out && tsum32 > fuse_max)  // (a thread whose counts sum to <= fuse_max queues nothing)
 #pragma unroll 1
       for (int q = 0; q < PER; q++) {
         const uint32_t vq = (s_cnt[(q >> 1) * OT + tid] >> (16 * (q & 1))) & 0xFFFFu;
         const bool cp = rem + q < seg_per_pat ? cp0 : cp1;
         nqd += (base + (int64_t)tid * PER + q < nseg && vq > fuse_max && !cp) ? 1u : 0u;
       }
-    uint32_t qinc = nqd;
+    if (__any_sync(0xffffffffu, nqd != 0)) {
+      uint32_t qinc = nqd;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, qinc, d);
-      if (lane >= d) qinc += v;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, qinc, d);
+        if (lane >= d) qinc += v;
+      }
+      const uint32_t wtotal = __shfl_sync(0xffffffffu, qinc, 31);
+      unsigned long long wbase = 0;
+      if (lane == 0) wbase = atomicAdd(&P.ticket[P.dense_slot], (unsigned long long)wtotal);
+      qslot = __shfl_sync(0xffffffffu, wbase, 0) + (qinc - nqd);
     }
-    const uint32_t wtotal = __shfl_sync(0xffffffffu, qinc, 31);
-    unsigned long long wbase = 0;
-    if (lane == 0 && wtotal) wbase = atomicAdd(&P.ticket[P.dense_slot], (unsigned long long)wtotal);
-    qslot = __shfl_sync(0xffffffffu, wbase, 0) + (qinc - nqd);
   }
   // nothing to emit and no pattern ends in this thread's range: done
   const bool idle = tsum == 0 && rem + PER < seg_per_pat;

@@ -184,7 +184,47 @@ __global__ void __launch_bounds__(NT + 32, is_shiftor<Filt>::value ? 2 : 0) scan
     // this lane's 64 positions of the segment: linear bitmap words 2*lane, 2*lane+1
     uint32_t w0 = 0, w1 = 0;
     bool have;
-    if constexpr (is_shiftor<Filt>::value) {
+    if constexpr (is_run1<Filt>::value) {
+      // ---- c^m: nz bitmap of the segment + halo straight from the staged bytes
+      const uint32_t c4 = 0x01010101u * spat[0];
+      const int hw = ((int)pd.m + 30) >> 5;  // halo words covering m - 1 bits
+      MB_CHECK(S + c0 + SEG + 32 * hw <= send);
+      bool anyc = false;
+      __syncwarp();  // the previous segment's bitmap has been read
+#pragma unroll
+      for (int r = 0; r < SEG / 512; r++) {
+        const uint4 X = *reinterpret_cast<const uint4*>(S + c0 + r * 512 + lane * 16);
+        const uint32_t nz = run1_nz16(X, c4, anyc);
+        const uint32_t o = __shfl_down_sync(0xffffffffu, nz, 1);
+        if (!(lane & 1)) brk[r * 16 + (lane >> 1)] = nz | (o << 16);
+      }
+      for (int h = 0; h < 2 * hw; h += 32) {  // halo: 16 bytes per lane, 2 hw lanes (hw <= 32)
+        const int l2 = h + lane;
+        uint32_t nz = 0xFFFFu;
+        if (l2 < 2 * hw) {
+          bool dummy = false;  // a c byte in the halo alone starts nothing in this segment
+          nz = run1_nz16(*reinterpret_cast<const uint4*>(S + c0 + SEG + l2 * 16), c4, dummy);
+        }
+        const uint32_t o = __shfl_down_sync(0xffffffffu, nz, 1);
+        if (!(lane & 1) && l2 < 2 * hw) brk[SEG / 32 + (l2 >> 1)] = nz | (o << 16);
+      }
+      have = __any_sync(0xffffffffu, anyc);
+      if (have) {
+        __syncwarp();
+        const uint64_t mm = run1_lane_matches(brk, SEG / 32 + hw, (int)pd.m, lane);
+        w0 = (uint32_t)mm;
+        w1 = (uint32_t)(mm >> 32);
+        if (!interior) {
+          const int64_t b = segb + 64 * lane;
+          uint64_t vm = 0;
+          for (int i = 0; i < 64; i++)
+            if (b + i >= blo && b + i <= bhi) vm |= 1ULL << i;
+          w0 &= (uint32_t)vm;
+          w1 &= (uint32_t)(vm >> 32);
+        }
+        have = __any_sync(0xffffffffu, (w0 | w1) != 0);
+      }
+    } else if constexpr (is_shiftor<Filt>::value) {
       // ---- K2: the segment's bytes packed into symbol bit planes (16 bytes
       // per lane and round, even lanes store a 32-bit plane word; lanes 0..3
       // add the 64-byte halo), then each lane ANDs the pattern's m shifted
@@ -271,17 +311,7 @@ __global__ void __launch_bounds__(NT + 32, is_shiftor<Filt>::value ? 2 : 0) scan
       if (!always_exact<Filt>::value && !pd.exact &&
           __any_sync(0xffffffffu, (w0 | w1) != 0)) {
         const uint8_t* Y0 = S - pd.delta;  // Y0[rel] = text byte at the start position of tile bit rel
-        if (pd.periodic && pd.per == 1) {
-          // c^m: exact match bits from the staged bytes (device_common.cuh
-          // run1_lane_matches); the filter's candidates carry the text-edge
-          // validity, so the intersection is the answer
-          const int nwords = (SEG + (int)pd.m + 31) / 32;
-          MB_CHECK(Y0 + c0 >= sbeg && Y0 + c0 + 32 * nwords + 9 <= send);
-          warp_run_nz(Y0 + c0, S + c0, pd.delta, 0x01010101u * spat[0], nwords, brk, nbw, false);
-          const uint64_t mm = run1_lane_matches(brk, nwords, (int)pd.m, lane);
-          w0 &= (uint32_t)mm;
-          w1 &= (uint32_t)(mm >> 32);
-        } else if (pd.periodic) {
+        if (pd.periodic) {
           // s matches <=> t[s..s+per) = p[0..per) and no break t[y] != t[y+per] for
           // y in [s, s+L).  A break y kills starts [y-L+1, y]: walk the few breaks
           // that reach this lane's 64 starts, mask them out in bulk.

@@ -506,6 +506,16 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
         d.periodic = 1;
         d.L = (int)(m - ph->period);
       }
+      // c^m (any m this family takes): the exact run filter (FiltRUN1) -- bit b
+      // is start b, the nz bitmap needs no anchor and nothing is verified
+      if (ph->period == 1 && !(opts && opts->anchor_words)) {
+        d.periodic = 1;
+        d.L = (int)(m - 1);
+        d.nw = 1;
+        d.delta = 0;
+        d.exact = 1;
+        ph->anchor = 0;
+      }
       break;
     }
     case MB_FAM_SHIFTOR: {
