@@ -105,6 +105,13 @@ static int plan_device(const mb_plan* p, const PatDev** out) {
   return MB_OK;
 }
 
+// what plan_pass needs of a pattern (a plan's host side, or a prepared batch's copy)
+struct PatSrc {
+  const uint8_t* bytes;
+  int64_t m;
+  int period;
+};
+
 // One batch-level pass over the text (K5; see plan_pass).
 struct BatchPass {
   int kind = 0;
@@ -201,6 +208,10 @@ struct mb_batch {
   uint32_t* d_mp = nullptr;  // pass tables on the device
   int32_t* d_rep = nullptr;   // representatives (| REP_COPY) when the batch has duplicates
   uint32_t* d_need = nullptr; // per-pattern scan flags (pass / duplicates)
+  // pattern bytes and periods, for re-planning the pass per sub-batch on texts
+  // whose scratch does not fit the whole batch (run_batch)
+  std::vector<std::vector<uint8_t>> pat_bytes;
+  std::vector<PatSrc> src;
 };
 
 extern "C" {
@@ -681,7 +692,15 @@ static void pass_chunk(int kc, int ent_words, const Ent& ent_of, std::vector<uin
   *nout = nent;
 }
 
-static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, BatchPass* bp) {
+struct PatBytes {  // a pattern's bytes as plan_pass reads them
+  const uint8_t* p;
+  size_t n;
+  const uint8_t* data() const { return p; }
+  size_t size() const { return n; }
+  uint8_t operator[](size_t i) const { return p[i]; }
+};
+
+static void plan_pass(const PatSrc* src, const PatDev* h_pats, int K, BatchPass* bp) {
   *bp = BatchPass();
   // identical patterns are searched once: rep[k] = first k' with the same bytes
   bp->rep.resize(K);
@@ -689,7 +708,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     std::unordered_map<std::string, int> first;
     first.reserve((size_t)K * 2);
     for (int k = 0; k < K; k++) {
-      const auto& pb = plans[k]->h.pat;
+      const PatBytes pb{src[k].bytes, (size_t)src[k].m};
       auto ins = first.emplace(std::string(reinterpret_cast<const char*>(pb.data()), pb.size()), k);
       bp->rep[k] = ins.first->second;
       bp->ndup += ins.first->second != k;
@@ -699,7 +718,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
   double hist[256] = {0}, tot = 0;
   int64_t minm = INT64_MAX;
   for (int k = 0; k < K; k++) {
-    const auto& pb = plans[k]->h.pat;
+    const PatBytes pb{src[k].bytes, (size_t)src[k].m};
     const size_t lim = std::min<size_t>(pb.size(), 64);
     for (size_t i = 0; i < lim; i++) hist[pb[i]] += 1, tot += 1;
     minm = std::min<int64_t>(minm, h_pats[k].m);
@@ -718,7 +737,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
   bp->dcopy.assign(K, 0);
   for (int k = 0; k < K; k++)
     if (rep[k] != k) {
-      const auto& pb = plans[k]->h.pat;
+      const PatBytes pb{src[k].bytes, (size_t)src[k].m};
       bp->dcopy[k] = 2048.0 * gp(pb.data(), (int)std::min<size_t>(pb.size(), 32)) < 256.0 ? 1 : 0;
     }
   if (K - bp->ndup < 8 || K > MP_CHUNK * MAX_MP_CHUNKS) return;
@@ -769,7 +788,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
   int64_t qm = INT64_MAX;
   int n_in = 0;
   for (int k = 0; k < K; k++) {
-    const auto& pb = plans[k]->h.pat;
+    const PatBytes pb{src[k].bytes, (size_t)src[k].m};
     const int64_t m = (int64_t)pb.size();
     if (rep[k] != k) {  // searched through its representative: no entry, no scan
       need[k] = 0u;
@@ -779,7 +798,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     // batch joins the pass (500 sampled scans of a 4 MiB text: 65-93 us; the pass: ~30)
     if (m < 2 || (h_pats[k].family == MB_FAM_SAMPLED && K - bp->ndup < 64)) continue;
     const double per_seg = 2048.0 * gp(pb.data(), (int)std::min<int64_t>(m, 32));
-    if (per_seg > (plans[k]->h.period < m ? 2.0 : 8.0)) continue;
+    if (per_seg > (src[k].period < m ? 2.0 : 8.0)) continue;
     need[k] = 0u;
     n_in++;
     qm = std::min(qm, m);
@@ -794,7 +813,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     for (int k = 0; k < K; k++)
       if (!need[k] && rep[k] == k) {
         double best = 1;
-        const auto& pb = plans[k]->h.pat;
+        const PatBytes pb{src[k].bytes, (size_t)src[k].m};
         for (int64_t a = 0; a + 8 <= (int64_t)pb.size(); a++) best = std::min(best, gp(pb.data() + a, 8));
         pool8 += best;
       }
@@ -805,7 +824,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
   double pooled = 0;
   for (int k = 0; k < K; k++) {
     if (need[k] || rep[k] != k) continue;
-    const auto& pb = plans[k]->h.pat;
+    const PatBytes pb{src[k].bytes, (size_t)src[k].m};
     const int64_t m = (int64_t)pb.size();
     // rarest window, spread over distinct gram values (a value shared by many
     // patterns makes every text hit on it walk all of them)
@@ -841,7 +860,7 @@ static void plan_pass(const mb_plan* const* plans, const PatDev* h_pats, int K, 
     pass_chunk(std::min(MP_CHUNK, K - k0), 4,
                [&](int i, int j, uint32_t* h, uint32_t* w) {
                  if (j || need[k0 + i] || rep[k0 + i] != k0 + i) return false;  // one gram per pattern in the pass
-                 const auto& pb = plans[k0 + i]->h.pat;
+                 const PatBytes pb{src[k0 + i].bytes, (size_t)src[k0 + i].m};
                  uint8_t g[16] = {0};
                  memcpy(g, pb.data() + anchor[k0 + i], q);
                  uint32_t gw[4];
@@ -1194,7 +1213,7 @@ int mb_find(mb_ctx* c, const mb_plan* p, const uint8_t* d_text, int64_t n, int64
 // queue; a third of free memory, <= 16 GiB), chained through d_offsets.
 static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int K, const uint8_t* d_text, int64_t n,
                      int64_t* d_out, int64_t cap, int64_t* d_offsets, cudaStream_t st, const BatchPass* bp,
-                     const uint32_t* d_tab, const int32_t* d_rep_pre = nullptr,
+                     const uint32_t* d_tab, const PatSrc* src, const int32_t* d_rep_pre = nullptr,
                      const uint32_t* d_need_pre = nullptr) {
   const double per_pattern = (double)((n + 2 * MB_MAX_M + TILE) / TILE + 1) * NWARP * 346.0;
   // batches needing <= 1 GiB of scratch, or no more than a previous call
@@ -1212,6 +1231,41 @@ static int run_batch(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int 
   if (kc < K && kc >= MP_CHUNK) kc -= kc % MP_CHUNK;  // keep the pass tables' chunks aligned to sub-batches
   std::vector<int32_t> lrep;
   std::vector<uint32_t> lneed;
+  if (kc < K && src) {
+    // The text is too large for the whole batch's scratch: every sub-batch is
+    // planned on its own (duplicates and the batch pass among its patterns),
+    // so it still reads the text once -- not once per pattern.  Host planning
+    // and a table upload per sub-batch: negligible against GiB-sized scans.
+    for (int k0 = 0; k0 < K; k0 += kc) {
+      const int kk = std::min(kc, K - k0);
+      BatchPass sp;
+      plan_pass(src + k0, h_pats + k0, kk, &sp);
+      const bool dups = sp.ndup > 0, whole = sp.kind != 0;
+      lrep.resize(kk);
+      lneed.resize(kk);
+      for (int i = 0; i < kk; i++) {
+        lrep[i] = sp.rep[i];
+        if (lrep[i] != i && sp.dcopy[i]) lrep[i] |= REP_COPY;
+        lneed[i] = whole ? sp.need[i] : (sp.rep[i] == i ? 1u : 0u);
+      }
+      int rc;
+      if (whole) {
+        if ((rc = grow(&c->mp_tab, &c->mp_tab_cap, sp.words(), "batch pass tables"))) return rc;
+        if ((rc = stage_upload(c, c->mp_tab, sp.img.data(), sizeof(uint32_t) * sp.img.size(), st))) return rc;
+      }
+      SubBatch sb;
+      sb.bp = whole ? &sp : nullptr;
+      sb.d_tab = whole ? c->mp_tab : nullptr;
+      sb.chunk0 = 0;
+      sb.h_rep = dups ? lrep.data() : nullptr;
+      sb.h_need = (dups || whole) ? lneed.data() : nullptr;
+      sb.csr0 = k0 == 0 ? d_offsets : nullptr;
+      rc = run_search(c, d_pats + k0, h_pats + k0, kk, d_text, n, d_out, cap, d_offsets + 1 + k0, st,
+                      k0 ? d_offsets + k0 : nullptr, sb);
+      if (rc) return rc;
+    }
+    return MB_OK;
+  }
   for (int k0 = 0; k0 < K; k0 += kc) {
     const int kk = std::min(kc, K - k0);
     // the pass runs on sub-batches made of whole table chunks
@@ -1266,12 +1320,15 @@ int mb_find_batch(mb_ctx* c, const mb_plan* const* plans, int K, const uint8_t* 
   if ((rc = grow(&c->d_pats, &c->pats_cap, K, "batch params"))) return rc;
   if ((rc = stage_begin(c))) return rc;
   if ((rc = stage_upload(c, c->d_pats, c->h_pats.data(), sizeof(PatDev) * K, st))) return rc;
-  plan_pass(plans, c->h_pats.data(), K, &c->pass);
+  std::vector<PatSrc> src(K);
+  for (int k = 0; k < K; k++) src[k] = PatSrc{plans[k]->h.pat.data(), plans[k]->h.m, plans[k]->h.period};
+  plan_pass(src.data(), c->h_pats.data(), K, &c->pass);
   if (c->pass.kind) {
     if ((rc = grow(&c->mp_tab, &c->mp_tab_cap, c->pass.words(), "batch pass tables"))) return rc;
     if ((rc = stage_upload(c, c->mp_tab, c->pass.img.data(), sizeof(uint32_t) * c->pass.img.size(), st))) return rc;
   }
-  rc = run_batch(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets, st, &c->pass, c->mp_tab);
+  rc = run_batch(c, c->d_pats, c->h_pats.data(), K, d_text, n, d_out, cap, d_offsets, st, &c->pass, c->mp_tab,
+                 src.data());
   if (rc) tickets_recover(c, st);
   const int rc2 = stage_end(c, st);
   const int rc3 = ctx_leave(c, st);
@@ -1294,7 +1351,13 @@ int mb_batch_create(const mb_plan* const* plans, int K, mb_batch** out) {
     b->h_pats[k] = plans[k]->dview;
   }
   cudaGetDevice(&b->device);
-  plan_pass(plans, b->h_pats.data(), K, &b->pass);
+  b->pat_bytes.resize(K);
+  b->src.resize(K);
+  for (int k = 0; k < K; k++) {
+    b->pat_bytes[k] = plans[k]->h.pat;
+    b->src[k] = PatSrc{b->pat_bytes[k].data(), plans[k]->h.m, plans[k]->h.period};
+  }
+  plan_pass(b->src.data(), b->h_pats.data(), K, &b->pass);
   const BatchPass& bp = b->pass;
   const std::vector<uint32_t>& img = bp.img;
   // the whole batch's representative / scan-flag arrays (run_batch's sub-batch
@@ -1350,7 +1413,7 @@ int mb_find_batch_prepared(mb_ctx* c, const mb_batch* b, const uint8_t* d_text, 
   if (rc) return rc;
   if ((rc = stage_begin(c))) return rc;
   rc = run_batch(c, b->d_pats, b->h_pats.data(), b->K, d_text, n, d_out, cap, d_offsets, st, &b->pass, b->d_mp,
-                 b->d_rep, b->d_need);
+                 b->src.data(), b->d_rep, b->d_need);
   if (rc) tickets_recover(c, st);
   const int rc2 = stage_end(c, st);
   const int rc3 = ctx_leave(c, st);

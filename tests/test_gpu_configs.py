@@ -132,3 +132,37 @@ def test_config4_full(cuda):
         props(got, p, t)
     del d
     torch.cuda.empty_cache()
+
+
+def test_large_text_batch_keeps_the_pass_per_sub_batch(cuda, monkeypatch):
+    """A 256 MiB text against 96 patterns with a scratch budget that fits ~40
+    patterns: the batch runs as 3 chained sub-batches, each planned on its own
+    and each still ONE pass over the text (not one scan per pattern); every
+    position of every pattern equals the threaded C oracle."""
+    n = 256 << 20
+    t = inputs.rand_text_np(64, n, derive_seed(2026, "large-batch"))
+    rng = np.random.default_rng(77)
+    pats = []
+    for i in range(96):
+        m = int(rng.integers(12, 41))
+        off = int(rng.integers(0, n - m))
+        pats.append(t[off : off + m].tobytes())
+    pats[17] = pats[3]  # a duplicate inside one sub-batch
+    pats[70] = pats[5]  # ... and one whose first copy sits in an earlier sub-batch
+    d = torch.from_numpy(t).cuda()
+    plans = engine.Batch([engine.Plan(p) for p in pats])
+    per_pattern = (n // 2048 + 64) * 346
+    monkeypatch.setenv("MB_SCRATCH_BUDGET", str(per_pattern * 40))
+    before = engine.mp_batches()
+    pos, offs = engine.find_batch(plans, d)
+    assert engine.mp_batches() == before + 3, "a sub-batch fell back to per-pattern scans"
+    pos, offs = pos.cpu().numpy(), offs.cpu().numpy()
+    assert offs[0] == 0 and offs.size == len(pats) + 1
+    for k, p in enumerate(pats):
+        want = oracle.search(p, t, threads=THREADS)
+        assert np.array_equal(pos[offs[k] : offs[k + 1]], want), k
+    # the ad-hoc entry (mb_find_batch: plans given per call) takes the same route
+    before = engine.mp_batches()
+    pos2, offs2 = engine.find_batch([engine.Plan(p) for p in pats], d)
+    assert engine.mp_batches() == before + 3
+    assert np.array_equal(pos2.cpu().numpy(), pos) and np.array_equal(offs2.cpu().numpy(), offs)
