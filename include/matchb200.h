@@ -45,7 +45,7 @@ extern "C" {
 #define MB_FAM_SWAR 1    /* K1, m <= 3 or 5..8: SWAR xor/zero-byte packed compare, exact */
 #define MB_FAM_WIN4 2    /* K1, 4 <= m <= 6: packed 32-bit window compare */
 #define MB_FAM_ALIGNED 3 /* K1/K3, m >= 7: aligned-word q-gram anchor + smem verify */
-#define MB_FAM_SHIFTOR 4 /* K2, m <= 64: per-thread bit-parallel shift-or */
+#define MB_FAM_SHIFTOR 4 /* K2, m <= 64: per-thread bit-parallel Shift-And over 1-2 symbol bit planes (small alphabets; verified) */
 #define MB_FAM_SAMPLED 5 /* K3, m >= 272: sampled q-gram hash filter, sublinear DRAM reads */
 #define MB_FAM_GRAM 6    /* K1G, m >= 15: strided q-gram bloom filter over the staged tile (small alphabets) */
 
@@ -62,13 +62,13 @@ typedef struct {
 typedef struct {
   int64_t m;
   int family;     /* chosen MB_FAM_* */
-  int anchor;     /* pattern offset of the anchor window (ALIGNED, WIN4) */
+  int anchor;     /* pattern offset of the anchor window (ALIGNED, WIN4) / of K2's AND-step window */
   int delta;      /* bitmap index shift: bit b <-> position b - delta */
   int period;     /* smallest period of the pattern (== m if aperiodic) */
   int periodic;   /* 1 if verification uses the period/break-run test */
   int stride;     /* sampling stride S in bytes (K3 SAMPLED, K1G GRAM; else 0) */
   int gram;       /* gram length q in bytes (K3 SAMPLED, K1G GRAM; else 0) */
-  int words;      /* ALIGNED anchor words (window 4 words + 3 bytes; 0 for other families) */
+  int words;      /* ALIGNED anchor words (window 4 words + 3 bytes); K2 SHIFTOR: symbol bit planes (1 or 2); else 0 */
 } mb_plan_info_t;
 
 /* ---- plans: the compile_X(p) analogue (comparison.py:70-352 preprocessing) ---- */

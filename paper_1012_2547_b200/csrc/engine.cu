@@ -255,7 +255,7 @@ int mb_plan_info(const mb_plan* p, mb_plan_info_t* info) {
   const bool strided = p->h.family == MB_FAM_SAMPLED || p->h.family == MB_FAM_GRAM;
   info->stride = strided ? p->h.dev.S : 0;
   info->gram = strided ? p->h.dev.q : 0;
-  info->words = p->h.family == MB_FAM_ALIGNED ? p->h.dev.nw : 0;
+  info->words = (p->h.family == MB_FAM_ALIGNED || p->h.family == MB_FAM_SHIFTOR) ? p->h.dev.nw : 0;
   return MB_OK;
 }
 

@@ -51,10 +51,10 @@ constexpr int LIST_CAP = 32;      // sparse segments keep <= 32 uint16 tile offs
 // ticket counters (one uint64 each, zeroed between searches):
 // count-kernel launches of one batch: one per family key (engine.cu
 // family_key: SWAR m = 1,2,3,5..8 (7), WIN4 and WIN4E (2), ALIGNED 1/2/3 words
-// and RUN1 (4), SAMPLED (1), SO32/SO64 (2), GRAM (S, Q) (4) = NFAMILY_KEYS),
+// and RUN1 (4), SAMPLED (1), K2 with one / two planes (2), GRAM (S, Q) (4) = NFAMILY_KEYS),
 // twice with a batch pass (scans + overflow fallback)
 constexpr int NFAMILY_KEYS = 20;
-constexpr int MAX_GROUPS = 2 * NFAMILY_KEYS;  // slots 0..31
+constexpr int MAX_GROUPS = 2 * NFAMILY_KEYS;  // slots 0..39
 constexpr int TICKET_OFFSETS = MAX_GROUPS;    // offsets_kernel chunks (ticket order)
 constexpr int MAX_MP_CHUNKS = 7;    // batch-pass table chunks (MP_CHUNK patterns each)
 constexpr int TICKET_MP0 = TICKET_OFFSETS + 1;

@@ -402,8 +402,8 @@ def test_mpb_byte_offset_pass(cuda, sigma, lo, hi):
 
 
 def test_batch_with_every_family_group(cuda):
-    """One batch spanning all ten family keys (SWAR m=1/2/3, WIN4, ALIGNED
-    1/2/3 words, sampled, shift-or 32/64): one count launch per group."""
+    """One batch spanning ten family keys (SWAR m=1/2/3, WIN4, ALIGNED
+    1/2/3 words, sampled, K2 with one and two bit planes): one count launch per group."""
     rng = np.random.default_rng(404)
     n = 2 * TILE + 999
     t = rand_bytes(rng, 256, n)
@@ -411,10 +411,9 @@ def test_batch_with_every_family_group(cuda):
     t = t[:9000] + tb + t[9000 + len(tb):]
     specs = [(t[100:101], "auto", 0), (t[200:202], "auto", 0), (t[300:303], "auto", 0), (t[400:405], "auto", 0),
              (t[500:524], "auto", 1), (tb[10:50], "auto", 2), (tb[100:160], "auto", 3),
-             (t[700:1300], "auto", 0), (t[2000:2020], "shiftor", 0), (t[3000:3050], "shiftor", 0)]
+             (t[700:1300], "auto", 0), (tb[2000:2020], "shiftor", 0), (t[3000:3050], "shiftor", 0)]
     plans = [engine.Plan(p, fam, anchor_words=nw) for p, fam, nw in specs]
-    keys = {(pl.info().family, pl.m if pl.info().family == "swar" else pl.info().words,
-             pl.m <= 32 if pl.info().family == "shiftor" else None) for pl in plans}
+    keys = {(pl.info().family, pl.m if pl.info().family == "swar" else pl.info().words) for pl in plans}
     assert len(keys) == 10, keys
     for obj in (plans, plans * 3):
         pos, offs = engine.find_batch(obj, t)
@@ -587,7 +586,7 @@ def test_batch_duplicate_patterns(cuda, sigma, m, monkeypatch):
 def test_batch_every_family_key_with_pass(cuda):
     """All 16 family keys of engine.cu family_key (SWAR m = 1,2,3,5..8, WIN4,
     even-window WIN4, ALIGNED 1/2/3 words, the c^m run filter, sampled,
-    shift-or 32/64) in ONE batch together with enough sparse long patterns for
+    K2 with one / two bit planes) in ONE batch together with enough sparse long patterns for
     a batch pass -- every key then launches twice (ungated, and gated behind
     the pass's overflow flag): 32 count-kernel groups, the ticket-slot limit."""
     rng = np.random.default_rng(405)
@@ -602,10 +601,10 @@ def test_batch_every_family_key_with_pass(cuda):
     specs += [(tb[i * 40: i * 40 + m], "swar", 0) for i, m in enumerate((5, 6, 7, 8), 1)]
     specs += [(t[500:524], "auto", 1), (tb[300:340], "auto", 2), (tb[400:460], "auto", 3),
               (b"\x07" * 20, "auto", 0), (t[60000:60700], "auto", 0),
-              (t[2000:2020], "shiftor", 0), (t[3000:3050], "shiftor", 0)]
+              (tb[2000:2020], "shiftor", 0), (t[3000:3050], "shiftor", 0)]
     plans = [engine.Plan(p, fam, anchor_words=nw) for p, fam, nw in specs]
     infos = [pl.info() for pl in plans]
-    keys = {(i.family, i.m if i.family == "swar" else i.words, i.m <= 32 if i.family == "shiftor" else None,
+    keys = {(i.family, i.m if i.family == "swar" else i.words,
              i.periodic and i.period == 1 if i.family == "aligned" else i.m == 4 if i.family == "win4" else None)
             for i in infos}
     assert len(keys) == 16, keys
