@@ -116,6 +116,7 @@ struct PatSrc {
 struct BatchPass {
   int kind = 0;
   int q = 0;
+  int exact = 0;  // kind 2: every pattern of the pass has length q -- a gram match is an occurrence
   std::vector<uint32_t> img;                    // all chunks, each 16-byte aligned
   struct Chunk {
     int64_t off;  // word offset in img
@@ -785,8 +786,16 @@ static void plan_pass(const PatSrc* src, const PatDev* h_pats, int K, BatchPass*
   // if self-overlapping: a^8 clusters in a binary text) take the pass, the
   // others keep their per-pattern scan; worth it when most are sparse
   std::vector<uint32_t> need(K, 1u);
-  int64_t qm = INT64_MAX;
+  int64_t qm = INT64_MAX, qmax = 0;
   int n_in = 0;
+  // a batch of equally long short patterns (m = 2, 3, 4, 8: the gram is the
+  // whole pattern, a gram match needs no verification) may be denser
+  bool uniform = true;
+  for (int k = 1; k < K; k++) uniform &= src[k].m == src[0].m;
+  uniform &= src[0].m == 2 || src[0].m == 3 || src[0].m == 4 || src[0].m == 8;
+  // (config 2, 500 patterns per 4 MiB text, limits 8 / 2 -> 16 / 8: sigma = 16, m = 2 0.334 -> 0.252 ms,
+  // sigma = 2, m = 8 0.41 -> 0.375, sigma = 4, m = 4 0.377 -> 0.349; 40 / 20: sigma = 8, m = 2 0.23 -> 0.49)
+  const double dens_max = uniform ? 16.0 : 8.0, dens_max_ov = uniform ? 8.0 : 2.0;
   for (int k = 0; k < K; k++) {
     const PatBytes pb{src[k].bytes, (size_t)src[k].m};
     const int64_t m = (int64_t)pb.size();
@@ -798,10 +807,11 @@ static void plan_pass(const PatSrc* src, const PatDev* h_pats, int K, BatchPass*
     // batch joins the pass (500 sampled scans of a 4 MiB text: 65-93 us; the pass: ~30)
     if (m < 2 || (h_pats[k].family == MB_FAM_SAMPLED && K - bp->ndup < 64)) continue;
     const double per_seg = 2048.0 * gp(pb.data(), (int)std::min<int64_t>(m, 32));
-    if (per_seg > (src[k].period < m ? 2.0 : 8.0)) continue;
+    if (per_seg > (src[k].period < m ? dens_max_ov : dens_max)) continue;
     need[k] = 0u;
     n_in++;
     qm = std::min(qm, m);
+    qmax = std::max(qmax, m);
   }
   if (n_in < 8 || 2 * n_in < K - bp->ndup) return;
   int q = qm >= 8 ? 8 : qm >= 4 ? 4 : (int)qm;
@@ -845,6 +855,10 @@ static void plan_pass(const PatSrc* src, const PatDev* h_pats, int K, BatchPass*
   if (pooled > 8.0) return;
   bp->kind = 2;
   bp->q = q;
+  bp->exact = (q != 16 && qm == q && qmax == q) ? 1 : 0;
+  for (int k = 0; k < K && bp->exact; k++)
+    if (!need[k] && rep[k] == k && (anchor[k] != 0 || h_pats[k].delta < 0 || h_pats[k].delta > 0xFFFF)) bp->exact = 0;
+  const bool exact = bp->exact != 0;
   bp->need = need;
   int64_t pre = 0, post = 0;
   for (int k = 0; k < K; k++) {
@@ -867,7 +881,8 @@ static void plan_pass(const PatSrc* src, const PatDev* h_pats, int K, BatchPass*
                  memcpy(gw, g, 16);
                  w[0] = gw[0];
                  w[1] = gw[1];
-                 w[2] = ((uint32_t)i << 16) | (uint32_t)anchor[k0 + i];
+                 // (exact pass: the anchor is 0 and the slot carries the family's bitmap shift)
+                 w[2] = ((uint32_t)i << 16) | (uint32_t)(exact ? h_pats[k0 + i].delta : anchor[k0 + i]);
                  w[3] = q == 16 ? pass_fp16(gw[2], gw[3]) : 0u;
                  *h = q == 16 ? pass_hash16(gw[0], gw[1], gw[2], gw[3]) : pass_hash(w[0], w[1]);
                  return true;
@@ -1079,6 +1094,7 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       M.B = B;
       M.nents = bp->chunks[ci].nent;
       M.kbase = k0;
+      M.exact_m = (bp->kind == 2 && bp->exact) ? bp->q : 0;
       M.ticket = c->ticket + TICKET_MP0 + (ci - chunk0);
       M.zero_n = k0 == 0 ? T + 2 : 0;  // the first launch's prologue (its grid is co-resident)
       auto smem_for = [&](int ns) {

@@ -322,6 +322,11 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
           const uint4 en = ents[e];
           if (en.x != lo || en.y != hi || en.w != fp) continue;
           const int kl = (int)(en.z >> 16);
+          if (P.exact_m) {  // the gram is the whole pattern: an occurrence, recorded at its family's bit
+            const int64_t sp0 = x - P.off;
+            if (sp0 >= 0 && sp0 + P.exact_m <= P.n) mp_record(P, P.kbase + kl, x + (int64_t)(en.z & 0xFFFFu));
+            continue;
+          }
           const int a = (int)(en.z & 0xFFFFu);
           const int64_t sv = x - a;  // virtual start
           const int64_t spos = sv - P.off;
