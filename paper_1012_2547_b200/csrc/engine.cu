@@ -544,7 +544,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
     const int64_t units = ((wunits + SMP_WARPS - 1) / SMP_WARPS) * gk;
     const int64_t grid_s = std::min<int64_t>(units, (int64_t)c->nsm * per_sm_s);
     if (fused) *fused = false;
-    sampled_kernel<<<(int)grid_s, SMP_NT, smem_s, st>>>(P);
+    CUDA_TRY(launch_ex(sampled_kernel, (int)grid_s, SMP_NT, smem_s, st, P, true, false));
   } else {
     auto smem_for = [&](int ns) {
       return (size_t)SM_STAGES + (size_t)ns * P.stage_bytes + NWARP * SEG_WORDS * 4 +
@@ -581,7 +581,7 @@ static int launch_group(mb_ctx* c, ScanParams P, const PatDev* h_pats, const int
     }
     if (per_sm < 1) return fail(MB_ECUDA, "scan kernel does not fit on an SM");
     const int64_t grid = std::min<int64_t>(P.group_tiles, (int64_t)c->nsm * per_sm);
-    scan_kernel<F, false><<<(int)grid, NT + 32, smem, st>>>(P);
+    CUDA_TRY(launch_ex(scan_kernel<F, false>, (int)grid, NT + 32, smem, st, P, true, false));
   }
   g_launches++;
   CUDA_TRY(cudaGetLastError());

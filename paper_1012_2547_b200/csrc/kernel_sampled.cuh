@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(SMP_NT, MB_SMP_MINB) sampled_kernel(const Scan
   uint16_t* bent = reinterpret_cast<uint16_t*>(smem + 8192 + 2064);    // <= 4096
   uint32_t* lists = reinterpret_cast<uint32_t*>(smem + 8192 + 2064 + 8192);  // [SMP_WARPS][SMP_LIST]
   int64_t* s_ticket = reinterpret_cast<int64_t*>(lists + SMP_WARPS * SMP_LIST);
-  pdl_trigger();  // the offsets kernel may be scheduled as SMs drain (it waits for this grid)
+  pdl_trigger();  // the next grid may be scheduled as SMs drain
+  pdl_wait();     // (see scan_kernel: count kernels are programmatic dependent launches)
   if (P.run_if && *P.run_if == 0u) return;  // conditional fallback launch (MP did not overflow)
   uint8_t* spat = reinterpret_cast<uint8_t*>(s_ticket + 2);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
