@@ -470,6 +470,9 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
           // run by run (warp-uniform bounds): the rows of run r cover the aligned
           // indices [O_r + head, O_{r+1} + head); a row shared by two runs is
           // written by both, each its own lanes
+          // (the low-word add and the row pointer are strength-reduced by hand: 3-4
+          // instructions per 256-byte row, so a few warps per SM keep the stores flowing)
+          const uint32_t splo = (uint32_t)sp, sphi = (uint32_t)((uint64_t)sp >> 32);
           for (uint32_t r = 0; r < R; r++) {
             const uint32_t O = tab_o[r];
             if (O >= lim) break;
@@ -477,10 +480,23 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
             const uint32_t dl = tab_s[r] - O;  // position - rank inside this run
             const uint32_t jlo = O + head, jhi = On + head;
             uint32_t j = (jlo & ~31u) + lane;
-            if (j >= jlo && j < jhi) exp_store(d0 + (j - head), sp, j - head + dl, nocarry);
-            j += 32;
-#pragma unroll 4
-            for (; j < jhi; j += 32) exp_store(d0 + (j - head), sp, j - head + dl, nocarry);
+            if (nocarry) {
+              uint2* p = reinterpret_cast<uint2*>(d0 + ((int64_t)j - (int64_t)head));
+              uint32_t v = splo + (j - head + dl);
+              if (j >= jlo && j < jhi) *p = make_uint2(v, sphi);
+              j += 32, p += 32, v += 32;
+#pragma unroll 1
+              for (; j + 96 < jhi; j += 128, p += 128, v += 128) {
+                p[0] = make_uint2(v, sphi);
+                p[32] = make_uint2(v + 32, sphi);
+                p[64] = make_uint2(v + 64, sphi);
+                p[96] = make_uint2(v + 96, sphi);
+              }
+              for (; j < jhi; j += 32, p += 32, v += 32) *p = make_uint2(v, sphi);
+            } else {
+              if (j >= jlo && j < jhi) d0[j - head] = sp + (j - head + dl);
+              for (j += 32; j < jhi; j += 32) d0[j - head] = sp + (j - head + dl);
+            }
           }
         } else {
           // ---- general: set bits -> uint16 offsets in the warp's smem run

@@ -37,6 +37,30 @@ __global__ void __launch_bounds__(256) k_warp_al(int64_t* __restrict__ out, cons
     }
   }
 }
+// warp per segment, aligned rows, plus the real kernel's reads: a 256-byte
+// bitmap and a 24-byte queue entry per segment, prefetched one segment ahead
+__global__ void __launch_bounds__(256) k_warp_al_rd(int64_t* __restrict__ out, const int64_t* __restrict__ off, int nseg,
+                                                    const uint2* __restrict__ bm) {
+  const int lane = threadIdx.x & 31;
+  const int W = gridDim.x * 8;
+  int g = blockIdx.x * 8 + (threadIdx.x >> 5);
+  uint2 x = g < nseg ? bm[(size_t)g * 32 + lane] : make_uint2(0, 0);
+  for (; g < nseg; g += W) {
+    const uint2 nx = g + W < nseg ? bm[(size_t)(g + W) * 32 + lane] : make_uint2(0, 0);
+    const int64_t o = off[g];
+    const unsigned sz = (unsigned)(off[g + 1] - o);
+    int64_t* d = out + o;
+    const unsigned head = (unsigned)(o & 31);
+    const unsigned nrows = (head + sz + 31) >> 5;
+    const int64_t v0 = (int64_t)g * 2048 + (x.x ^ x.y);
+#pragma unroll 4
+    for (unsigned r = 0; r < nrows; r++) {
+      const unsigned i = 32 * r + lane - head;
+      if (i < sz) d[i] = v0 + i;
+    }
+    x = nx;
+  }
+}
 // CTA per segment, aligned rows, warp w on rows w, w + 8, ...
 __global__ void __launch_bounds__(256) k_cta_al(int64_t* __restrict__ out, const int64_t* __restrict__ off, int nseg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -120,11 +144,15 @@ int main() {
     cudaMalloc(&d_off, off.size() * 8);
     cudaMemcpy(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice);
     const double bytes = total * 8.0;
+    uint2* d_bm;
+    cudaMalloc(&d_bm, (size_t)nseg * 256);
+    cudaMemset(d_bm, 0x55, (size_t)nseg * 256);
     printf("sizes %d..%d (%d segments):\n", range.first, range.second, nseg);
     for (int mult : {1, 2, 4, 5, 8}) {
       const int g = nsm * mult;
-      printf("  grid %4d: warp/seg aligned %6.0f  cta/seg aligned %6.0f |", g,
+      printf("  grid %4d: warp/seg aligned %6.0f  +reads %6.0f  cta/seg aligned %6.0f |", g,
              timeit([&] { k_warp_al<<<g, 256>>>(out, d_off, nseg); }, bytes),
+             timeit([&] { k_warp_al_rd<<<g, 256>>>(out, d_off, nseg, d_bm); }, bytes),
              timeit([&] { k_cta_al<<<g, 256>>>(out, d_off, nseg); }, bytes));
       printf(" warp/seg %6.0f  cta/seg %6.0f  out256/warp %6.0f  out1024/warp %6.0f  out2048/cta %6.0f out8192/cta %6.0f GB/s\n",
              timeit([&] { k_warp<<<g, 256>>>(out, d_off, nseg); }, bytes),
@@ -135,6 +163,7 @@ int main() {
              timeit([&] { k_out_cta<1024><<<g, 256>>>(out, total); }, bytes));
     }
     cudaFree(d_off);
+    cudaFree(d_bm);
   }
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
