@@ -181,6 +181,19 @@ __device__ __forceinline__ uint32_t shr8(uint32_t lo, uint32_t hi, int k) {
 // positions: a cheap existence test first, the exact bit set only on a hit.
 
 // K1 / m <= 3: byte d of x_k is zero iff t[v..v+m) == p (v = 4k + d).
+// zero-byte flags of four words -> 16 mask bits: per word the exact 0x80 flags
+// (3 operations), one IMAD gathering them into the top nibble (the partial
+// products of (2^21 + 2^14 + 2^7 + 1) never overlap) and one funnel shift
+// appending it -- 4 ALU + 1 FMA-pipe operations per word instead of 9.
+__device__ __forceinline__ uint32_t zero_flags16(const uint32_t* x) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 3; k >= 0; k--) {
+    const uint32_t y = ~(((x[k] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x[k] | 0x7F7F7F7Fu);  // 0x80 in each zero byte
+    acc = __funnelshift_l(y * 0x00204081u, acc, 4);
+  }
+  return acc;
+}
 template <int M>
 struct FiltSWAR {
   static constexpr bool kAlwaysExact = true;  // no verification code in this instantiation
@@ -195,10 +208,20 @@ struct FiltSWAR {
       acc |= (v - 0x01010101u) & ~v;
     }
     if (!(acc & 0x80808080u)) return 0;
-    uint32_t mk = 0;  // per-word IMAD packing keeps part of this off the ALU pipe
+    return zero_flags16(x);
+  }
+  // the mask alone (no early-out test): while the warp's previous segment had
+  // matches (small alphabets: every segment has)
+  __device__ static __forceinline__ uint32_t run_direct(const uint32_t* w, const PatDev& P) {
+    uint32_t x[4];
 #pragma unroll
-    for (int k = 0; k < 4; k++) mk |= zero_bytes4(x[k]) << (4 * k);
-    return mk;
+    for (int k = 0; k < 4; k++) {
+      uint32_t v = w[k] ^ P.G[0];
+#pragma unroll
+      for (int j = 1; j < M; j++) v |= shr8(w[k + (j >> 2)], w[k + (j >> 2) + 1], j & 3) ^ P.G[j];
+      x[k] = v;
+    }
+    return zero_flags16(x);
   }
 };
 

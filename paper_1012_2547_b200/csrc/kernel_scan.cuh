@@ -1,4 +1,4 @@
-// kernel_scan.cuh -- scan_kernel<Filter>: warp-specialised TMA ring, one 2 KiB segment per consumer warp (K1 filters, K2 shift-or)
+// kernel_scan.cuh -- scan_kernel<Filter>: warp-specialised TMA ring, one 2 KiB segment per consumer warp (K1 filters, K1G gram, RUN1, K2 bit-plane Shift-And)
 // (part of libmatchb200; included by engine.cu)
 #pragma once
 
