@@ -316,8 +316,9 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
 // the path.  Unsorted (MP) lists get a 32-lane bitonic sort.  Dense segments
 // (bitmaps; each lane holds 64 consecutive bits) are written in 256-byte rows
 // ALIGNED to the output's 256-byte lines (first and last row partial), from
-//  * a table of its runs of ones when there are at most EXP_RUNS of them
-//    (c^m over a text of mostly c): position = row index + a per-run offset;
+//  * a table of its runs of ones when there are at most EXP_RUNS of them,
+//    32 matches long on average (c^m over a text of mostly c): position =
+//    row index + a per-run offset;
 //  * else a per-warp smem run of uint16 offsets, the set bits extracted one
 //    by one (brev + clz, a running pointer; >= 50% set: a predicated pass).
 // tools/probe_expand_pattern.cu (B200): rows starting at the segment's own
@@ -444,7 +445,8 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
         // (o + omis + i) & 31; aligned index j = i + head
         const uint32_t head = (uint32_t)((o + omis) & 31);
         const uint32_t iend = head + lim;
-        if (R <= (uint32_t)EXP_RUNS) {
+        if (R <= (uint32_t)EXP_RUNS && c >= 32u * R) {  // few LONG runs (a row per run at least): c^m with short m
+                                                          // over random text has dozens of 1-2 match runs -- staged below
           // ---- run-structured (c^m over a text of mostly c, config 5): a table of
           // (first position, output rank) per run; a row inside one run is
           // position = i + one warp-uniform offset -- no staging of positions

@@ -420,19 +420,22 @@ __global__ void __launch_bounds__(NT + 32, is_shiftor<Filt>::value ? 2 : 0) scan
       }
       // ---- count + compact store (segment g = tile * NWARP + warp)
       const uint32_t c2 = __popc(w0) + __popc(w1);
-      uint32_t inc = c2;
+      cnt = __reduce_add_sync(0xffffffffu, c2);  // one REDUX; the prefix scan only where offsets are needed
+      auto prefix = [&]() -> uint32_t {  // exclusive prefix of c2 over the lanes
+        uint32_t inc = c2;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-      }
-      cnt = __shfl_sync(0xffffffffu, inc, 31);
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+          if (lane >= d) inc += o;
+        }
+        return inc - c2;
+      };
       if constexpr (FUSED) {
-        f_w0 = w0, f_w1 = w1, f_ex = inc - c2;
+        f_w0 = w0, f_w1 = w1, f_ex = prefix();
       } else {
         const int64_t g = tk * NWARP + warp;
         if (cnt <= LIST_CAP) {
-          uint32_t j = inc - c2;
+          uint32_t j = prefix();
           uint16_t* L = P.lists + g * LIST_CAP;
           uint64_t bits = ((uint64_t)w1 << 32) | w0;
           while (bits) {
