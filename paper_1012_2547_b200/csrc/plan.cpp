@@ -74,6 +74,10 @@ static inline uint32_t load_le32(const uint8_t* p) {
 #ifndef MB_SWAR_RATE
 #define MB_SWAR_RATE 2e-2  // anchor hits per text word above which 5 <= m <= 8 take exact SWAR
 #endif
+#ifndef MB_SWAR_RATE4
+#define MB_SWAR_RATE4 4e-3  // ... when the caller's text histogram shows at most 4 byte values (sigma <= 4: 1 GiB m = 5, 6 SWAR
+                           // 0.29-0.31 ms vs WIN4 0.44; sigma = 8 keeps WIN4 / ALIGNED at 0.20-0.23)
+#endif
 #ifndef MB_ALIGNED2_RATE
 #define MB_ALIGNED2_RATE 4e-3
 #endif
@@ -342,7 +346,15 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       best_win4(pat, m, pr, &r);
     else
       best_aligned(pat, m, pr, 1, &r);
-    if (r > MB_SWAR_RATE) fam = MB_FAM_SWAR;
+    // byte values carrying more than 1% of the text -- only with the caller's text
+    // histogram: a 5-byte pattern cannot tell a 4-letter text from a 16-letter one
+    // (half of the 5-byte patterns over 16 letters hold <= 4 distinct bytes)
+    int nsym = 256;
+    if (hist) {
+      nsym = 0;
+      for (int c = 0; c < 256; c++) nsym += pr[c] > 0.01;
+    }
+    if (r > MB_SWAR_RATE || (nsym <= 4 && r > MB_SWAR_RATE4)) fam = MB_FAM_SWAR;
   }
   if (auto_long && fam == MB_FAM_ALIGNED) {
     // ALIGNED tests 4 grams of one 7-byte window per word; WIN4 one gram at
@@ -404,13 +416,13 @@ int build_plan(const uint8_t* pat, int64_t m, const mb_plan_opts* opts, PlanHost
       busy = g * 16.0 / gram_S > MB_GRAM_MAX_RATE;  // (sigma = 2, m = 16..22: 0.40 ms; quieter variants run at 0.17-0.20)
     }
     if (busy) {
-      // measured on 1 GiB texts (profiles/r2/k2_*): one plane (binary texts) wins from
-      // m = 7 (0.47 vs 0.51 ms; m = 8: 0.38 vs 0.46; m = 12..22: 0.24-0.28 vs 0.40-0.44);
-      // two planes (sigma 3..4) at m = 5 (0.36 vs 0.47) and narrowly from m = 7
-      // (0.27-0.29 vs 0.28-0.30), not at m = 6 (exact SWAR 0.29 vs 0.31)
+      // measured on 1 GiB texts (profiles/r2/k2_vs_swar_m5_8.json, after the SWAR flag
+      // gather): K2 wins from m = 8 -- sigma = 2: 0.379 vs SWAR 0.400 ms (m = 7: 0.479 vs
+      // 0.426), sigma = 4: 0.283 vs 0.300 (m = 5: 0.366 vs 0.306, m = 7: 0.291 vs 0.294);
+      // m = 12..22 over binary texts 0.24-0.28 vs 0.40-0.44 for two-word ALIGNED
       int bits[2];
       const int np = plane_count(pr);
-      const bool len_ok = np == 1 ? m >= 7 : (m == 5 || m >= 7);
+      const bool len_ok = m >= 8;
       if (len_ok && choose_planes(pat, m, pr, np, bits) <= MB_K2_MAX_CAND) fam = MB_FAM_SHIFTOR;
     }
   }

@@ -133,8 +133,8 @@ def test_plan_info_families():
         assert engine.Plan(b"\x05" * (m - 1) + b"\x07").info().family == "win4", m
         assert engine.Plan(b"\x07" + b"\x05" * (m - 1)).info().family == "win4", m
     assert engine.Plan(b"a" * 100).info().periodic
-    # small alphabets: exact SWAR at m = 5, 6 instead of a busy anchor filter, K2 from m = 7
-    for m, fam in ((5, "swar"), (6, "swar"), (7, "shiftor"), (8, "shiftor")):
+    # small alphabets: exact SWAR at m = 5..7 instead of a busy anchor filter, K2 from m = 8
+    for m, fam in ((5, "swar"), (6, "swar"), (7, "swar"), (8, "shiftor")):
         assert engine.Plan(bytes(rng0.integers(0, 2, m, dtype=np.uint8))).info().family == fam, m
     assert engine.Plan(bytes(range(40, 48))).info().family == "aligned"
     # sampled (K3) only for periods >= 294: a 256 KiB unit's occurrences fit its list
@@ -158,7 +158,7 @@ def test_plan_info_families():
     assert engine.Plan(long_random, family="aligned").info().family == "aligned"
     with pytest.raises(ValueError):
         engine.Plan(b"a" * 1024, family="sampled")
-    # K2 (bit-plane Shift-And): auto for binary texts at 7 <= m <= 22 and 4-letter ones at m = 5, 7..14,
+    # K2 (bit-plane Shift-And): auto for binary texts at 8 <= m <= 22 and 3-4-letter ones at 8 <= m <= 14,
     # where the word filters are busy; longer patterns take the strided gram filter
     assert engine.Plan(bytes(rng.integers(0, 4, 40, dtype=np.uint8))).info().family == "gram"
     assert engine.Plan(bytes([0, 1, 1, 0, 1, 0, 0, 0, 1, 1, 1, 0])).info().family == "shiftor"

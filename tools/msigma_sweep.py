@@ -32,6 +32,7 @@ ap.add_argument("--check", action="store_true")
 ap.add_argument("--sigmas", default="2,4,16,64,256")
 ap.add_argument("--lengths", default="")
 ap.add_argument("--family", default="auto")
+ap.add_argument("--no-hist", action="store_true", help="plan without the text's byte histogram (K0)")
 args = ap.parse_args()
 
 n = int(args.gib * (1 << 30))
@@ -44,11 +45,14 @@ for sigma in [int(x) for x in args.sigmas.split(",")]:
     d = torch.randint(0, sigma, (n,), dtype=torch.uint8, device="cuda", generator=g)
     h = d.cpu().numpy() if args.check else None
     rng = np.random.default_rng(sigma)
+    # the text's byte histogram (K0 on the device) goes to the planner, as the reference's
+    # select(pattern, text) sees the text's alphabet (registry.py:209-222)
+    hist = None if args.no_hist else engine.histogram(d).cpu().numpy()
     for m in lengths:
         off = int(rng.integers(0, n - m))
         p = d[off : off + m].cpu().numpy().tobytes()
         try:
-            pl = engine.Plan(p, args.family)
+            pl = engine.Plan(p, args.family, hist=hist)
         except ValueError:
             continue
         for _ in range(2):
