@@ -425,9 +425,13 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
         const uint32_t xa = cur.xa, xb = cur.xb;
         const uint32_t pc = __popc(xa) + __popc(xb);
         // starts of runs of ones (bit b set, bit b - 1 clear; the previous lane's top bit carries in)
-        const uint32_t prev_top = __shfl_up_sync(0xffffffffu, xb, 1) >> 31;
-        const uint32_t sa = xa & ~((xa << 1) | (lane ? prev_top : 0u));
-        const uint32_t sb2 = xb & ~((xb << 1) | (xa >> 31));
+        const bool try_runs = c >= 32u * 16u;  // (a run table pays from 32 matches per run: not below 512)
+        uint32_t sa = 0, sb2 = 0;
+        if (try_runs) {
+          const uint32_t prev_top = __shfl_up_sync(0xffffffffu, xb, 1) >> 31;
+          sa = xa & ~((xa << 1) | (lane ? prev_top : 0u));
+          sb2 = xb & ~((xb << 1) | (xa >> 31));
+        }
         const uint32_t nr = __popc(sa) + __popc(sb2);
         uint32_t inc = pc | (nr << 16);  // both prefixes in one scan (sum pc <= 2048, sum nr <= 1024)
 #pragma unroll
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
         // (o + omis + i) & 31; aligned index j = i + head
         const uint32_t head = (uint32_t)((o + omis) & 31);
         const uint32_t iend = head + lim;
-        if (R <= (uint32_t)EXP_RUNS && c >= 32u * R) {  // few LONG runs (a row per run at least): c^m with short m
+        if (try_runs && R <= (uint32_t)EXP_RUNS && c >= 32u * R) {  // few LONG runs (a row per run at least): c^m with short m
                                                           // over random text has dozens of 1-2 match runs -- staged below
           // ---- run-structured (c^m over a text of mostly c, config 5): a table of
           // (first position, output rank) per run; a row inside one run is
@@ -526,10 +530,20 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const ScanParams
             }
           }
           __syncwarp();
+          if (nocarry) {  // (decided once per segment; pointers advanced by hand)
+            const uint32_t splo = (uint32_t)sp, sphi = (uint32_t)((uint64_t)sp >> 32);
+            uint32_t j = lane;
+            if (j >= head && j < iend) *reinterpret_cast<uint2*>(d0 + (j - head)) = make_uint2(splo + sb[j - head], sphi);
+            j += 32;
+            uint2* p = reinterpret_cast<uint2*>(d0 + ((int64_t)j - (int64_t)head));
+            const uint16_t* q = sb + ((int32_t)j - (int32_t)head);
 #pragma unroll 4
-          for (uint32_t j = lane; j < iend; j += 32) {
-            const uint32_t i = j - head;  // wraps below 0 for the first row's leading lanes
-            if (i < lim) exp_store(d0 + i, sp, sb[i], nocarry);
+            for (; j < iend; j += 32, p += 32, q += 32) *p = make_uint2(splo + *q, sphi);
+          } else {
+            for (uint32_t j = lane; j < iend; j += 32) {
+              const uint32_t i = j - head;  // wraps below 0 for the first row's leading lanes
+              if (i < lim) d0[i] = sp + sb[i];
+            }
           }
         }
         __syncwarp();  // the next segment overwrites sb / the run table
