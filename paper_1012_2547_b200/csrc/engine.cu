@@ -1009,7 +1009,11 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
     P.dense_slot = (P.epoch & 1) ? TICKET_DENSE_ODD : TICKET_DENSE;
     // chunk = NT * scan_per counts; the largest chunks run as 256-thread CTAs
     // x 64 counts (4 CTAs per SM, so 16 GiB's 512 chunks stay co-resident)
-    P.offs_resident = nchunks <= (int64_t)c->nsm * (scan_per == 32 ? 4 : 2) ? 1 : 0;  // __launch_bounds__
+    // co-resident grids of more than 32 chunks: grid barrier (a cooperative launch, which
+    // cannot start before its predecessor has drained: ~3 us after the scan's last CTA).
+    // Up to 32 chunks (single searches up to ~256 MiB) the ticket-ordered look-back is one
+    // round trip and the kernel stays a plain dependent launch, resident while the scan drains
+    P.offs_resident = (nchunks > 32 && nchunks <= (int64_t)c->nsm * (scan_per == 32 ? 4 : 2)) ? 1 : 0;  // __launch_bounds__
     const bool coop = P.offs_resident != 0;  // grid barrier: cooperative launch (see launch_ex)
     if (scan_per == 32)
       CUDA_TRY(launch_pdl(offsets_kernel<64, NT / 2>, (int)nchunks, NT / 2, st, P, coop));
