@@ -87,13 +87,37 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
     const int64_t r = rem + q;
     return r < seg_per_pat ? rb0 + r : rb1 + (r - seg_per_pat);
   };
+  if (!P.rep) {
+    // no duplicates: the chunk's counts are one contiguous run -- read it with
+    // coalesced 16-byte loads (granule g = q8 * OT + tid; a thread reading its
+    // own PER counts touches 32 lines per load, half of every sector unused:
+    // 30 us per pass over config 3's 16.4 M counts) and hand every granule to
+    // its owner thread through s_cnt, in the layout the counts keep below
+    constexpr int GPT = PER / 8;  // granules per thread
+    const uint4* c16 = reinterpret_cast<const uint4*>(P.counts + base);
 #pragma unroll
-  for (int q8 = 0; q8 < PER / 8; q8++) {
-    // counts are allocated to a whole number of chunks; past the last pattern
-    // the slots are read unmapped and zeroed below
-    const int64_t t0 = base + (int64_t)tid * PER + 8 * q8;
-    const uint4 x = *reinterpret_cast<const uint4*>(P.counts + (t0 < nseg ? dseg(8 * q8) : t0));
-    v2[4 * q8] = x.x, v2[4 * q8 + 1] = x.y, v2[4 * q8 + 2] = x.z, v2[4 * q8 + 3] = x.w;
+    for (int q8 = 0; q8 < GPT; q8++) {
+      const int g = q8 * OT + tid;
+      const uint4 x = c16[g];  // (counts are allocated to a whole number of chunks)
+      const int o = g / GPT, q = g % GPT;
+      s_cnt[(4 * q + 0) * OT + o] = x.x;
+      s_cnt[(4 * q + 1) * OT + o] = x.y;
+      s_cnt[(4 * q + 2) * OT + o] = x.z;
+      s_cnt[(4 * q + 3) * OT + o] = x.w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < PER / 2; h++) v2[h] = s_cnt[h * OT + tid];
+    __syncthreads();  // the rows are rewritten (last chunk: zeroed tail) below
+  } else {
+#pragma unroll
+    for (int q8 = 0; q8 < PER / 8; q8++) {
+      // counts are allocated to a whole number of chunks; past the last pattern
+      // the slots are read unmapped and zeroed below
+      const int64_t t0 = base + (int64_t)tid * PER + 8 * q8;
+      const uint4 x = *reinterpret_cast<const uint4*>(P.counts + (t0 < nseg ? dseg(8 * q8) : t0));
+      v2[4 * q8] = x.x, v2[4 * q8 + 1] = x.y, v2[4 * q8 + 2] = x.z, v2[4 * q8 + 3] = x.w;
+    }
   }
   if (base + (int64_t)OT * PER > nseg) {  // last chunk: zero the slots past the last segment
 #pragma unroll
