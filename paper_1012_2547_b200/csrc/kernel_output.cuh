@@ -124,22 +124,36 @@ __global__ void __launch_bounds__(OT, 1024 / OT) offsets_kernel(const ScanParams
     for (int q = 0; q < PER; q++)
       if (base + (int64_t)tid * PER + q >= nseg) v2[q >> 1] &= (q & 1) ? 0x0000FFFFu : 0xFFFF0000u;
   }
+  {
+    // both 16-bit halves of every word summed at once, in 4 independent
+    // accumulators (<= 16 counts of <= 2048 each: no carry between the halves)
+    uint32_t a4[4] = {0, 0, 0, 0};
 #pragma unroll
-  for (int h = 0; h < PER / 2; h++) tsum32 += (v2[h] & 0xFFFFu) + (v2[h] >> 16);
+    for (int h = 0; h < PER / 2; h++) a4[h & 3] += v2[h];
+#pragma unroll
+    for (int i = 0; i < 4; i++) tsum32 += (a4[i] & 0xFFFFu) + (a4[i] >> 16);
+  }
+  static_assert(PER / 2 / 4 * 2048 <= 65535, "packed count sums must not carry");
   const int64_t tsum = tsum32;
   // the first 8 list entries of this thread's first non-empty segment are
   // fetched now, so they arrive during the exclusive-offset computation
+  // (threads without matches -- nearly all of a sparse batch -- skip the search)
   int fq = -1;
+  if (tsum32) {
 #pragma unroll
-  for (int q = PER - 1; q >= 0; q--)
-    if ((v2[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) fq = q;
+    for (int h = PER / 2 - 1; h >= 0; h--)
+      if (v2[h]) fq = 2 * h + ((v2[h] & 0xFFFFu) ? 0 : 1);
+  }
   uint4 pre = make_uint4(0, 0, 0, 0);
   if (fq >= 0 && P.out) pre = *reinterpret_cast<const uint4*>(P.lists + dseg(fq) * LIST_CAP);
   // the counts go through shared memory (transposed: conflict-free) so the
   // output loop below is not unrolled, and they stop occupying registers
-  // across the prefix computation (the 64-count variant would spill)
+  // across the prefix computation (the 64-count variant would spill); the
+  // coalesced path has them there already (unless the last chunk zeroed a tail)
+  if (P.rep || base + (int64_t)OT * PER > nseg) {
 #pragma unroll
-  for (int h = 0; h < PER / 2; h++) s_cnt[h * OT + tid] = v2[h];
+    for (int h = 0; h < PER / 2; h++) s_cnt[h * OT + tid] = v2[h];
+  }
   int64_t inc = tsum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
