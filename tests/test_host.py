@@ -180,6 +180,24 @@ def test_plan_info_families():
         engine.Plan(b"x" * 65, family="shiftor")
 
 
+def test_text_histogram_steers_small_alphabet_plans():
+    """With the text's byte histogram (mb_plan_opts.hist, K0 on the device) the
+    planner knows a 4-letter text from a 16-letter one: exact SWAR at m = 5..7
+    and K2 from m = 8 over <= 4 letters, WIN4 / one-word ALIGNED over 16."""
+    rng = np.random.default_rng(11)
+    h4 = np.zeros(256, dtype=np.int64)
+    h4[:4] = 1 << 20
+    h16 = np.zeros(256, dtype=np.int64)
+    h16[:16] = 1 << 18
+    for m, fam4, fam16 in ((5, "swar", "win4"), (6, "swar", "win4"), (7, "swar", "aligned"), (8, "shiftor", "aligned"),
+                           (12, "shiftor", "aligned")):
+        p = bytes(rng.permutation(4)[np.arange(m) % 4].astype(np.uint8))  # 4 distinct letters, no short period
+        p = p[:-1] + bytes([p[-1] ^ 1])
+        assert engine.Plan(p, hist=h4).info().family == fam4, (m, "sigma 4")
+        assert engine.Plan(p, hist=h16).info().family == fam16, (m, "sigma 16")
+    assert engine.Plan(bytes([0, 1, 2, 3, 1, 0, 2, 2, 3, 1, 0, 3]), hist=h4).info().words == 2  # K2: two planes over 4 letters
+
+
 def test_aligned_anchor_words():
     """The ALIGNED family widens its anchor to 2 words (11-byte window) over
     small alphabets (auto plans take K2 or the strided gram filter there);
