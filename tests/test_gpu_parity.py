@@ -230,6 +230,44 @@ def test_shiftor_auto_small_alphabets(cuda, sigma):
         assert (8, "shiftor") in fams, fams
 
 
+@pytest.mark.parametrize("m", [7, 9, 15, 16, 33, 64, 200, 1000])
+def test_run_filter_edges_and_capacity(cuda, m):
+    """c^m (the exact run filter, m >= 7) on a text larger than one resident
+    wave (the 3-launch pipeline: run-table and staged expansion), runs of c
+    ending and starting at tile and segment boundaries and at the text edges,
+    every pointer misalignment, and an output buffer cut inside a dense
+    segment (prefix of the list, full count)."""
+    n = 12 << 20  # > the fused single-wave limit
+    t = np.zeros(n, dtype=np.uint8) + ord("q")
+    rng = np.random.default_rng(60 + m)
+    t[rng.choice(n, n // 3000, replace=False)] = ord("z")  # long runs broken by rare bytes
+    for b in (ENGINE_TILE, 7 * ENGINE_TILE, 5 * SEG, 100 * SEG + 3):
+        for d in (-m - 1, -m, -m + 1, -1, 0, 1):
+            t[b + d] = ord("z")
+    t[:3] = ord("z")
+    t[n - m - 2] = ord("z")
+    t[200 * SEG : 260 * SEG : 2] = ord("z")  # every other byte: no match, dozens of 1-byte runs per segment
+    t[300 * SEG : 330 * SEG] = np.frombuffer(b"qqqz" * (30 * SEG // 4), dtype=np.uint8)  # runs of 3
+    p = b"q" * m
+    assert engine.Plan(p).info().period == 1
+    base = torch.from_numpy(np.concatenate([np.zeros(16, np.uint8), t])).cuda()
+    host = t.tobytes()
+    want = oracle.search(p, host, threads=4)
+    for off in (0, 1, 7, 15):
+        view = base[16 - off : 16 - off + n + off][off:] if off else base[16 : 16 + n]
+        got = engine.find(engine.Plan(p), view).cpu().numpy()
+        assert np.array_equal(got, want), (m, off, got.size, want.size)
+    # capacity cut inside a dense segment
+    cap = int(want.size // 2 + 777)
+    out = torch.full((cap + 8,), -1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    engine.find_into(engine.Plan(p), base[16 : 16 + n], out[:cap], cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == want.size
+    assert np.array_equal(out[:cap].cpu().numpy(), want[:cap])
+    assert (out[cap:] == -1).all(), "wrote past the capacity"
+
+
 @pytest.mark.parametrize("tiles", [1, 2, 150, 295, 296, 297, 300, 450])
 def test_single_wave_fused_boundary(cuda, tiles):
     """Texts of up to one resident wave of tiles run as ONE fused launch (scan,
