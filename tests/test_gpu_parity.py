@@ -268,6 +268,32 @@ def test_run_filter_edges_and_capacity(cuda, m):
     assert (out[cap:] == -1).all(), "wrote past the capacity"
 
 
+@pytest.mark.parametrize("sigma", [2, 3, 4, 16, 256])
+def test_plans_with_text_histogram(cuda, sigma):
+    """Plans built with the text's byte histogram (K0 on the device, the text side
+    of the reference's select(pattern, text)): anchors, bit planes and families are
+    chosen from the true byte probabilities -- results equal the oracle for every
+    m, and the families are the small-alphabet ones where they should be."""
+    rng = np.random.default_rng(8100 + sigma)
+    n = 5 * ENGINE_TILE + 321
+    t = rand_bytes(rng, sigma, n)
+    d = torch.from_numpy(np.frombuffer(t, dtype=np.uint8).copy()).cuda()
+    hist = engine.histogram(d).cpu().numpy()
+    assert int(hist.sum()) == n and int((hist > 0).sum()) <= sigma
+    fams = {}
+    for m in (1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 15, 16, 23, 31, 40, 64, 65, 300):
+        off = int(rng.integers(0, n - m))
+        p = t[off : off + m]
+        pl = engine.Plan(p, hist=hist)
+        fams[m] = pl.info().family
+        got = engine.find(pl, d).cpu().numpy()
+        assert np.array_equal(got, oracle.search(p, t)), (sigma, m, fams[m])
+    if sigma == 4:
+        assert fams[5] == fams[6] == "swar", fams
+    if sigma == 256:
+        assert fams[5] == "win4" and fams[8] == "aligned", fams
+
+
 @pytest.mark.parametrize("tiles", [1, 2, 150, 295, 296, 297, 300, 450])
 def test_single_wave_fused_boundary(cuda, tiles):
     """Texts of up to one resident wave of tiles run as ONE fused launch (scan,
