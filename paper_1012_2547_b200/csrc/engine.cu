@@ -1448,8 +1448,10 @@ int mb_histogram(mb_ctx* c, const uint8_t* d_text, int64_t n, int64_t* d_hist, v
   if (dev != c->device) return fail(MB_EINVAL, "current CUDA device differs from the context's device");
   CUDA_TRY(cudaMemsetAsync(d_hist, 0, 256 * sizeof(int64_t), st));
   if (n <= 0) return MB_OK;
-  int64_t blocks = std::min<int64_t>((n + 4095) / 4096, (int64_t)c->nsm * 8);
-  hist_kernel<<<(int)blocks, 256, 0, st>>>(d_text, n, (unsigned long long*)d_hist);
+  // per-warp counters are 32-bit: a warp sees at most n / (warps in the grid) + 64 KiB bytes
+  int64_t blocks = std::min<int64_t>((n + 65535) / 65536, (int64_t)c->nsm * 8);
+  blocks = std::max<int64_t>(blocks, (n >> 31) + 1);
+  hist_kernel<<<(int)blocks, HIST_WARPS * 32, 0, st>>>(d_text, n, (unsigned long long*)d_hist);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return MB_OK;

@@ -350,16 +350,50 @@ __global__ void fill_kernel(int64_t* dst, const int64_t* src, int n) {
   if (i < n) dst[i] = *src;
 }
 
-// K0: byte histogram (Text.alphabet_size, core.py:42-44)
-__global__ void hist_kernel(const uint8_t* t, int64_t n, unsigned long long* hist) {
-  __shared__ unsigned int h[256];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+// K0: byte histogram (Text.alphabet_size, core.py:42-44).  16-byte coalesced
+// loads (4 in flight per thread), one private 256-bin histogram per warp in
+// smem (a byte-per-load loop with one CTA-wide histogram ran at 2.0 TB/s,
+// bound by its load instructions), merged per CTA and added to the result.
+constexpr int HIST_WARPS = 8;
+__global__ void __launch_bounds__(HIST_WARPS * 32) hist_kernel(const uint8_t* t, int64_t n, unsigned long long* hist) {
+  __shared__ unsigned int h[HIST_WARPS][256];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < HIST_WARPS * 256; i += HIST_WARPS * 32) (&h[0][0])[i] = 0;
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(&h[t[i]], 1u);
+  unsigned int* hw = h[warp];
+  auto add4 = [&](uint32_t w) {
+    atomicAdd(&hw[w & 0xFFu], 1u);
+    atomicAdd(&hw[(w >> 8) & 0xFFu], 1u);
+    atomicAdd(&hw[(w >> 16) & 0xFFu], 1u);
+    atomicAdd(&hw[w >> 24], 1u);
+  };
+  // head bytes up to the first 16-byte boundary, 16-byte body, tail bytes
+  const int64_t mis = (int64_t)((16 - ((uintptr_t)t & 15)) & 15);
+  const int64_t head = n < mis ? n : mis;
+  const uint4* body = reinterpret_cast<const uint4*>(t + head);
+  const int64_t nv = (n - head) / 16;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid, stride = (int64_t)gridDim.x * blockDim.x;
+  if (gtid < head) atomicAdd(&hw[t[gtid]], 1u);
+  for (int64_t i = head + 16 * nv + gtid; i < n; i += stride) atomicAdd(&hw[t[i]], 1u);
+  int64_t i = gtid;
+  for (; i + 3 * stride < nv; i += 4 * stride) {
+    const uint4 a = body[i], b = body[i + stride], c = body[i + 2 * stride], d = body[i + 3 * stride];
+    add4(a.x), add4(a.y), add4(a.z), add4(a.w);
+    add4(b.x), add4(b.y), add4(b.z), add4(b.w);
+    add4(c.x), add4(c.y), add4(c.z), add4(c.w);
+    add4(d.x), add4(d.y), add4(d.z), add4(d.w);
+  }
+  for (; i < nv; i += stride) {
+    const uint4 a = body[i];
+    add4(a.x), add4(a.y), add4(a.z), add4(a.w);
+  }
   __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += blockDim.x)
-    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+  for (int bin = tid; bin < 256; bin += HIST_WARPS * 32) {
+    unsigned int v = 0;
+#pragma unroll
+    for (int w = 0; w < HIST_WARPS; w++) v += h[w][bin];
+    if (v) atomicAdd(&hist[bin], (unsigned long long)v);
+  }
 }
 
 
