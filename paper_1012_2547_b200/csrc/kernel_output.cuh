@@ -666,11 +666,14 @@ __global__ void __launch_bounds__(512) replicate_kernel(const ScanParams P) {
     if (sz[q] >= 0) s_pref[rank] = pref, s_dup[rank] = 4 * tid + q, pref += sz[q], rank++;
   if (tid == 0) s_pref[nd_all] = sum_all;
   __syncthreads();
-  // 2. 256-position chunks of the concatenated ranges, grid-stride by warp
-  const int64_t nchunks = (sum_all + 255) / 256;
+  // 2. 1024-position chunks of the concatenated ranges, grid-stride by warp
+  // (one smem search per chunk), copied in pieces of 8 rows of 32 positions
+  // aligned to the destination's 256-byte lines
+  const uint32_t omis = (uint32_t)(((uintptr_t)P.out >> 3) & 31u);
+  const int64_t nchunks = (sum_all + 1023) / 1024;
   for (int64_t c = (int64_t)blockIdx.x * 16 + warp; c < nchunks; c += (int64_t)gridDim.x * 16) {
-    int64_t e = c * 256;
-    const int64_t e_end = min(e + 256, sum_all);
+    int64_t e = c * 1024;
+    const int64_t e_end = min(e + 1024, sum_all);
     int lo = 0, hi = nd_all - 1;  // last duplicate whose range starts at or before e
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -680,22 +683,28 @@ __global__ void __launch_bounds__(512) replicate_kernel(const ScanParams P) {
       const int k = s_dup[d];
       const int r = P.rep[k] & ~REP_COPY;
       const int64_t run_end = min(e_end, s_pref[d + 1]);
+      const int64_t doff = start(k) - s_pref[d];  // destination index of concatenated index 0 of this run
       const int64_t* src = P.out + start(r) - s_pref[d];
-      int64_t* dst = P.out + start(k) - s_pref[d];
-      // all of a lane's loads first (src and dst share P.out, so the compiler
-      // would otherwise keep each load behind the previous store)
-      int64_t v[8];
+      int64_t* dst = P.out + doff;
+      while (e < run_end) {
+        // rows start on a destination line: back up to it, mask the lanes before e
+        const int64_t e0 = e - (int64_t)((uint32_t)(e + doff + omis) & 31u);
+        const int64_t piece_end = min(run_end, e0 + 256);
+        // all of a lane's loads first (src and dst share P.out, so the compiler
+        // would otherwise keep each load behind the previous store)
+        int64_t v[8];
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int64_t i = e + lane + 32 * j;
-        if (i < run_end) v[j] = src[i];
-      }
+        for (int j = 0; j < 8; j++) {
+          const int64_t i = e0 + lane + 32 * j;
+          if (i >= e && i < piece_end) v[j] = src[i];
+        }
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int64_t i = e + lane + 32 * j;
-        if (i < run_end) __stcs(dst + i, v[j]);
+        for (int j = 0; j < 8; j++) {
+          const int64_t i = e0 + lane + 32 * j;
+          if (i >= e && i < piece_end) __stcs(dst + i, v[j]);
+        }
+        e = piece_end;
       }
-      e = run_end;
     }
   }
 }
