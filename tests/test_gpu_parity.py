@@ -384,6 +384,17 @@ def test_histogram_alphabet(cuda):
     h = engine.histogram(t).cpu().numpy()
     assert np.array_equal(h, np.bincount(np.frombuffer(t, np.uint8), minlength=256))
     assert mb.Text(t).alphabet_size() == len(set(t))
+    # K0 reads 16-byte vectors: every pointer misalignment, lengths around the vector and
+    # block sizes, a text of one byte value (every lane on one bin), a multi-block text
+    base = torch.from_numpy(np.frombuffer(rand_bytes(rng, 256, (9 << 20) + 64), np.uint8).copy()).cuda()
+    hb = base.cpu().numpy()
+    for off in (0, 1, 7, 15):
+        for n in (0, 1, 15, 16, 17, 31, 4097, 65536 + 5, (9 << 20) + 3):
+            got = engine.histogram(base[off : off + n]).cpu().numpy()
+            assert np.array_equal(got, np.bincount(hb[off : off + n], minlength=256)), (off, n)
+    ones = torch.full((3 << 20,), 7, dtype=torch.uint8, device="cuda")
+    h1 = engine.histogram(ones[3:]).cpu().numpy()
+    assert h1[7] == (3 << 20) - 3 and h1.sum() == h1[7]
 
 
 def test_instrumented_text_rejected(cuda):
