@@ -1099,10 +1099,17 @@ static int run_search(mb_ctx* c, const PatDev* d_pats, const PatDev* h_pats, int
       M.nents = bp->chunks[ci].nent;
       M.kbase = k0;
       M.exact_m = (bp->kind == 2 && bp->exact) ? bp->q : 0;
+      M.exact_local = 0;
+      if (M.exact_m) {  // every pass pattern of this chunk at bitmap shift 0 (SWAR, K2, m = 4 windows at anchor 0)
+        M.exact_local = 1;
+        for (int k = k0; k < std::min(K, k0 + MP_CHUNK); k++)
+          if (!h_need[k] && (!h_rep || (h_rep[k] & ~REP_COPY) == k) && h_pats[k].delta != 0) M.exact_local = 0;
+      }
       M.ticket = c->ticket + TICKET_MP0 + (ci - chunk0);
       M.zero_n = k0 == 0 ? T + 2 : 0;  // the first launch's prologue (its grid is co-resident)
       auto smem_for = [&](int ns) {
-        return (size_t)SM_STAGES + (size_t)ns * M.stage_bytes + 8192 + 4 * bs_words + (size_t)4 * ent_words * M.nents;
+        return (size_t)SM_STAGES + (size_t)ns * M.stage_bytes + 8192 + 4 * bs_words + (size_t)4 * ent_words * M.nents +
+               (M.exact_local ? (size_t)NWARP * MP_CHUNK * 2 + 16 : 0);
       };
       // 3 stages, or for the aligned pass 2 where that keeps two CTAs per SM
       // (big tables / halos; measured 55 -> 40 us on config 3, m = 16).  The

@@ -250,6 +250,8 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
   uint32_t* bstart = bloom + 2048;
   uint4* ents = reinterpret_cast<uint4*>(bstart + (((1 << P.B) + 1 + 3) & ~3));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // exact_local: this warp's per-pattern match counts of its current segment (packed uint16 pairs)
+  uint32_t* wc = reinterpret_cast<uint32_t*>(ents + P.nents) + (warp < NWARP ? warp : 0) * (MP_CHUNK / 2);
   // barriers first: the producer starts the tile loads while the consumers
   // stage the tables (and run the search's prologue)
   if (tid == 0) {
@@ -264,6 +266,8 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
     for (int i = tid; i < 2048; i += NT) bloom[i] = P.bloom[i];
     for (int i = tid; i <= (1 << P.B); i += NT) bstart[i] = P.bstart[i];
     for (int i = tid; i < P.nents; i += NT) ents[i] = P.ents4[i];
+    if (P.exact_local)
+      for (int i = lane; i < MP_CHUNK / 2; i += 32) wc[i] = 0u;
     mp_prologue(P);
     consumer_sync();
   }
@@ -324,7 +328,23 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
           const int kl = (int)(en.z >> 16);
           if (P.exact_m) {  // the gram is the whole pattern: an occurrence, recorded at its family's bit
             const int64_t sp0 = x - P.off;
-            if (sp0 >= 0 && sp0 + P.exact_m <= P.n) mp_record(P, P.kbase + kl, x + (int64_t)(en.z & 0xFFFFu));
+            if (sp0 >= 0 && sp0 + P.exact_m <= P.n) {
+              if (P.exact_local) {
+                // bit = position: this warp's own segment of pattern kl -- the slot from
+                // the warp's smem counter (flushed to the global counts after the segment)
+                const unsigned int sh = 16u * (unsigned)(kl & 1);
+                const unsigned int old = (atomicAdd(&wc[kl >> 1], 1u << sh) >> sh) & 0xFFFFu;
+                if (old < (unsigned)LIST_CAP) {
+                  const int64_t g = ((int64_t)(P.kbase + kl) * P.ntiles + tau) * NWARP + warp;
+                  P.lists[g * LIST_CAP + old] = (uint16_t)(c + p);
+                } else {
+                  P.need[P.kbase + kl] = 1u;
+                  atomicExch(P.overflow, 1u);
+                }
+              } else {
+                mp_record(P, P.kbase + kl, x + (int64_t)(en.z & 0xFFFFu));
+              }
+            }
             continue;
           }
           const int a = (int)(en.z & 0xFFFFu);
@@ -340,6 +360,17 @@ __global__ void __launch_bounds__(NT + 32) mpb_scan_kernel(const MPParams P) {
       mp_verify_queued(P, cq, S, B0, lane);
     }
     __syncwarp();
+    if (P.exact_local) {  // the segment's counts: plain stores (this warp is their only writer), counters cleared
+      for (int i = lane; i < MP_CHUNK / 2; i += 32) {
+        const uint32_t v = wc[i];
+        if (v) {
+          wc[i] = 0u;
+          if (v & 0xFFFFu) P.counts[((int64_t)(P.kbase + 2 * i) * P.ntiles + tau) * NWARP + warp] = (uint16_t)(v & 0xFFFFu);
+          if (v >> 16) P.counts[((int64_t)(P.kbase + 2 * i + 1) * P.ntiles + tau) * NWARP + warp] = (uint16_t)(v >> 16);
+        }
+      }
+      __syncwarp();
+    }
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 }

@@ -139,6 +139,8 @@ struct MPParams {
   const uint4* ents4;      // byte-offset pass: {gram lo, gram hi, (batch index << 16) | a, 0} sorted by bucket
   int B, nents;
   int kbase;               // batch index of this chunk's first pattern
+  int exact_local;         // exact pass whose patterns all have bitmap shift 0: a hit lands in the segment of the warp
+                           // that found it -- counts and list slots per warp in smem (MP_CHUNK packed uint16), no global atomics
   int exact_m;             // byte-offset pass: every pattern has this length = the gram (0: verify); the entry's
                            // low 16 bits then hold the pattern's bitmap shift (delta) instead of an anchor
   const PatDev* pats;      // whole batch
