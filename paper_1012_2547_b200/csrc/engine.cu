@@ -731,15 +731,17 @@ static void plan_pass(const PatSrc* src, const PatDev* h_pats, int K, BatchPass*
     for (int i = 0; i < q; i++) r *= pr[g[i]];
     return r;
   };
-  // duplicates of patterns expected below 256 matches per 2 KiB segment are
+  // duplicates of patterns expected below 600 matches per 2 KiB segment are
   // copied from the representative's output (expansion there costs more
   // instructions per position than a copy); denser ones re-expand its
-  // segments (a copy would add the source reads to a write-bound stream)
+  // segments (a copy would add the source reads to a write-bound stream).
+  // (256 until replicate_kernel wrote destination-line-aligned rows; config 2
+  // sigma = 2, m = 2 -- 512 per segment -- copies at 0.857 ms vs 0.891 re-expanded)
   bp->dcopy.assign(K, 0);
   for (int k = 0; k < K; k++)
     if (rep[k] != k) {
       const PatBytes pb{src[k].bytes, (size_t)src[k].m};
-      bp->dcopy[k] = 2048.0 * gp(pb.data(), (int)std::min<size_t>(pb.size(), 32)) < 256.0 ? 1 : 0;
+      bp->dcopy[k] = 2048.0 * gp(pb.data(), (int)std::min<size_t>(pb.size(), 32)) < 600.0 ? 1 : 0;
     }
   if (K - bp->ndup < 8 || K > MP_CHUNK * MAX_MP_CHUNKS) return;
   // kind 1
